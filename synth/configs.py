@@ -1,0 +1,54 @@
+"""The five BASELINE.json configurations as plain data (no arithmetic of the method).
+
+Geometry ids (shared vocabulary with include/fdiga.h `FDIGA_GEOM_*`):
+  0 identity map on [0,1]^d
+  1 quarter annulus, radii (r0, r1) = geo_params[0:2]            (2D, "quarter of ring")
+  2 deformed cube x_k = xi_k + a*prod_l sin(pi xi_l), a = geo_params[0]   (3D, BASELINE.json configs[2])
+  3 thick quarter ring: annulus x height, (r0, r1, height) = geo_params[0:3]  (3D, BASELINE.json configs[4])
+"""
+from dataclasses import dataclass, field
+from typing import Tuple
+
+GEOM_IDENTITY = 0
+GEOM_ANNULUS = 1
+GEOM_DEFORMED_CUBE = 2
+GEOM_THICK_RING = 3
+
+
+@dataclass(frozen=True)
+class Config:
+    cfg: int
+    d: int
+    p: int
+    ne: int                  # elements per direction (uniform open knots)
+    geometry: int
+    geo_params: Tuple[float, ...] = field(default_factory=tuple)
+    note: str = ""
+
+    @property
+    def n(self) -> int:
+        # n = m - 2 with m = ne + p basis functions per direction
+        return self.ne + self.p - 2
+
+    @property
+    def N(self) -> int:
+        return self.n ** self.d
+
+
+CONFIGS = {
+    1: Config(1, 2, 2, 32, GEOM_IDENTITY, (), "2D p=2 32x32 identity; FD exact => GMRES 1 iteration"),
+    2: Config(2, 2, 3, 256, GEOM_ANNULUS, (1.0, 2.0), "2D p=3 256x256 quarter annulus r in [1,2]"),
+    3: Config(3, 3, 3, 64, GEOM_DEFORMED_CUBE, (0.1,), "3D p=3 64^3 deformed cube"),
+    5: Config(5, 3, 5, 128, GEOM_THICK_RING, (1.0, 2.0, 1.0), "3D p=5 128^3 thick quarter ring"),
+}
+
+# cfg4 is the isolated FD-apply sweep: d=3, n in {128, 256, 512}, random factors.
+FD_SWEEP_N = (128, 256, 512)
+
+
+def get_config(cfg: int) -> Config:
+    return CONFIGS[cfg]
+
+
+def n_dofs(ne: int, p: int) -> int:
+    return ne + p - 2
