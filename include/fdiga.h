@@ -1,0 +1,175 @@
+/*
+ * fdiga.h — C ABI of libfdiga.so: the B200 (sm_100a) hot path of the nonsymmetric
+ * Fast-Diagonalization (FD) preconditioner inside restarted GMRES for isogeometric
+ * collocation of the Poisson problem (M. Tani, arXiv:1705.04384).
+ *
+ * Citations "P:<line>" refer to the paper's text, "S:<line>" to SPEC.md.
+ *
+ * Conventions shared by every entry point
+ *   - Return value: 0 (FDIGA_OK) or a negative fdiga_status.  No exception crosses the ABI.
+ *     A human-readable message for the last failure on the calling thread is returned by
+ *     fdiga_last_error().
+ *   - Vectors of the discrete problem are FP64, contiguous, in the flattened order of P:159:
+ *     i = i_1 + n_1 (i_2 + n_2 i_3) (0-based), i.e. an array X[i_d]...[i_1] with i_1 fastest.
+ *     On nranks > 1 a vector argument holds only this rank's slab of the last index
+ *     i_d in [begin, end) (fdiga_slab).
+ *   - Matrices passed from the host are row-major FP64, copied before the call returns
+ *     (the caller keeps ownership).  Handles own all device memory they allocate.
+ *   - Device vector arguments are caller-owned device pointers (e.g. torch data_ptr()).
+ *   - Stream semantics: fd_apply and stencil_matvec are asynchronous on the context's stream;
+ *     fd_setup*, colloc_assemble, stencil_create and gmres_solve synchronise before returning.
+ *   - Multi-rank: every call is collective; all ranks call it in the same order with the
+ *     same global arguments.
+ */
+#ifndef FDIGA_H
+#define FDIGA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FDIGA_OK = 0,
+  FDIGA_ERR_INVALID_ARG = -1,
+  FDIGA_ERR_CUDA = -2,
+  FDIGA_ERR_CUSOLVER = -3,
+  FDIGA_ERR_NCCL = -4,
+  FDIGA_ERR_COMPLEX_SPECTRUM = -5, /* complex eigenvalues and opts->allow_complex_pairs == 0 */
+  FDIGA_ERR_ILL_CONDITIONED = -6,  /* cond_1(U_l) > opts->cond_max (Remark 1) */
+  FDIGA_ERR_SINGULAR = -7,         /* min |Lambda| <= 1e3 eps max |Lambda| */
+  FDIGA_ERR_NOT_CONVERGED = -8,    /* gmres_solve hit max_iters; report filled, x = last iterate */
+  FDIGA_ERR_BREAKDOWN = -9,        /* NaN/Inf met inside gmres_solve */
+  FDIGA_ERR_NOT_SUPPORTED = -10,
+  FDIGA_ERR_OOM = -11
+} fdiga_status;
+
+/* Geometry ids for colloc_assemble (analytic maps of BASELINE.json's configs). */
+enum {
+  FDIGA_GEOM_IDENTITY = 0,      /* F = id on [0,1]^d */
+  FDIGA_GEOM_ANNULUS = 1,       /* 2D quarter annulus, geo_params = {r0, r1} */
+  FDIGA_GEOM_DEFORMED_CUBE = 2, /* 3D x_k = xi_k + a prod_l sin(pi xi_l), geo_params = {a} */
+  FDIGA_GEOM_THICK_RING = 3     /* 3D quarter annulus x [0,h], geo_params = {r0, r1, h} */
+};
+
+typedef struct fdiga_ctx fdiga_ctx;
+typedef struct fd_plan fd_plan;
+typedef struct fdiga_stencil fdiga_stencil;
+
+/* ---------------------------------------------------------------- context ---- */
+
+/* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t to run on (caller-owned,
+ * must outlive the context), or NULL for the legacy default stream.  nranks/rank/nccl_unique_id: the process group
+ * (nccl_unique_id = 128-byte ncclUniqueId, NULL iff nranks == 1). */
+int fdiga_ctx_create(int device, void* cuda_stream, int nranks, int rank, const void* nccl_unique_id,
+                     fdiga_ctx** out);
+int fdiga_ctx_destroy(fdiga_ctx* ctx); /* NULL -> no-op */
+/* This rank's slab [begin, end) of the last tensor index for a last-axis length n_last
+ * (balanced: the first n_last % nranks ranks own one extra plane). */
+int fdiga_slab(const fdiga_ctx* ctx, int64_t n_last, int64_t* begin, int64_t* end);
+/* Fill a 128-byte buffer with a fresh ncclUniqueId (call on rank 0, broadcast it). */
+int fdiga_nccl_unique_id(void* out128);
+const char* fdiga_status_string(int status);
+const char* fdiga_last_error(void);
+
+/* ------------------------------------------------------ FD preconditioner ---- */
+
+typedef struct {
+  double tol_imag;         /* |Im lambda| <= tol_imag * rho(M^{-1}K) counts as real (default 1e-8) */
+  double cond_max;         /* reject cond_1(U_l) above this (default 1e8) */
+  int allow_complex_pairs; /* 1: keep complex pairs as real 2x2 blocks of D_l; 0: fail */
+} fd_setup_opts;
+
+/* Setup from the 1D pencils (eq:eigendecomposition):
+ *   M_l^{-1} K_l U_l = U_l D_l,  W_l := V_l^T = (M_l U_l)^{-1},  l = 1..d,
+ * with U_l columns of unit 2-norm and eigenvalues ascending.  d in {2,3};
+ * n[l] = size of direction l+1; M[l], K[l]: host row-major n[l] x n[l].  opts may be NULL.
+ * Computed with cuSOLVER (getrf/getrs, Xgeev) — one time, not on the hot path. */
+int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, const double* const* K,
+             const fd_setup_opts* opts, fd_plan** out);
+/* Setup from explicit real factors (host, row-major): U[l], W[l] = (M_l U_l)^{-1}, lam[l]. */
+int fd_setup_from_factors(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* U,
+                          const double* const* W, const double* const* lam, fd_plan** out);
+/* Setup from an eigenbasis: W_l = (M_l U_l)^{-1} computed on the device (M = NULL means M_l = I,
+ * i.e. W_l = U_l^{-1}: BASELINE.json configs[3] "U_k^{-1} computed exactly in setup"). */
+int fd_setup_from_eig(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* U,
+                      const double* const* lam, const double* const* M, fd_plan** out);
+/* Copy factors of direction l (0-based) to host buffers (any may be NULL).  lam_im holds the
+ * imaginary parts (+b/-b on the two members of a complex pair, else 0). */
+int fd_get_factors(const fd_plan* plan, int l, double* U, double* W, double* lam_re, double* lam_im);
+/* s = P^{-1} r by eq:FD2D / eq:FD3D:
+ *   s = (U_d (x)..(x) U_1) Lambda^{-1} (W_d (x)..(x) W_1) r,  Lambda = sum_l I(x)..D_l..(x)I.
+ * r, s: device, local slab, length N_local; s may alias r.  Asynchronous on the ctx stream. */
+int fd_apply(fd_plan* plan, const double* r, double* s);
+/* Same, with HOST buffers r, s (copied in and out inside the call; synchronises). */
+int fd_apply_host(fd_plan* plan, const double* r_host, double* s_host);
+/* Algorithmic flops of one apply: 4 N sum_l n_l (= 12 n^4 in 3D P:481, 8 n^3 in 2D P:464). */
+double fd_apply_flops(const fd_plan* plan);
+int fd_plan_destroy(fd_plan* plan);
+
+/* ----------------------------------------------------- collocation operator ---- */
+
+/* Stored collocation matrix A_C (eq:collocationsystem) in "tensor-window" form.
+ * Row i = (i_1..i_d) couples to the box of columns j_l in [start_l[i_l], start_l[i_l] + width_l[i_l]).
+ * values: for each row in flattened order, the w_d*..*w_1 values of its box, j_1 fastest;
+ * row offsets are implied by the prefix sums of the widths (no index arrays).
+ * start[l], width[l]: host int32 arrays of length n[l].  values: host or device
+ * (values_on_device = 1), copied either way.  The library may re-layout values internally. */
+int stencil_create(fdiga_ctx* ctx, int d, const int64_t* n, const int32_t* const* start,
+                   const int32_t* const* width, const double* values, int values_on_device,
+                   fdiga_stencil** out);
+/* Assemble A_C on the device for degree p, ne[l] uniform elements per direction, open knots
+ * (P:144-148), Greville collocation points, K = I, on geometry `geometry_id`
+ * with parameters geo_params (see FDIGA_GEOM_*).  Row i holds (L (B_j o F^{-1}))(F(tau_i)). */
+int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
+                    fdiga_stencil** out);
+/* y = A x.  x, y: device, length N (no aliasing).  Asynchronous on the ctx stream. */
+int stencil_matvec(fdiga_stencil* A, const double* x, double* y);
+/* Number of stored values and the 1D window tables (host copies; any pointer may be NULL). */
+int stencil_info(const fdiga_stencil* A, int64_t* nnz, int64_t* n_out, int32_t* start_l0, int32_t* width_l0);
+/* Copy the canonical (tensor-window, row-major box) values to a host buffer of length nnz. */
+int stencil_get_values(const fdiga_stencil* A, double* values_host);
+int stencil_destroy(fdiga_stencil* A);
+/* Univariate collocation factors of the same discretisation (host out, row-major n x n):
+ * M[i][j] = B_j(tau_i), K[i][j] = -B''_j(tau_i) (eq:univariatecolloc). */
+int colloc_1d_factors(int p, int64_t ne, double* M, double* K);
+
+/* -------------------------------------------------------------------- GMRES ---- */
+
+enum { FDIGA_ORTH_CGS_DGKS = 0, FDIGA_ORTH_CGS2 = 1 };
+
+typedef struct {
+  int m;             /* restart length (default 30) */
+  double rtol;       /* stop when ||b - A x|| <= rtol ||b|| (default 1e-8) */
+  int max_iters;     /* Arnoldi steps over all cycles (default 1000) */
+  int orth;          /* FDIGA_ORTH_* (default CGS with DGKS re-orthogonalisation) */
+  int use_x0;        /* 1: x holds the initial guess; 0: x0 = 0 */
+} gmres_opts;
+
+typedef struct {
+  int iters;              /* Arnoldi steps (one P^{-1} apply + one matvec each) */
+  int restarts;           /* cycles started */
+  int converged;
+  int reorth;             /* DGKS second passes taken */
+  double rel_res_true;    /* ||b - A x|| / ||b|| at return */
+  double rel_res_implicit;/* |g_{j+1}| / ||b|| of the last step */
+  double t_total_ms;
+  double* history;        /* optional (caller-owned, length history_cap): implicit rel. residual per step */
+  int history_cap;
+} gmres_report;
+
+/* Right-preconditioned restarted GMRES(m) (Saad & Schultz 1986):
+ * solve A x = b with A P^{-1} y = b, x = P^{-1} y.  P == NULL: unpreconditioned.
+ * b, x: device, local slab.  opts/report may be NULL (defaults / no report).  Synchronises. */
+int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const double* b, double* x,
+                const gmres_opts* opts, gmres_report* report);
+
+/* ------------------------------------------------------------ instrumentation ---- */
+/* Number of kernels this library launched since the context was created (all entry points). */
+int64_t fdiga_kernel_launches(const fdiga_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDIGA_H */

@@ -1,0 +1,12 @@
+"""paper_1705_04384_b200 — B200-native FD-preconditioned GMRES for nonsymmetric IGA collocation.
+
+The hot path (FD apply, stored-operator matvec, Arnoldi kernels) lives in libfdiga.so
+(csrc/, C ABI in include/fdiga.h).  This package is its thin ctypes binding; it never falls back
+to a CPU implementation: importing the API without the built library raises ImportError.
+"""
+from ._lib import LIB_PATH, FdigaError, load  # noqa: F401
+from .api import (ORTH_CGS2, ORTH_CGS_DGKS, Context, FDPlan, Stencil, colloc_1d_factors,  # noqa: F401
+                  colloc_assemble, fd_apply, fd_apply_host, fd_setup, fd_setup_from_eig,
+                  fd_setup_from_factors, gmres_solve, stencil_create, stencil_matvec)
+
+GEOM_IDENTITY, GEOM_ANNULUS, GEOM_DEFORMED_CUBE, GEOM_THICK_RING = 0, 1, 2, 3

@@ -1,0 +1,262 @@
+"""Thin Python binding over libfdiga.so (include/fdiga.h), same names as the C ABI.
+
+Marshalling only: host matrices come in as numpy float64 arrays (copied by the library), device
+vectors as torch float64 CUDA tensors (their data_ptr is passed through), and every step of the
+hot path runs in the library's kernels.  torch provides device memory and streams only.
+"""
+import ctypes as C
+
+import numpy as np
+
+from ._lib import (FdSetupOpts, GmresOpts, GmresReport, c_double_p, c_int32_p, check, load)
+
+ORTH_CGS_DGKS = 0
+ORTH_CGS2 = 1
+
+
+def _dptr(a):
+    return a.ctypes.data_as(c_double_p)
+
+
+def _host_f64(a, shape=None):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if shape is not None and a.shape != tuple(shape):
+        raise ValueError(f"expected shape {shape}, got {a.shape}")
+    return a
+
+
+def _devptr(t, n=None):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise TypeError("expected a contiguous float64 CUDA tensor")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"expected {n} elements, got {t.numel()}")
+    return C.c_void_p(t.data_ptr())
+
+
+class Context:
+    """fdiga_ctx: a device, a stream and (optionally) an NCCL process group."""
+
+    def __init__(self, device=0, stream=None, nranks=1, rank=0, nccl_unique_id=None):
+        lib = load()
+        self._lib = lib
+        h = C.c_void_p()
+        s = C.c_void_p(stream) if stream is not None else None
+        uid = C.c_char_p(bytes(nccl_unique_id)) if nccl_unique_id is not None else None
+        check(lib.fdiga_ctx_create(int(device), s, int(nranks), int(rank), uid, C.byref(h)), "fdiga_ctx_create")
+        self.handle = h
+        self.device = device
+
+    def slab(self, n_last):
+        b, e = C.c_int64(), C.c_int64()
+        check(self._lib.fdiga_slab(self.handle, int(n_last), C.byref(b), C.byref(e)), "fdiga_slab")
+        return b.value, e.value
+
+    def kernel_launches(self):
+        return int(self._lib.fdiga_kernel_launches(self.handle))
+
+    def close(self):
+        if self.handle:
+            self._lib.fdiga_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class FDPlan:
+    """fd_plan: per-direction factors (U_l, W_l = (M_l U_l)^{-1}, lam_l) resident on the device."""
+
+    def __init__(self, ctx, handle, ns):
+        self.ctx, self.handle, self.n = ctx, handle, list(ns)
+        self.N = int(np.prod(self.n))
+
+    def factors(self, l):
+        n = self.n[l]
+        U, W = np.empty((n, n)), np.empty((n, n))
+        lr, li = np.empty(n), np.empty(n)
+        check(self.ctx._lib.fd_get_factors(self.handle, l, _dptr(U), _dptr(W), _dptr(lr), _dptr(li)),
+              "fd_get_factors")
+        return U, W, lr, li
+
+    def flops(self):
+        return float(self.ctx._lib.fd_apply_flops(self.handle))
+
+    def close(self):
+        if self.handle:
+            self.ctx._lib.fd_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Stencil:
+    """fdiga_stencil: the stored collocation operator A_C."""
+
+    def __init__(self, ctx, handle):
+        self.ctx, self.handle = ctx, handle
+        nnz = C.c_int64()
+        n = (C.c_int64 * 3)(1, 1, 1)
+        check(ctx._lib.stencil_info(handle, C.byref(nnz), n, None, None), "stencil_info")
+        self.nnz = nnz.value
+        self.n = [n[0], n[1], n[2]]
+        self.N = n[0] * n[1] * n[2]
+
+    def windows(self):
+        """(start, width) of the column windows of direction 1 (int32 arrays of length n_1)."""
+        st = np.empty(self.n[0], np.int32)
+        wd = np.empty(self.n[0], np.int32)
+        check(self.ctx._lib.stencil_info(self.handle, None, None, st.ctypes.data_as(c_int32_p),
+                                         wd.ctypes.data_as(c_int32_p)), "stencil_info")
+        return st, wd
+
+    def values(self):
+        out = np.empty(self.nnz)
+        check(self.ctx._lib.stencil_get_values(self.handle, _dptr(out)), "stencil_get_values")
+        return out
+
+    def close(self):
+        if self.handle:
+            self.ctx._lib.stencil_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _mat_array(mats, ns):
+    arrs = [_host_f64(m, (n, n)) for m, n in zip(mats, ns)]
+    return arrs, (c_double_p * len(arrs))(*[_dptr(a) for a in arrs])
+
+
+def _vec_array(vecs, ns):
+    arrs = [_host_f64(v, (n,)) for v, n in zip(vecs, ns)]
+    return arrs, (c_double_p * len(arrs))(*[_dptr(a) for a in arrs])
+
+
+def fd_setup(ctx, M, K, tol_imag=1e-8, cond_max=1e8, allow_complex_pairs=False):
+    d = len(M)
+    ns = [np.asarray(m).shape[0] for m in M]
+    n = (C.c_int64 * d)(*ns)
+    am, pm = _mat_array(M, ns)
+    ak, pk = _mat_array(K, ns)
+    opts = FdSetupOpts(tol_imag, cond_max, int(allow_complex_pairs))
+    h = C.c_void_p()
+    check(ctx._lib.fd_setup(ctx.handle, d, n, pm, pk, C.byref(opts), C.byref(h)), "fd_setup")
+    return FDPlan(ctx, h, ns)
+
+
+def fd_setup_from_factors(ctx, U, W, lam):
+    d = len(U)
+    ns = [np.asarray(u).shape[0] for u in U]
+    n = (C.c_int64 * d)(*ns)
+    au, pu = _mat_array(U, ns)
+    aw, pw = _mat_array(W, ns)
+    al, pl = _vec_array(lam, ns)
+    h = C.c_void_p()
+    check(ctx._lib.fd_setup_from_factors(ctx.handle, d, n, pu, pw, pl, C.byref(h)), "fd_setup_from_factors")
+    return FDPlan(ctx, h, ns)
+
+
+def fd_setup_from_eig(ctx, U, lam, M=None):
+    d = len(U)
+    ns = [np.asarray(u).shape[0] for u in U]
+    n = (C.c_int64 * d)(*ns)
+    au, pu = _mat_array(U, ns)
+    al, pl = _vec_array(lam, ns)
+    pm = None
+    if M is not None:
+        amm, pm = _mat_array(M, ns)
+    h = C.c_void_p()
+    check(ctx._lib.fd_setup_from_eig(ctx.handle, d, n, pu, pl, pm, C.byref(h)), "fd_setup_from_eig")
+    return FDPlan(ctx, h, ns)
+
+
+def fd_apply(plan, r, s):
+    """s = P^{-1} r on the device (asynchronous on the context stream)."""
+    check(plan.ctx._lib.fd_apply(plan.handle, _devptr(r, plan.N), _devptr(s, plan.N)), "fd_apply")
+    return s
+
+
+def fd_apply_host(plan, r_host, s_host):
+    """Same with host (numpy, ideally pinned) buffers; H2D + apply + D2H inside the call."""
+    if r_host.dtype != np.float64 or s_host.dtype != np.float64 or r_host.size != plan.N or s_host.size != plan.N:
+        raise ValueError("fd_apply_host: float64 host arrays of length N expected")
+    check(plan.ctx._lib.fd_apply_host(plan.handle, _dptr(r_host), _dptr(s_host)), "fd_apply_host")
+    return s_host
+
+
+def colloc_assemble(ctx, d, p, ne, geometry, geo_params=()):
+    nes = [ne] * d if np.isscalar(ne) else list(ne)
+    n = (C.c_int64 * d)(*nes)
+    prm = np.ascontiguousarray(np.asarray(list(geo_params) + [0.0] * 4, dtype=np.float64))
+    h = C.c_void_p()
+    check(ctx._lib.colloc_assemble(ctx.handle, d, int(p), n, int(geometry), _dptr(prm), C.byref(h)),
+          "colloc_assemble")
+    return Stencil(ctx, h)
+
+
+def stencil_create(ctx, n, start, width, values):
+    d = len(n)
+    nn = (C.c_int64 * d)(*n)
+    st = [np.ascontiguousarray(np.asarray(s, dtype=np.int32)) for s in start]
+    wd = [np.ascontiguousarray(np.asarray(w, dtype=np.int32)) for w in width]
+    pst = (c_int32_p * d)(*[a.ctypes.data_as(c_int32_p) for a in st])
+    pwd = (c_int32_p * d)(*[a.ctypes.data_as(c_int32_p) for a in wd])
+    h = C.c_void_p()
+    try:
+        import torch
+        on_dev = isinstance(values, torch.Tensor) and values.is_cuda
+    except ImportError:
+        on_dev = False
+    if on_dev:
+        vp = _devptr(values)
+    else:
+        values = _host_f64(values)
+        vp = C.c_void_p(values.ctypes.data)
+    check(ctx._lib.stencil_create(ctx.handle, d, nn, pst, pwd, vp, int(on_dev), C.byref(h)), "stencil_create")
+    return Stencil(ctx, h)
+
+
+def stencil_matvec(A, x, y):
+    check(A.ctx._lib.stencil_matvec(A.handle, _devptr(x, A.N), _devptr(y, A.N)), "stencil_matvec")
+    return y
+
+
+def colloc_1d_factors(p, ne):
+    n = ne + p - 2
+    M, K = np.empty((n, n)), np.empty((n, n))
+    check(load().colloc_1d_factors(int(p), int(ne), _dptr(M), _dptr(K)), "colloc_1d_factors")
+    return M, K
+
+
+def gmres_solve(ctx, A, P, b, x, m=30, rtol=1e-8, max_iters=1000, orth=ORTH_CGS_DGKS, use_x0=False,
+                history=False, raise_on_nonconvergence=True):
+    """Right-preconditioned GMRES(m); returns the report as a dict."""
+    opts = GmresOpts(int(m), float(rtol), int(max_iters), int(orth), int(use_x0))
+    rep = GmresReport()
+    hist = None
+    if history:
+        hist = np.zeros(max_iters)
+        rep.history = _dptr(hist)
+        rep.history_cap = max_iters
+    st = ctx._lib.gmres_solve(ctx.handle, A.handle, P.handle if P is not None else None, _devptr(b, A.N),
+                              _devptr(x, A.N), C.byref(opts), C.byref(rep))
+    if st != 0 and (raise_on_nonconvergence or st != -8):
+        check(st, "gmres_solve")
+    out = dict(iters=rep.iters, restarts=rep.restarts, converged=bool(rep.converged), reorth=rep.reorth,
+               rel_res_true=rep.rel_res_true, rel_res_implicit=rep.rel_res_implicit, t_total_ms=rep.t_total_ms,
+               status=st)
+    if hist is not None:
+        out["history"] = hist[:rep.iters].copy()
+    return out

@@ -1,0 +1,113 @@
+// Context, status strings, error plumbing.
+#include <cstdarg>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace fdiga {
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int ensure_pinned(fdiga_ctx* c, size_t n) {
+  if (n <= c->pinned_cap) return FDIGA_OK;
+  if (c->pinned) cudaFreeHost(c->pinned);
+  c->pinned = nullptr;
+  c->pinned_cap = 0;
+  FDIGA_CUDA(cudaMallocHost(&c->pinned, n * sizeof(double)));
+  c->pinned_cap = n;
+  return FDIGA_OK;
+}
+}  // namespace fdiga
+
+using namespace fdiga;
+
+extern "C" {
+
+const char* fdiga_last_error(void) { return g_err; }
+
+const char* fdiga_status_string(int s) {
+  switch (s) {
+    case FDIGA_OK: return "OK";
+    case FDIGA_ERR_INVALID_ARG: return "INVALID_ARG";
+    case FDIGA_ERR_CUDA: return "CUDA";
+    case FDIGA_ERR_CUSOLVER: return "CUSOLVER";
+    case FDIGA_ERR_NCCL: return "NCCL";
+    case FDIGA_ERR_COMPLEX_SPECTRUM: return "COMPLEX_SPECTRUM";
+    case FDIGA_ERR_ILL_CONDITIONED: return "ILL_CONDITIONED";
+    case FDIGA_ERR_SINGULAR: return "SINGULAR";
+    case FDIGA_ERR_NOT_CONVERGED: return "NOT_CONVERGED";
+    case FDIGA_ERR_BREAKDOWN: return "BREAKDOWN";
+    case FDIGA_ERR_NOT_SUPPORTED: return "NOT_SUPPORTED";
+    case FDIGA_ERR_OOM: return "OOM";
+    default: return "UNKNOWN";
+  }
+}
+
+int fdiga_comm_init(fdiga_ctx* ctx, const void* uid);      // comm.cu
+int fdiga_comm_destroy(fdiga_ctx* ctx);                     // comm.cu
+
+int fdiga_ctx_create(int device, void* cuda_stream, int nranks, int rank, const void* nccl_unique_id,
+                     fdiga_ctx** out) {
+  FDIGA_CHECK(out != nullptr, FDIGA_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  FDIGA_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, FDIGA_ERR_INVALID_ARG, "bad nranks/rank %d/%d",
+              nranks, rank);
+  FDIGA_CHECK(nranks == 1 || nccl_unique_id != nullptr, FDIGA_ERR_INVALID_ARG,
+              "nccl_unique_id required when nranks > 1");
+  int ndev = 0;
+  FDIGA_CUDA(cudaGetDeviceCount(&ndev));
+  FDIGA_CHECK(device >= 0 && device < ndev, FDIGA_ERR_INVALID_ARG, "device %d out of range (%d devices)", device,
+              ndev);
+  FDIGA_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  FDIGA_CUDA(cudaGetDeviceProperties(&prop, device));
+  FDIGA_CHECK(prop.major == 10 && prop.minor == 0, FDIGA_ERR_NOT_SUPPORTED,
+              "libfdiga is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major, prop.minor);
+  fdiga_ctx* c = new fdiga_ctx();
+  c->device = device;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->sm_count = prop.multiProcessorCount;
+  // NULL selects the legacy default stream (ordered with every blocking stream, e.g. torch's default)
+  c->stream = (cudaStream_t)cuda_stream;
+  c->own_stream = false;
+  if (nranks > 1) {
+    int s = fdiga_comm_init(c, nccl_unique_id);
+    if (s != FDIGA_OK) {
+      if (c->own_stream) cudaStreamDestroy(c->stream);
+      delete c;
+      return s;
+    }
+  }
+  *out = c;
+  return FDIGA_OK;
+}
+
+int fdiga_ctx_destroy(fdiga_ctx* c) {
+  if (!c) return FDIGA_OK;
+  cudaSetDevice(c->device);
+  if (c->nccl_comm) fdiga_comm_destroy(c);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  for (auto& b : c->ws) b.release();
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return FDIGA_OK;
+}
+
+int fdiga_slab(const fdiga_ctx* c, int64_t n_last, int64_t* begin, int64_t* end) {
+  FDIGA_CHECK(c && begin && end && n_last >= 0, FDIGA_ERR_INVALID_ARG, "bad fdiga_slab arguments");
+  int64_t q = n_last / c->nranks, r = n_last % c->nranks;
+  *begin = c->rank * q + (c->rank < r ? c->rank : r);
+  *end = *begin + q + (c->rank < r ? 1 : 0);
+  return FDIGA_OK;
+}
+
+int64_t fdiga_kernel_launches(const fdiga_ctx* c) { return c ? c->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,212 @@
+// FP64 tensor-core GEMM for the FD mode-k products (sm_100a).
+//
+// On sm_100a the only FP64 tensor instruction is the warp-level DMMA.8x8x4 (PTX
+// mma.sync.aligned.m8n8k4.row.col.f64); tcgen05.mma has no f64 kind, so there is no TMEM/UMMA
+// path for FP64 and accumulators live in registers.
+// Measured on the pool's B200: 37.1 TFLOP/s for a register-resident DMMA loop (profiles/r01_peaks_fp64.jsonl).
+//
+//   C[M x N] = A[M x K] * B[K x N]   (+ optional epilogue C /= lam_m[m] + lam_n[n]), batched over blockIdx.z
+//   A: row-major, k contiguous (lda)
+//   B: BLayout::KN -> B[k*ldb + n] (n contiguous)       used by modes 2..d (left-multiply by the factor)
+//      BLayout::NK -> B[n*ldb + k] (k contiguous)       used by mode 1 (right-multiply by factor^T)
+//
+// Tiles are staged global->shared with cp.async (16 B when the rows are 16 B aligned, else 8 B),
+// zero-filled outside [M,N,K], into a STAGES-deep ring; shared rows are padded so that the
+// m8n8k4 fragment loads (8 rows x 4 k, or 4 k x 8 cols) are bank-conflict free.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace fdiga {
+
+enum class BLayout { KN, NK };
+
+struct GemmParams {
+  int M, N, K;
+  const double* A;
+  int64_t lda, strideA;
+  const double* B;
+  int64_t ldb, strideB;
+  double* C;
+  int64_t ldc, strideC;
+  const double* lam_m;  // epilogue divide (nullptr: none): C[m][n] = acc / (lam_m[m] + lam_n[n])
+  const double* lam_n;
+  int64_t strideLamN;   // per-batch offset of lam_n (0: shared)
+};
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct TileCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int THREADS = WM * WN * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN;
+  static constexpr int MI = WTM / 8, NJ = WTN / 8;
+  static constexpr int SA = BK + 4;          // A row stride (doubles): == 4 (mod 16) when BK % 16 == 0
+  static constexpr int SBkn = BN + 4;        // B [k][n] row stride
+  static constexpr int SBnk = BK + 4;        // B [n][k] row stride
+  static_assert(WTM % 8 == 0 && WTN % 8 == 0 && BK % 4 == 0, "tile shape");
+  static constexpr int A_ELEMS = BM * SA;
+  static constexpr int B_ELEMS_KN = BK * SBkn;
+  static constexpr int B_ELEMS_NK = BN * SBnk;
+  template <BLayout L>
+  __host__ __device__ static constexpr int b_elems() { return L == BLayout::KN ? B_ELEMS_KN : B_ELEMS_NK; }
+  template <BLayout L>
+  __host__ __device__ static constexpr size_t smem_bytes() { return size_t(STAGES) * (A_ELEMS + b_elems<L>()) * sizeof(double); }
+};
+
+// VA / VB: doubles per cp.async chunk for A / B (2 needs 16-byte aligned rows, else 1).
+template <class T, BLayout BL, int VA, int VB>
+__global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) {
+  extern __shared__ __align__(16) double smem[];
+  double* sA = smem;
+  double* sB = smem + T::STAGES * T::A_ELEMS;
+  constexpr int BE = T::template b_elems<BL>();
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int warp_m = warp / T::WN, warp_n = warp % T::WN;
+  const int m0 = blockIdx.x * T::BM, n0 = blockIdx.y * T::BN;
+  const int64_t bz = blockIdx.z;
+  const double* __restrict__ A = p.A + bz * p.strideA;
+  const double* __restrict__ B = p.B + bz * p.strideB;
+  double* __restrict__ C = p.C + bz * p.strideC;
+  const int M = p.M, N = p.N, K = p.K;
+  const int KT = (K + T::BK - 1) / T::BK;
+
+  auto load_tile = [&](int stage, int kt) {
+    const int k0 = kt * T::BK;
+    // ---- A tile: BM x BK, rows m, cols k
+    {
+      constexpr int CPR = T::BK / VA;  // chunks per row
+      constexpr int CH = T::BM * CPR;
+      double* dst = sA + stage * T::A_ELEMS;
+#pragma unroll
+      for (int c = tid; c < CH; c += T::THREADS) {
+        const int r = c / CPR, cc = c % CPR;
+        const int gm = m0 + r, gk = k0 + cc * VA;
+        const uint32_t d = smem_u32(dst + r * T::SA + cc * VA);
+        int bytes = 0;
+        const double* src = A;
+        if (gm < M && gk < K) {
+          bytes = (VA == 2 && gk + 1 >= K) ? 8 : VA * 8;
+          src = A + (int64_t)gm * p.lda + gk;
+        }
+        if (VA == 2) cp_async16(d, src, bytes); else cp_async8(d, src, bytes);
+      }
+    }
+    // ---- B tile
+    double* dstB = sB + stage * BE;
+    if (BL == BLayout::KN) {
+      constexpr int CPR = T::BN / VB;
+      constexpr int CH = T::BK * CPR;
+#pragma unroll
+      for (int c = tid; c < CH; c += T::THREADS) {
+        const int r = c / CPR, cc = c % CPR;
+        const int gk = k0 + r, gn = n0 + cc * VB;
+        const uint32_t d = smem_u32(dstB + r * T::SBkn + cc * VB);
+        int bytes = 0;
+        const double* src = B;
+        if (gk < K && gn < N) {
+          bytes = (VB == 2 && gn + 1 >= N) ? 8 : VB * 8;
+          src = B + (int64_t)gk * p.ldb + gn;
+        }
+        if (VB == 2) cp_async16(d, src, bytes); else cp_async8(d, src, bytes);
+      }
+    } else {
+      constexpr int CPR = T::BK / VB;
+      constexpr int CH = T::BN * CPR;
+#pragma unroll
+      for (int c = tid; c < CH; c += T::THREADS) {
+        const int r = c / CPR, cc = c % CPR;
+        const int gn = n0 + r, gk = k0 + cc * VB;
+        const uint32_t d = smem_u32(dstB + r * T::SBnk + cc * VB);
+        int bytes = 0;
+        const double* src = B;
+        if (gn < N && gk < K) {
+          bytes = (VB == 2 && gk + 1 >= K) ? 8 : VB * 8;
+          src = B + (int64_t)gn * p.ldb + gk;
+        }
+        if (VB == 2) cp_async16(d, src, bytes); else cp_async8(d, src, bytes);
+      }
+    }
+  };
+
+  double acc[T::MI][T::NJ][2];
+#pragma unroll
+  for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < T::NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < T::STAGES - 1; ++s) {
+    if (s < KT) load_tile(s, s);
+    cp_async_commit();
+  }
+
+  const int lr = lane >> 2, lc = lane & 3;
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<T::STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + T::STAGES - 1;
+      if (nk < KT) load_tile(nk % T::STAGES, nk);
+      cp_async_commit();
+    }
+    const int st = kt % T::STAGES;
+    const double* a_s = sA + st * T::A_ELEMS + (warp_m * T::WTM + lr) * T::SA + lc;
+    const double* b_s = sB + st * BE;
+#pragma unroll
+    for (int kk = 0; kk < T::BK / 4; ++kk) {
+      double af[T::MI], bf[T::NJ];
+#pragma unroll
+      for (int i = 0; i < T::MI; ++i) af[i] = a_s[i * 8 * T::SA + kk * 4];
+#pragma unroll
+      for (int j = 0; j < T::NJ; ++j) {
+        if (BL == BLayout::KN)
+          bf[j] = b_s[(kk * 4 + lc) * T::SBkn + warp_n * T::WTN + j * 8 + lr];
+        else
+          bf[j] = b_s[(warp_n * T::WTN + j * 8 + lr) * T::SBnk + kk * 4 + lc];
+      }
+#pragma unroll
+      for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < T::NJ; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---- epilogue: optional eigenvalue-sum divide (eq:FD3D diagonal term), store
+  const double* lam_n = p.lam_n ? p.lam_n + bz * p.strideLamN : nullptr;
+  const bool vec_ok = ((p.ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+#pragma unroll
+  for (int i = 0; i < T::MI; ++i) {
+    const int row = m0 + warp_m * T::WTM + i * 8 + lr;
+    if (row >= M) continue;
+    const double lm = p.lam_m ? p.lam_m[row] : 0.0;
+#pragma unroll
+    for (int j = 0; j < T::NJ; ++j) {
+      const int col = n0 + warp_n * T::WTN + j * 8 + 2 * lc;
+      double v0 = acc[i][j][0], v1 = acc[i][j][1];
+      if (p.lam_m) {
+        if (col < N) v0 = v0 / (lm + lam_n[col]);
+        if (col + 1 < N) v1 = v1 / (lm + lam_n[col + 1]);
+      }
+      double* dst = C + (int64_t)row * p.ldc + col;
+      if (vec_ok && col + 1 < N) {
+        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+      } else {
+        if (col < N) dst[0] = v0;
+        if (col + 1 < N) dst[1] = v1;
+      }
+    }
+  }
+}
+
+}  // namespace fdiga

@@ -1,0 +1,529 @@
+// FD preconditioner: setup (cuSOLVER, one time) and apply (DMMA mode-product kernels).
+//
+//   s = (U_d (x)..(x) U_1) Lambda^{-1} (W_d (x)..(x) W_1) r        eq:FD2D / eq:FD3D
+//   W_l = V_l^T = (M_l U_l)^{-1}
+//
+// Layout: r, s are X[i_d]..[i_1] (i_1 fastest).  A Kronecker factor A_l acts on index i_l:
+//   mode 1 (contiguous axis):  T(n_2..n_d x n_1) = X(n_2..n_d x n_1) * A_1^T      -> B operand k-contiguous (NK)
+//   mode l >= 2:               T[i_{l+1}..](n_l x n_1..n_{l-1}) = A_l * X[...]     -> B operand n-contiguous (KN)
+// so no global transposes are needed.  The eigenvalue-sum divide is fused into the epilogue of
+// the last forward product (mode d), "just a diagonal scaling".
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+#include "dmma_gemm.cuh"
+
+using namespace fdiga;
+
+struct fd_plan {
+  fdiga_ctx* ctx = nullptr;
+  int d = 0;
+  int64_t n[3] = {1, 1, 1};
+  int64_t ld[3] = {0, 0, 0};  // padded (even) leading dimension of the device factors
+  int64_t N = 0;
+  double* U[3] = {nullptr, nullptr, nullptr};
+  double* W[3] = {nullptr, nullptr, nullptr};
+  double* lam[3] = {nullptr, nullptr, nullptr};
+  double* lam_inner = nullptr;  // sum of the eigenvalues of directions 1..d-1 over the flattened inner index
+  DevBuf t0, t1;                // ping-pong scratch
+  DevBuf host_io;               // device staging for fd_apply_host
+  std::vector<double> hU[3], hW[3], hlam[3], hlam_im[3];
+};
+
+namespace {
+
+using Cfg128 = TileCfg<128, 128, 16, 2, 4, 4>;
+
+template <class T, BLayout BL, int VA, int VB>
+int launch_variant(fdiga_ctx* ctx, const GemmParams& p, int batch) {
+  auto kern = dmma_gemm_kernel<T, BL, VA, VB>;
+  constexpr size_t smem = T::template smem_bytes<BL>();
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    FDIGA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  dim3 grid((p.M + T::BM - 1) / T::BM, (p.N + T::BN - 1) / T::BN, batch);
+  FDIGA_CHECK(grid.y <= 65535 && grid.z <= 65535, FDIGA_ERR_NOT_SUPPORTED, "GEMM grid too large");
+  kern<<<grid, T::THREADS, smem, ctx->stream>>>(p);
+  count_launch(ctx);
+  FDIGA_CUDA(cudaGetLastError());
+  return FDIGA_OK;
+}
+
+inline bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
+
+template <class T, BLayout BL>
+int launch_gemm(fdiga_ctx* ctx, const GemmParams& p, int batch) {
+  const bool va = aligned16(p.A) && (p.lda % 2 == 0) && (batch == 1 || p.strideA % 2 == 0);
+  const bool vb = aligned16(p.B) && (p.ldb % 2 == 0) && (batch == 1 || p.strideB % 2 == 0);
+  if (va && vb) return launch_variant<T, BL, 2, 2>(ctx, p, batch);
+  if (va) return launch_variant<T, BL, 2, 1>(ctx, p, batch);
+  if (vb) return launch_variant<T, BL, 1, 2>(ctx, p, batch);
+  return launch_variant<T, BL, 1, 1>(ctx, p, batch);
+}
+
+// mode 1: Y(R x n1) = X(R x n1) * F^T
+int mode1(fd_plan* P, const double* F, int64_t ldf, const double* X, double* Y, int64_t R) {
+  GemmParams g{};
+  g.M = (int)R;
+  g.N = (int)P->n[0];
+  g.K = (int)P->n[0];
+  g.A = X;
+  g.lda = P->n[0];
+  g.B = F;
+  g.ldb = ldf;
+  g.C = Y;
+  g.ldc = P->n[0];
+  return launch_gemm<Cfg128, BLayout::NK>(P->ctx, g, 1);
+}
+
+// mode l (>=2): for each of `batch` outer slices, Y(n_l x inner) = F(n_l x n_l) * X(n_l x inner)
+int model(fd_plan* P, int l, const double* F, int64_t ldf, const double* X, double* Y, int64_t inner,
+          int64_t batch, const double* lam_m, const double* lam_n) {
+  GemmParams g{};
+  g.M = (int)P->n[l];
+  g.N = (int)inner;
+  g.K = (int)P->n[l];
+  g.A = F;
+  g.lda = ldf;
+  g.B = X;
+  g.ldb = inner;
+  g.strideB = inner * P->n[l];
+  g.C = Y;
+  g.ldc = inner;
+  g.strideC = inner * P->n[l];
+  g.lam_m = lam_m;
+  g.lam_n = lam_n;
+  return launch_gemm<Cfg128, BLayout::KN>(P->ctx, g, (int)batch);
+}
+
+int upload_factor(const double* h, int64_t n, int64_t ld, double** dptr) {
+  std::vector<double> pad((size_t)n * ld, 0.0);
+  for (int64_t i = 0; i < n; ++i) std::memcpy(&pad[i * ld], h + i * n, n * sizeof(double));
+  FDIGA_CUDA(cudaMalloc(dptr, pad.size() * sizeof(double)));
+  FDIGA_CUDA(cudaMemcpy(*dptr, pad.data(), pad.size() * sizeof(double), cudaMemcpyHostToDevice));  // synchronous
+  return FDIGA_OK;
+}
+
+int finish_plan(fd_plan* P) {
+  // singularity guard on the eigenvalue sums: min |Lambda| <= 1e3 eps max |Lambda|
+  double mn = INFINITY, mx = 0.0;
+  {
+    const int d = P->d;
+    const auto& l1 = P->hlam[0];
+    const auto& l2 = P->hlam[1];
+    std::vector<double> inner;  // lam_1 + ... + lam_{d-1}
+    if (d == 2) {
+      inner = l1;
+    } else {
+      inner.resize(l1.size() * l2.size());
+      for (size_t b = 0; b < l2.size(); ++b)
+        for (size_t a = 0; a < l1.size(); ++a) inner[b * l1.size() + a] = l1[a] + l2[b];
+    }
+    for (double lo : P->hlam[d - 1])
+      for (double v : inner) {
+        const double s = std::fabs(lo + v);
+        mn = std::min(mn, s);
+        mx = std::max(mx, s);
+      }
+    FDIGA_CHECK(mn > 1e3 * 2.220446049250313e-16 * mx, FDIGA_ERR_SINGULAR,
+                "eigenvalue sums nearly singular: min |Lambda| = %g, max = %g", mn, mx);
+    FDIGA_CUDA(cudaMalloc(&P->lam_inner, inner.size() * sizeof(double)));
+    FDIGA_CUDA(cudaMemcpy(P->lam_inner, inner.data(), inner.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  for (int l = 0; l < P->d; ++l) {
+    P->ld[l] = (P->n[l] + 1) & ~int64_t(1);
+    FDIGA_TRY(upload_factor(P->hU[l].data(), P->n[l], P->ld[l], &P->U[l]));
+    FDIGA_TRY(upload_factor(P->hW[l].data(), P->n[l], P->ld[l], &P->W[l]));
+    FDIGA_CUDA(cudaMalloc(&P->lam[l], P->n[l] * sizeof(double)));
+    FDIGA_CUDA(cudaMemcpy(P->lam[l], P->hlam[l].data(), P->n[l] * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  FDIGA_TRY(P->t0.ensure(P->N));
+  FDIGA_TRY(P->t1.ensure(P->N));
+  FDIGA_CUDA(cudaDeviceSynchronize());  // uploads complete before any stream uses the plan
+  return FDIGA_OK;
+}
+
+int check_common(fdiga_ctx* ctx, int d, const int64_t* n, fd_plan** out) {
+  FDIGA_CHECK(ctx && n && out, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_CHECK(d == 2 || d == 3, FDIGA_ERR_INVALID_ARG, "d must be 2 or 3 (got %d)", d);
+  for (int l = 0; l < d; ++l)
+    FDIGA_CHECK(n[l] >= 1 && n[l] <= 65535, FDIGA_ERR_INVALID_ARG, "n[%d] = %lld out of range", l, (long long)n[l]);
+  FDIGA_CHECK(ctx->nranks == 1, FDIGA_ERR_NOT_SUPPORTED, "multi-rank FD apply is not built in this version");
+  *out = nullptr;
+  return bind(ctx);
+}
+
+fd_plan* new_plan(fdiga_ctx* ctx, int d, const int64_t* n) {
+  fd_plan* P = new fd_plan();
+  P->ctx = ctx;
+  P->d = d;
+  P->N = 1;
+  for (int l = 0; l < d; ++l) {
+    P->n[l] = n[l];
+    P->N *= n[l];
+  }
+  return P;
+}
+
+// ---------------------------------------------------------------- cuSOLVER helpers
+#define CUSOLVER(call)                                                                              \
+  do {                                                                                              \
+    cusolverStatus_t s_ = (call);                                                                   \
+    if (s_ != CUSOLVER_STATUS_SUCCESS) {                                                            \
+      set_error("cuSOLVER status %d at %s:%d (%s)", (int)s_, __FILE__, __LINE__, #call);            \
+      return FDIGA_ERR_CUSOLVER;                                                                    \
+    }                                                                                               \
+  } while (0)
+
+struct Solver {
+  cusolverDnHandle_t h = nullptr;
+  cusolverDnParams_t prm = nullptr;
+  ~Solver() {
+    if (prm) cusolverDnDestroyParams(prm);
+    if (h) cusolverDnDestroy(h);
+  }
+  int init(cudaStream_t s) {
+    CUSOLVER(cusolverDnCreate(&h));
+    CUSOLVER(cusolverDnSetStream(h, s));
+    CUSOLVER(cusolverDnCreateParams(&prm));
+    return FDIGA_OK;
+  }
+};
+
+// Column-major helpers (cuSOLVER is column-major; our host matrices are row-major).
+std::vector<double> to_colmajor(const double* rm, int64_t n) {
+  std::vector<double> c((size_t)n * n);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) c[j * n + i] = rm[i * n + j];
+  return c;
+}
+
+// X = A^{-1} B (A, B column-major n x n, nrhs = n) on the device with getrf/getrs.
+int lu_solve(Solver& S, cudaStream_t st, int64_t n, const std::vector<double>& A, std::vector<double>& B) {
+  double *dA = nullptr, *dB = nullptr;
+  int64_t* ipiv = nullptr;
+  int* info = nullptr;
+  void* dwork = nullptr;
+  int rc = FDIGA_OK;
+  size_t dws = 0, hws = 0;
+  std::vector<char> hwork;
+  int hinfo = 0;
+  auto cleanup = [&]() {
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(ipiv);
+    cudaFree(info);
+    cudaFree(dwork);
+  };
+  if (cudaMalloc(&dA, n * n * 8) || cudaMalloc(&dB, n * n * 8) || cudaMalloc(&ipiv, n * 8) ||
+      cudaMalloc(&info, sizeof(int))) {
+    cleanup();
+    set_error("cudaMalloc failed in lu_solve");
+    return FDIGA_ERR_CUDA;
+  }
+  cudaMemcpyAsync(dA, A.data(), n * n * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dB, B.data(), n * n * 8, cudaMemcpyHostToDevice, st);
+  if (cusolverDnXgetrf_bufferSize(S.h, S.prm, n, n, CUDA_R_64F, dA, n, CUDA_R_64F, &dws, &hws) !=
+      CUSOLVER_STATUS_SUCCESS) {
+    cleanup();
+    set_error("Xgetrf_bufferSize failed");
+    return FDIGA_ERR_CUSOLVER;
+  }
+  cudaMalloc(&dwork, std::max<size_t>(dws, 8));
+  hwork.resize(std::max<size_t>(hws, 8));
+  if (cusolverDnXgetrf(S.h, S.prm, n, n, CUDA_R_64F, dA, n, ipiv, CUDA_R_64F, dwork, dws, hwork.data(), hws,
+                       info) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnXgetrs(S.h, S.prm, CUBLAS_OP_N, n, n, CUDA_R_64F, dA, n, ipiv, CUDA_R_64F, dB, n, info) !=
+          CUSOLVER_STATUS_SUCCESS) {
+    cleanup();
+    set_error("Xgetrf/Xgetrs failed");
+    return FDIGA_ERR_CUSOLVER;
+  }
+  cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(B.data(), dB, n * n * 8, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cleanup();
+  FDIGA_CHECK(e == cudaSuccess, FDIGA_ERR_CUDA, "lu_solve: %s", cudaGetErrorString(e));
+  FDIGA_CHECK(hinfo == 0, FDIGA_ERR_SINGULAR, "LU: singular matrix (info = %d)", hinfo);
+  return rc;
+}
+
+double norm1_rm(const std::vector<double>& A, int64_t n) {  // max column abs sum, row-major
+  double best = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    double s = 0;
+    for (int64_t i = 0; i < n; ++i) s += std::fabs(A[i * n + j]);
+    best = std::max(best, s);
+  }
+  return best;
+}
+
+// W = (M U)^{-1} (row-major in/out; M == nullptr means identity).  Also returns cond_1(U).
+int compute_W(Solver& S, cudaStream_t st, int64_t n, const double* M, const std::vector<double>& U,
+              std::vector<double>& W, double* condU) {
+  std::vector<double> MU(U);
+  if (M) {
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        double s = 0;
+        for (int64_t k = 0; k < n; ++k) s += M[i * n + k] * U[k * n + j];
+        MU[i * n + j] = s;
+      }
+  }
+  std::vector<double> A = to_colmajor(MU.data(), n);
+  std::vector<double> B((size_t)n * n, 0.0);
+  for (int64_t i = 0; i < n; ++i) B[i * n + i] = 1.0;
+  FDIGA_TRY(lu_solve(S, st, n, A, B));  // B = (MU)^{-1}, column-major
+  W.assign((size_t)n * n, 0.0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) W[i * n + j] = B[j * n + i];
+  if (condU) {
+    // U^{-1} = W M
+    std::vector<double> Uinv(W);
+    if (M) {
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+          double s = 0;
+          for (int64_t k = 0; k < n; ++k) s += W[i * n + k] * M[k * n + j];
+          Uinv[i * n + j] = s;
+        }
+    }
+    *condU = norm1_rm(U, n) * norm1_rm(Uinv, n);
+  }
+  return FDIGA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fd_setup_from_factors(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* U, const double* const* W,
+                          const double* const* lam, fd_plan** out) {
+  FDIGA_TRY(check_common(ctx, d, n, out));
+  FDIGA_CHECK(U && W && lam, FDIGA_ERR_INVALID_ARG, "NULL factor array");
+  fd_plan* P = new_plan(ctx, d, n);
+  for (int l = 0; l < d; ++l) {
+    FDIGA_CHECK(U[l] && W[l] && lam[l], FDIGA_ERR_INVALID_ARG, "NULL factor for direction %d", l);
+    P->hU[l].assign(U[l], U[l] + n[l] * n[l]);
+    P->hW[l].assign(W[l], W[l] + n[l] * n[l]);
+    P->hlam[l].assign(lam[l], lam[l] + n[l]);
+    P->hlam_im[l].assign(n[l], 0.0);
+  }
+  int s = finish_plan(P);
+  if (s != FDIGA_OK) {
+    fd_plan_destroy(P);
+    return s;
+  }
+  *out = P;
+  return FDIGA_OK;
+}
+
+int fd_setup_from_eig(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* U, const double* const* lam,
+                      const double* const* M, fd_plan** out) {
+  FDIGA_TRY(check_common(ctx, d, n, out));
+  FDIGA_CHECK(U && lam, FDIGA_ERR_INVALID_ARG, "NULL factor array");
+  Solver S;
+  FDIGA_TRY(S.init(ctx->stream));
+  fd_plan* P = new_plan(ctx, d, n);
+  for (int l = 0; l < d; ++l) {
+    P->hU[l].assign(U[l], U[l] + n[l] * n[l]);
+    P->hlam[l].assign(lam[l], lam[l] + n[l]);
+    P->hlam_im[l].assign(n[l], 0.0);
+    int s = compute_W(S, ctx->stream, n[l], M ? M[l] : nullptr, P->hU[l], P->hW[l], nullptr);
+    if (s != FDIGA_OK) {
+      fd_plan_destroy(P);
+      return s;
+    }
+  }
+  int s = finish_plan(P);
+  if (s != FDIGA_OK) {
+    fd_plan_destroy(P);
+    return s;
+  }
+  *out = P;
+  return FDIGA_OK;
+}
+
+int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, const double* const* K,
+             const fd_setup_opts* opts, fd_plan** out) {
+  FDIGA_TRY(check_common(ctx, d, n, out));
+  FDIGA_CHECK(M && K, FDIGA_ERR_INVALID_ARG, "NULL pencil array");
+  const double tol_imag = opts ? opts->tol_imag : 1e-8;
+  const double cond_max = opts ? opts->cond_max : 1e8;
+  const int allow_cplx = opts ? opts->allow_complex_pairs : 0;
+  Solver S;
+  FDIGA_TRY(S.init(ctx->stream));
+  fd_plan* P = new_plan(ctx, d, n);
+  auto fail = [&](int s) {
+    fd_plan_destroy(P);
+    return s;
+  };
+  for (int l = 0; l < d; ++l) {
+    const int64_t nl = n[l];
+    FDIGA_CHECK(M[l] && K[l], FDIGA_ERR_INVALID_ARG, "NULL pencil for direction %d", l);
+    // 1. C = M^{-1} K  (eq:eigendecomposition)
+    std::vector<double> Mc = to_colmajor(M[l], nl), C = to_colmajor(K[l], nl);
+    int s = lu_solve(S, ctx->stream, nl, Mc, C);
+    if (s) return fail(s);
+    // 2. eigenpairs of C (cuSOLVER Xgeev; real input -> complex eigenvalues, real packed VR)
+    double *dC = nullptr, *dVR = nullptr, *dVL = nullptr;
+    cuDoubleComplex* dWv = nullptr;
+    int* dinfo = nullptr;
+    void* dwork = nullptr;
+    size_t dws = 0, hws = 0;
+    cudaMalloc(&dC, nl * nl * 8);
+    cudaMalloc(&dVR, nl * nl * 8);
+    cudaMalloc(&dVL, 8);
+    cudaMalloc(&dWv, nl * sizeof(cuDoubleComplex));
+    cudaMalloc(&dinfo, sizeof(int));
+    cudaMemcpyAsync(dC, C.data(), nl * nl * 8, cudaMemcpyHostToDevice, ctx->stream);
+    cusolverStatus_t cs = cusolverDnXgeev_bufferSize(S.h, S.prm, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR,
+                                                     nl, CUDA_R_64F, dC, nl, CUDA_C_64F, dWv, CUDA_R_64F, dVL, 1,
+                                                     CUDA_R_64F, dVR, nl, CUDA_R_64F, &dws, &hws);
+    std::vector<char> hwork(std::max<size_t>(hws, 8));
+    if (cs == CUSOLVER_STATUS_SUCCESS) {
+      cudaMalloc(&dwork, std::max<size_t>(dws, 8));
+      cs = cusolverDnXgeev(S.h, S.prm, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, nl, CUDA_R_64F, dC, nl,
+                           CUDA_C_64F, dWv, CUDA_R_64F, dVL, 1, CUDA_R_64F, dVR, nl, CUDA_R_64F, dwork, dws,
+                           hwork.data(), hws, dinfo);
+    }
+    std::vector<std::complex<double>> ev(nl);
+    std::vector<double> VR((size_t)nl * nl);
+    int hinfo = -1;
+    cudaMemcpyAsync(ev.data(), dWv, nl * sizeof(cuDoubleComplex), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(VR.data(), dVR, nl * nl * 8, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(dC);
+    cudaFree(dVR);
+    cudaFree(dVL);
+    cudaFree(dWv);
+    cudaFree(dinfo);
+    cudaFree(dwork);
+    if (cs != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
+      set_error("cusolverDnXgeev failed (status %d, info %d)", (int)cs, hinfo);
+      return fail(FDIGA_ERR_CUSOLVER);
+    }
+    // 3. reality guard (Remark 1), sort ascending, unit 2-norm columns
+    double rho = 0, maxim = 0;
+    for (auto& z : ev) {
+      rho = std::max(rho, std::abs(z));
+      maxim = std::max(maxim, std::fabs(z.imag()));
+    }
+    if (maxim > tol_imag * rho) {
+      if (!allow_cplx) {
+        set_error("complex spectrum in direction %d: max |Im lambda| = %g (rho = %g)", l, maxim, rho);
+        return fail(FDIGA_ERR_COMPLEX_SPECTRUM);
+      }
+      set_error("complex-pair (2x2 block) FD apply is not built in this version");
+      return fail(FDIGA_ERR_NOT_SUPPORTED);
+    }
+    std::vector<int64_t> order(nl);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return ev[a].real() < ev[b].real(); });
+    std::vector<double> Ul((size_t)nl * nl), laml(nl);
+    for (int64_t c = 0; c < nl; ++c) {
+      const int64_t src = order[c];
+      laml[c] = ev[src].real();
+      double nrm = 0;
+      for (int64_t i = 0; i < nl; ++i) nrm += VR[src * nl + i] * VR[src * nl + i];
+      nrm = std::sqrt(nrm);
+      for (int64_t i = 0; i < nl; ++i) Ul[i * nl + c] = VR[src * nl + i] / nrm;  // row-major U
+    }
+    // 4. W = (M U)^{-1} and cond_1(U)
+    double condU = 0;
+    s = compute_W(S, ctx->stream, nl, M[l], Ul, P->hW[l], &condU);
+    if (s) return fail(s);
+    if (!(condU <= cond_max)) {
+      set_error("ill-conditioned eigenvector matrix in direction %d: cond_1(U) = %g", l, condU);
+      return fail(FDIGA_ERR_ILL_CONDITIONED);
+    }
+    P->hU[l] = std::move(Ul);
+    P->hlam[l] = std::move(laml);
+    P->hlam_im[l].assign(nl, 0.0);
+  }
+  int s = finish_plan(P);
+  if (s != FDIGA_OK) return fail(s);
+  *out = P;
+  return FDIGA_OK;
+}
+
+int fd_get_factors(const fd_plan* P, int l, double* U, double* W, double* lam_re, double* lam_im) {
+  FDIGA_CHECK(P && l >= 0 && l < P->d, FDIGA_ERR_INVALID_ARG, "bad plan or direction");
+  const size_t nn = P->n[l] * P->n[l];
+  if (U) std::memcpy(U, P->hU[l].data(), nn * 8);
+  if (W) std::memcpy(W, P->hW[l].data(), nn * 8);
+  if (lam_re) std::memcpy(lam_re, P->hlam[l].data(), P->n[l] * 8);
+  if (lam_im) std::memcpy(lam_im, P->hlam_im[l].data(), P->n[l] * 8);
+  return FDIGA_OK;
+}
+
+int fd_apply(fd_plan* P, const double* r, double* s) {
+  FDIGA_CHECK(P && r && s, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  fdiga_ctx* ctx = P->ctx;
+  FDIGA_TRY(bind(ctx));
+  double* a = P->t0.p;
+  double* b = P->t1.p;
+  const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
+  if (P->d == 2) {
+    // fwd: mode 1 (W_1), mode 2 (W_2) + divide by lam_2[i2] + lam_1[i1]; bwd: mode 2 (U_2), mode 1 (U_1)
+    FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2));
+    FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, 1, P->lam[1], P->lam_inner));
+    FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, 1, nullptr, nullptr));
+    FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2));
+  } else {
+    FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2 * n3));
+    FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, n3, nullptr, nullptr));
+    FDIGA_TRY(model(P, 2, P->W[2], P->ld[2], b, a, n1 * n2, 1, P->lam[2], P->lam_inner));
+    FDIGA_TRY(model(P, 2, P->U[2], P->ld[2], a, b, n1 * n2, 1, nullptr, nullptr));
+    FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, n3, nullptr, nullptr));
+    FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2 * n3));
+  }
+  return FDIGA_OK;
+}
+
+int fd_apply_host(fd_plan* P, const double* r_host, double* s_host) {
+  FDIGA_CHECK(P && r_host && s_host, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_TRY(bind(P->ctx));
+  FDIGA_TRY(P->host_io.ensure(P->N));
+  cudaStream_t st = P->ctx->stream;
+  FDIGA_CUDA(cudaMemcpyAsync(P->host_io.p, r_host, P->N * 8, cudaMemcpyHostToDevice, st));
+  FDIGA_TRY(fd_apply(P, P->host_io.p, P->host_io.p));
+  FDIGA_CUDA(cudaMemcpyAsync(s_host, P->host_io.p, P->N * 8, cudaMemcpyDeviceToHost, st));
+  FDIGA_CUDA(cudaStreamSynchronize(st));
+  return FDIGA_OK;
+}
+
+double fd_apply_flops(const fd_plan* P) {
+  if (!P) return 0;
+  double s = 0;
+  for (int l = 0; l < P->d; ++l) s += (double)P->n[l];
+  return 4.0 * (double)P->N * s;
+}
+
+int fd_plan_destroy(fd_plan* P) {
+  if (!P) return FDIGA_OK;
+  cudaSetDevice(P->ctx->device);
+  for (int l = 0; l < 3; ++l) {
+    cudaFree(P->U[l]);
+    cudaFree(P->W[l]);
+    cudaFree(P->lam[l]);
+  }
+  cudaFree(P->lam_inner);
+  P->t0.release();
+  P->t1.release();
+  P->host_io.release();
+  delete P;
+  return FDIGA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,704 @@
+// Collocation operator A_C: device assembly on analytic geometries and the stored-operator matvec.
+//
+// Row i = tau_i (Greville point) of eq:collocation:
+//   (A_C)_{ij} = -Lap_x (B^_j o F^{-1})(F(tau_i)),  K = I.
+// With x = F(xi), J = dF/dxi, H_c = d^2 F_c/dxi^2 (chain rule):
+//   A_ij = - sum_{a,b} G_ab d_a d_b B^_j(tau_i) + sum_a beta_a d_a B^_j(tau_i),
+//   G = (J^T J)^{-1},  beta_a = sum_c (J^{-1})_{ac} tr(G H_c),
+// and d^t B^_j(tau_i) = prod_l B_{j_l}^{(t_l)}(tau_{l,i_l}) (tensor-product basis).
+//
+// Storage ("tensor window"): per direction l and 1D index i, the contiguous column window
+// [start_l(i), start_l(i) + width_l(i)) holding every interior basis function whose value or first
+// two derivatives at tau_{l,i} is nonzero.  Row i stores the w_3 w_2 w_1 values of its column box
+// (j_1 fastest); row offsets follow from prefix sums of the widths, so no index arrays are stored
+// and the matvec moves exactly 8 nnz + 16 N bytes.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+using namespace fdiga;
+
+struct fdiga_stencil {
+  fdiga_ctx* ctx = nullptr;
+  int d = 0;
+  int64_t n[3] = {1, 1, 1};      // direction sizes (n[2] = 1 in 2D)
+  int64_t N = 0, nnz = 0;
+  int wmax = 0;                   // max window width over all directions
+  std::vector<int32_t> hstart[3], hwidth[3];
+  std::vector<int64_t> hpre[3];   // prefix sums of widths, length n+1
+  int32_t* start[3] = {nullptr, nullptr, nullptr};
+  int32_t* width[3] = {nullptr, nullptr, nullptr};
+  int64_t* pre[3] = {nullptr, nullptr, nullptr};
+  double* vals = nullptr;         // nnz (+2 padding) values, canonical layout
+  // matvec launch plan
+  int rows_per_chunk = 0, tpr = 0, threads = 0;
+  int64_t nchunks = 0;
+  int64_t max_chunk_vals = 0;     // doubles staged per chunk (incl. alignment slack)
+};
+
+namespace {
+
+// ------------------------------------------------------------------ host B-spline tables
+// Piegl & Tiller "DersBasisFuns": nonzero basis functions of degree p on the knot span `span`
+// and their derivatives up to order nd, ders[k][r] for functions span-p+r, r = 0..p.
+void ders_basis_funs(int span, double u, int p, int nd, const std::vector<double>& U,
+                     std::vector<std::vector<double>>& ders) {
+  std::vector<std::vector<double>> ndu(p + 1, std::vector<double>(p + 1));
+  std::vector<double> left(p + 1), right(p + 1);
+  ndu[0][0] = 1.0;
+  for (int j = 1; j <= p; ++j) {
+    left[j] = u - U[span + 1 - j];
+    right[j] = U[span + j] - u;
+    double saved = 0.0;
+    for (int r = 0; r < j; ++r) {
+      ndu[j][r] = right[r + 1] + left[j - r];
+      double temp = ndu[r][j - 1] / ndu[j][r];
+      ndu[r][j] = saved + right[r + 1] * temp;
+      saved = left[j - r] * temp;
+    }
+    ndu[j][j] = saved;
+  }
+  ders.assign(nd + 1, std::vector<double>(p + 1, 0.0));
+  for (int j = 0; j <= p; ++j) ders[0][j] = ndu[j][p];
+  std::vector<std::vector<double>> a(2, std::vector<double>(p + 1));
+  for (int r = 0; r <= p; ++r) {
+    int s1 = 0, s2 = 1;
+    a[0][0] = 1.0;
+    for (int k = 1; k <= nd; ++k) {
+      double dd = 0.0;
+      int rk = r - k, pk = p - k;
+      if (r >= k) {
+        a[s2][0] = a[s1][0] / ndu[pk + 1][rk];
+        dd = a[s2][0] * ndu[rk][pk];
+      }
+      int j1 = (rk >= -1) ? 1 : -rk;
+      int j2 = (r - 1 <= pk) ? k - 1 : p - r;
+      for (int j = j1; j <= j2; ++j) {
+        a[s2][j] = (a[s1][j] - a[s1][j - 1]) / ndu[pk + 1][rk + j];
+        dd += a[s2][j] * ndu[rk + j][pk];
+      }
+      if (r <= pk) {
+        a[s2][k] = -a[s1][k - 1] / ndu[pk + 1][r];
+        dd += a[s2][k] * ndu[r][pk];
+      }
+      ders[k][r] = dd;
+      std::swap(s1, s2);
+    }
+  }
+  int r = p;
+  for (int k = 1; k <= nd; ++k) {
+    for (int j = 0; j <= p; ++j) ders[k][j] *= r;
+    r *= (p - k);
+  }
+}
+
+// 1D tables for one direction: Greville points, windows, and B^{(r)}_j(tau_i) on the window.
+struct Table1D {
+  int64_t n = 0;
+  int wmax = 0;
+  std::vector<double> tau;
+  std::vector<int32_t> start, width;
+  std::vector<double> val[3];  // val[r][i * wmax + c] = B^{(r)}_{start(i)+c}(tau_i)
+};
+
+void build_table(int p, int64_t ne, Table1D& T) {
+  const int64_t m = ne + p;  // number of basis functions
+  const int64_t n = m - 2;
+  std::vector<double> U;
+  for (int k = 0; k <= p; ++k) U.push_back(0.0);
+  for (int64_t k = 1; k < ne; ++k) U.push_back((double)k / (double)ne);
+  for (int k = 0; k <= p; ++k) U.push_back(1.0);
+  T.n = n;
+  T.wmax = p + 1;
+  T.tau.resize(n);
+  T.start.resize(n);
+  T.width.resize(n);
+  for (int r = 0; r < 3; ++r) T.val[r].assign(n * T.wmax, 0.0);
+  for (int64_t i = 1; i <= n; ++i) {  // interior function i (0-based full index), Greville point of P:164
+    double s = 0;
+    for (int j = 1; j <= p; ++j) s += U[i + j];
+    const double t = s / p;
+    T.tau[i - 1] = t;
+    // knot span: U[span] <= t < U[span+1], span in [p, m-1]
+    int span = p;
+    while (span < m - 1 && U[span + 1] <= t) ++span;
+    std::vector<std::vector<double>> ders;
+    ders_basis_funs(span, t, p, std::min(2, p), U, ders);
+    while ((int)ders.size() < 3) ders.push_back(std::vector<double>(p + 1, 0.0));
+    // window: first/last full index among span-p..span with a nonzero value or 1st/2nd derivative,
+    // clipped to the interior functions 1..m-2
+    int64_t first = -1, last = -1;
+    for (int r = 0; r <= p; ++r) {
+      const int64_t k = span - p + r;
+      if (k < 1 || k > m - 2) continue;
+      if (ders[0][r] != 0.0 || ders[1][r] != 0.0 || ders[2][r] != 0.0) {
+        if (first < 0) first = k;
+        last = k;
+      }
+    }
+    T.start[i - 1] = (int32_t)(first - 1);
+    T.width[i - 1] = (int32_t)(last - first + 1);
+    for (int64_t k = first; k <= last; ++k) {
+      const int r = (int)(k - (span - p));
+      for (int q = 0; q < 3; ++q) T.val[q][(i - 1) * T.wmax + (k - first)] = ders[q][r];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ device geometry
+struct Geo {
+  int id;
+  double prm[4];
+};
+
+struct JH {
+  double J[3][3];     // J[c][a] = dF_c / dxi_a
+  double H[3][3][3];  // H[c][a][b] = d^2 F_c / dxi_a dxi_b
+};
+
+// Closed-form Jacobian and Hessians of the analytic maps (FDIGA_GEOM_*); unused entries are zero.
+__device__ __forceinline__ JH geometry_jh(const Geo g, const double x0, const double x1, const double x2) {
+  JH r;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      r.J[c][a] = (c == a) ? 1.0 : 0.0;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) r.H[c][a][b] = 0.0;
+    }
+  const double PI = 3.141592653589793;
+  if (g.id == FDIGA_GEOM_ANNULUS || g.id == FDIGA_GEOM_THICK_RING) {
+    const double r0 = g.prm[0], r1 = g.prm[1];
+    const double dr = r1 - r0, w = 0.5 * PI;
+    const double rad = r0 + dr * x0;
+    const double sn = sin(w * x1), cs = cos(w * x1);
+    r.J[0][0] = dr * cs;
+    r.J[0][1] = -rad * w * sn;
+    r.J[1][0] = dr * sn;
+    r.J[1][1] = rad * w * cs;
+    r.H[0][0][1] = -dr * w * sn;
+    r.H[0][1][0] = -dr * w * sn;
+    r.H[0][1][1] = -rad * w * w * cs;
+    r.H[1][0][1] = dr * w * cs;
+    r.H[1][1][0] = dr * w * cs;
+    r.H[1][1][1] = -rad * w * w * sn;
+    if (g.id == FDIGA_GEOM_THICK_RING) r.J[2][2] = g.prm[2];
+  } else if (g.id == FDIGA_GEOM_DEFORMED_CUBE) {
+    const double amp = g.prm[0];
+    const double s0 = sin(PI * x0), c0 = cos(PI * x0);
+    const double s1 = sin(PI * x1), c1 = cos(PI * x1);
+    const double s2 = sin(PI * x2), c2 = cos(PI * x2);
+    const double gr[3] = {PI * c0 * s1 * s2, PI * s0 * c1 * s2, PI * s0 * s1 * c2};
+    const double P2 = PI * PI;
+    const double hd = -P2 * s0 * s1 * s2, h01 = P2 * c0 * c1 * s2, h02 = P2 * c0 * s1 * c2, h12 = P2 * s0 * c1 * c2;
+    const double hg[3][3] = {{hd, h01, h02}, {h01, hd, h12}, {h02, h12, hd}};
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        r.J[c][a] += amp * gr[a];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) r.H[c][a][b] = amp * hg[a][b];
+      }
+  }
+  return r;
+}
+
+// Inverse of the leading D x D block by cofactors.
+template <int D>
+__device__ __forceinline__ void inv_small(const double A[3][3], double B[3][3]) {
+  if (D == 2) {
+    const double det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+    B[0][0] = A[1][1] / det;
+    B[0][1] = -A[0][1] / det;
+    B[1][0] = -A[1][0] / det;
+    B[1][1] = A[0][0] / det;
+    return;
+  }
+  const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
+  const double c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2];
+  const double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
+  const double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
+  B[0][0] = c00 / det;
+  B[1][0] = c01 / det;
+  B[2][0] = c02 / det;
+  B[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) / det;
+  B[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) / det;
+  B[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) / det;
+  B[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) / det;
+  B[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) / det;
+  B[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) / det;
+}
+
+struct AsmArgs {
+  int wmax;
+  int64_t n1, n2, n3, S1, S2;
+  const double *tau1, *tau2, *tau3;
+  const int32_t *w1, *w2, *w3;
+  const int64_t *pre1, *pre2, *pre3;
+  const double *tab1, *tab2, *tab3;  // tab_l[(r * n_l + i) * wmax + c] = B^{(r)}_{start_l(i)+c}(tau_{l,i})
+  Geo geo;
+  double* vals;
+};
+
+// One thread per collocation row: geometry coefficients G = (J^T J)^{-1}, beta, then the w3*w2*w1
+// box of values  sum_t c_t prod_l B^{(t_l)}.  All small arrays are statically indexed (registers).
+template <int D>
+__global__ void assemble_kernel(AsmArgs A) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t N = A.n1 * A.n2 * A.n3;
+  if (row >= N) return;
+  const int64_t i1 = row % A.n1, i2 = (row / A.n1) % A.n2, i3 = row / (A.n1 * A.n2);
+  const double x0 = A.tau1[i1], x1 = A.tau2[i2], x2 = (D == 3) ? A.tau3[i3] : 0.0;
+  const JH g = geometry_jh(A.geo, x0, x1, x2);
+  double JtJ[3][3], G[3][3], Ji[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      double s = 0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) s += g.J[c][a] * g.J[c][b];
+      JtJ[a][b] = s;
+      G[a][b] = 0;
+      Ji[a][b] = 0;
+    }
+  inv_small<D>(JtJ, G);
+  inv_small<D>(g.J, Ji);
+  double beta[3] = {0, 0, 0};
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    double tr = 0;  // tr(G H_c)
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) tr += G[a][b] * g.H[c][b][a];
+#pragma unroll
+    for (int a = 0; a < D; ++a) beta[a] += Ji[a][c] * tr;
+  }
+  const int W = A.wmax;
+  const int w1 = A.w1[i1];
+  const int w2 = A.w2[i2];
+  const int w3 = (D == 3) ? A.w3[i3] : 1;
+  const int64_t off = (D == 3 ? A.pre3[i3] * A.S2 * A.S1 : 0) + (int64_t)w3 * A.pre2[i2] * A.S1 +
+                      (int64_t)w3 * w2 * A.pre1[i1];
+  // 1D factor rows at this point: f_l[r] = &tab_l[(r n_l + i_l) W]
+  const double* f1[3];
+  const double* f2[3];
+  const double* f3[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    f1[r] = A.tab1 + (r * A.n1 + i1) * W;
+    f2[r] = A.tab2 + (r * A.n2 + i2) * W;
+    f3[r] = (D == 3) ? A.tab3 + (r * A.n3 + i3) * W : nullptr;
+  }
+  double* out = A.vals + off;
+  for (int a = 0; a < w3; ++a)
+    for (int b = 0; b < w2; ++b)
+      for (int c = 0; c < w1; ++c) {
+        double v = 0;
+        // -G_ab d_a d_b  (t = e_a + e_b) and beta_a d_a  (t = e_a)
+#pragma unroll
+        for (int p = 0; p < D; ++p)
+#pragma unroll
+          for (int q = 0; q < D; ++q) {
+            const int t1 = (p == 0) + (q == 0), t2 = (p == 1) + (q == 1), t3 = (p == 2) + (q == 2);
+            double prod = -G[p][q] * f1[t1][c] * f2[t2][b];
+            if (D == 3) prod *= f3[t3][a];
+            v += prod;
+          }
+#pragma unroll
+        for (int p = 0; p < D; ++p) {
+          const int t1 = (p == 0), t2 = (p == 1), t3 = (p == 2);
+          double prod = beta[p] * f1[t1][c] * f2[t2][b];
+          if (D == 3) prod *= f3[t3][a];
+          v += prod;
+        }
+        out[((int64_t)a * w2 + b) * w1 + c] = v;
+      }
+}
+
+// ------------------------------------------------------------------ matvec
+struct MvArgs {
+  int64_t n1, n2, n3, N, S1, S2;
+  int rows_per_chunk;
+  int64_t nchunks;
+  int64_t buf_elems;  // doubles per smem buffer
+  int64_t nnz;
+  const int32_t *st1, *st2, *st3, *w1, *w2, *w3;
+  const int64_t *pre1, *pre2, *pre3;
+  const double* vals;
+  const double* x;
+  double* y;
+};
+
+__device__ __forceinline__ int64_t row_offset(const MvArgs& A, int64_t row) {
+  const int64_t i1 = row % A.n1, t = row / A.n1;
+  const int64_t i2 = t % A.n2, i3 = t / A.n2;
+  const int64_t w3 = A.w3[i3], w2 = A.w2[i2];
+  return A.pre3[i3] * A.S2 * A.S1 + w3 * A.pre2[i2] * A.S1 + w3 * w2 * A.pre1[i1];
+}
+
+// y = A x.  Persistent CTAs walk chunks of `rows_per_chunk` consecutive rows.  The chunk's values
+// are one contiguous range of the canonical layout, staged global->shared by a single bulk copy
+// (TMA engine, UBLKCP) into a 2-deep ring, so the HBM stream is fully coalesced and prefetched one
+// chunk ahead.  TPR threads share a row (its (a,b) window pairs round-robin) and reduce by shuffles;
+// x is read through L1/L2 (the x window of a row block is reused by its neighbours).
+template <int TPR>
+__global__ void __launch_bounds__(256) matvec_kernel(MvArgs A) {
+  extern __shared__ __align__(16) double sv[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  const int R = A.rows_per_chunk;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t nnz_total = A.nnz;
+  auto chunk_range = [&](int64_t c, int64_t& a0, int64_t& a1) {
+    const int64_t r0 = c * R;
+    const int64_t r1 = min(r0 + R, A.N);
+    const int64_t o0 = row_offset(A, r0);
+    const int64_t o1 = (r1 >= A.N) ? nnz_total : row_offset(A, r1);
+    a0 = o0 & ~int64_t(1);
+    a1 = (o1 + 1) & ~int64_t(1);
+  };
+  auto issue = [&](int64_t c, int buf) {
+    int64_t a0, a1;
+    chunk_range(c, a0, a1);
+    const uint32_t bytes = (uint32_t)((a1 - a0) * 8);
+    mbar_arrive_expect_tx(&bar[buf], bytes);
+    bulk_g2s(sv + buf * A.buf_elems, A.vals + a0, bytes, &bar[buf]);
+  };
+  int64_t c = blockIdx.x;
+  if (tid == 0 && c < A.nchunks) issue(c, 0);
+  uint32_t phase[2] = {0, 0};
+  const int rloc = tid / TPR, sub = tid % TPR;
+  const int64_t n12 = A.n1 * A.n2;
+  for (int buf = 0; c < A.nchunks; c += gridDim.x, buf ^= 1) {
+    const int64_t cn = c + gridDim.x;
+    if (tid == 0 && cn < A.nchunks) issue(cn, buf ^ 1);
+    mbar_wait(&bar[buf], phase[buf]);
+    phase[buf] ^= 1;
+    int64_t a0, a1;
+    chunk_range(c, a0, a1);
+    const double* s = sv + buf * A.buf_elems;
+    const int64_t row = c * R + rloc;
+    double acc = 0.0;
+    if (rloc < R && row < A.N) {
+      const int64_t i1 = row % A.n1, t = row / A.n1;
+      const int64_t i2 = t % A.n2, i3 = t / A.n2;
+      const int w1 = A.w1[i1], w2 = A.w2[i2], w3 = A.w3[i3];
+      const int64_t off = A.pre3[i3] * A.S2 * A.S1 + (int64_t)w3 * A.pre2[i2] * A.S1 + (int64_t)w3 * w2 * A.pre1[i1] - a0;
+      const int64_t xb = (int64_t)A.st3[i3] * n12 + (int64_t)A.st2[i2] * A.n1 + A.st1[i1];
+      const int npair = w3 * w2;
+      for (int q = sub; q < npair; q += TPR) {
+        const int a = q / w2, b = q - a * w2;
+        const double* xv = A.x + xb + (int64_t)a * n12 + (int64_t)b * A.n1;
+        const double* vv = s + off + (int64_t)q * w1;
+        for (int cc = 0; cc < w1; ++cc) acc = fma(vv[cc], __ldg(xv + cc), acc);
+      }
+    }
+#pragma unroll
+    for (int o = TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (sub == 0 && rloc < R && row < A.N) A.y[row] = acc;
+    __syncthreads();
+  }
+}
+
+int64_t host_row_offset(const fdiga_stencil* S, int64_t row) {
+  const int64_t i1 = row % S->n[0], t = row / S->n[0];
+  const int64_t i2 = t % S->n[1], i3 = t / S->n[1];
+  const int64_t S1 = S->hpre[0][S->n[0]], S2 = S->hpre[1][S->n[1]];
+  const int64_t w3 = S->hwidth[2][i3], w2 = S->hwidth[1][i2];
+  return S->hpre[2][i3] * S2 * S1 + w3 * S->hpre[1][i2] * S1 + w3 * w2 * S->hpre[0][i1];
+}
+
+MvArgs make_mv_args(const fdiga_stencil* S, const double* x, double* y) {
+  MvArgs A{};
+  A.n1 = S->n[0];
+  A.n2 = S->n[1];
+  A.n3 = S->n[2];
+  A.N = S->N;
+  A.S1 = S->hpre[0][S->n[0]];
+  A.S2 = S->hpre[1][S->n[1]];
+  A.rows_per_chunk = S->rows_per_chunk;
+  A.nchunks = S->nchunks;
+  A.buf_elems = S->max_chunk_vals;
+  A.nnz = S->nnz;
+  A.st1 = S->start[0];
+  A.st2 = S->start[1];
+  A.st3 = S->start[2];
+  A.w1 = S->width[0];
+  A.w2 = S->width[1];
+  A.w3 = S->width[2];
+  A.pre1 = S->pre[0];
+  A.pre2 = S->pre[1];
+  A.pre3 = S->pre[2];
+  A.vals = S->vals;
+  A.x = x;
+  A.y = y;
+  return A;
+}
+
+// Common tail of stencil_create / colloc_assemble: tables on the device, launch plan.
+int finish_stencil(fdiga_stencil* S) {
+  for (int l = 0; l < 3; ++l) {
+    const int64_t nl = S->n[l];
+    S->hpre[l].assign(nl + 1, 0);
+    for (int64_t i = 0; i < nl; ++i) {
+      FDIGA_CHECK(S->hwidth[l][i] >= 1 && S->hstart[l][i] >= 0 && S->hstart[l][i] + S->hwidth[l][i] <= nl,
+                  FDIGA_ERR_INVALID_ARG, "bad window in direction %d at %lld", l, (long long)i);
+      S->hpre[l][i + 1] = S->hpre[l][i] + S->hwidth[l][i];
+      S->wmax = std::max<int>(S->wmax, S->hwidth[l][i]);
+    }
+    FDIGA_CUDA(cudaMalloc(&S->start[l], nl * sizeof(int32_t)));
+    FDIGA_CUDA(cudaMalloc(&S->width[l], nl * sizeof(int32_t)));
+    FDIGA_CUDA(cudaMalloc(&S->pre[l], (nl + 1) * sizeof(int64_t)));
+    FDIGA_CUDA(cudaMemcpy(S->start[l], S->hstart[l].data(), nl * sizeof(int32_t), cudaMemcpyHostToDevice));
+    FDIGA_CUDA(cudaMemcpy(S->width[l], S->hwidth[l].data(), nl * sizeof(int32_t), cudaMemcpyHostToDevice));
+    FDIGA_CUDA(cudaMemcpy(S->pre[l], S->hpre[l].data(), (nl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  S->nnz = S->hpre[0][S->n[0]] * S->hpre[1][S->n[1]] * S->hpre[2][S->n[2]];
+  // launch plan: rows per chunk and threads per row from the mean row length
+  const double per_row = (double)S->nnz / (double)S->N;
+  S->threads = 256;
+  S->tpr = per_row > 48 ? 4 : 2;
+  S->rows_per_chunk = S->threads / S->tpr;
+  S->nchunks = (S->N + S->rows_per_chunk - 1) / S->rows_per_chunk;
+  int64_t mx = 0;
+  for (int64_t c = 0; c < S->nchunks; ++c) {
+    const int64_t r0 = c * S->rows_per_chunk, r1 = std::min<int64_t>(r0 + S->rows_per_chunk, S->N);
+    const int64_t o0 = host_row_offset(S, r0), o1 = (r1 >= S->N) ? S->nnz : host_row_offset(S, r1);
+    mx = std::max(mx, ((o1 + 1) & ~int64_t(1)) - (o0 & ~int64_t(1)));
+  }
+  S->max_chunk_vals = mx;
+  FDIGA_CUDA(cudaDeviceSynchronize());
+  FDIGA_CHECK(2 * mx * 8 <= 220 * 1024, FDIGA_ERR_NOT_SUPPORTED, "matvec chunk too large for shared memory");
+  return FDIGA_OK;
+}
+
+fdiga_stencil* new_stencil(fdiga_ctx* ctx, int d, const int64_t* n) {
+  fdiga_stencil* S = new fdiga_stencil();
+  S->ctx = ctx;
+  S->d = d;
+  S->N = 1;
+  for (int l = 0; l < 3; ++l) {
+    S->n[l] = l < d ? n[l] : 1;
+    S->N *= S->n[l];
+  }
+  if (d == 2) {  // dummy third direction: one plane, window {0}
+    S->hstart[2].assign(1, 0);
+    S->hwidth[2].assign(1, 1);
+  }
+  return S;
+}
+
+}  // namespace
+
+extern "C" {
+
+int stencil_destroy(fdiga_stencil* S) {
+  if (!S) return FDIGA_OK;
+  cudaSetDevice(S->ctx->device);
+  for (int l = 0; l < 3; ++l) {
+    cudaFree(S->start[l]);
+    cudaFree(S->width[l]);
+    cudaFree(S->pre[l]);
+  }
+  cudaFree(S->vals);
+  delete S;
+  return FDIGA_OK;
+}
+
+int stencil_create(fdiga_ctx* ctx, int d, const int64_t* n, const int32_t* const* start, const int32_t* const* width,
+                   const double* values, int values_on_device, fdiga_stencil** out) {
+  FDIGA_CHECK(ctx && n && start && width && values && out, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_CHECK(d == 2 || d == 3, FDIGA_ERR_INVALID_ARG, "d must be 2 or 3");
+  FDIGA_CHECK(ctx->nranks == 1, FDIGA_ERR_NOT_SUPPORTED, "multi-rank stencil is not built in this version");
+  *out = nullptr;
+  FDIGA_TRY(bind(ctx));
+  fdiga_stencil* S = new_stencil(ctx, d, n);
+  for (int l = 0; l < d; ++l) {
+    S->hstart[l].assign(start[l], start[l] + n[l]);
+    S->hwidth[l].assign(width[l], width[l] + n[l]);
+  }
+  int s = finish_stencil(S);
+  if (s == FDIGA_OK) {
+    cudaError_t e = cudaMalloc(&S->vals, (S->nnz + 2) * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemset(S->vals, 0, (S->nnz + 2) * sizeof(double));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(S->vals, values, S->nnz * sizeof(double),
+                     values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      set_error("stencil_create: %s", cudaGetErrorString(e));
+      s = FDIGA_ERR_CUDA;
+    }
+  }
+  if (s != FDIGA_OK) {
+    stencil_destroy(S);
+    return s;
+  }
+  *out = S;
+  return FDIGA_OK;
+}
+
+int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
+                    fdiga_stencil** out) {
+  FDIGA_CHECK(ctx && ne && out, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_CHECK(d == 2 || d == 3, FDIGA_ERR_INVALID_ARG, "d must be 2 or 3");
+  FDIGA_CHECK(p >= 1 && p <= 8, FDIGA_ERR_INVALID_ARG, "degree p = %d out of range", p);
+  FDIGA_CHECK(ctx->nranks == 1, FDIGA_ERR_NOT_SUPPORTED, "multi-rank stencil is not built in this version");
+  const bool ok_geo = geometry_id == FDIGA_GEOM_IDENTITY || (geometry_id == FDIGA_GEOM_ANNULUS && d == 2) ||
+                      ((geometry_id == FDIGA_GEOM_DEFORMED_CUBE || geometry_id == FDIGA_GEOM_THICK_RING) && d == 3);
+  FDIGA_CHECK(ok_geo, FDIGA_ERR_INVALID_ARG, "geometry %d not available in %dD", geometry_id, d);
+  *out = nullptr;
+  FDIGA_TRY(bind(ctx));
+  Table1D T[3];
+  int64_t n[3] = {1, 1, 1};
+  for (int l = 0; l < d; ++l) {
+    FDIGA_CHECK(ne[l] >= 1 && ne[l] + p - 2 >= 1, FDIGA_ERR_INVALID_ARG, "bad ne[%d]", l);
+    build_table(p, ne[l], T[l]);
+    n[l] = T[l].n;
+  }
+  fdiga_stencil* S = new_stencil(ctx, d, n);
+  for (int l = 0; l < d; ++l) {
+    S->hstart[l] = T[l].start;
+    S->hwidth[l] = T[l].width;
+  }
+  int s = finish_stencil(S);
+  std::vector<void*> tmp;
+  auto dev_copy = [&](const void* h, size_t bytes, void** dptr) -> int {
+    FDIGA_CUDA(cudaMalloc(dptr, bytes));
+    tmp.push_back(*dptr);
+    FDIGA_CUDA(cudaMemcpy(*dptr, h, bytes, cudaMemcpyHostToDevice));
+    return FDIGA_OK;
+  };
+  AsmArgs A{};
+  if (s == FDIGA_OK) {
+    A.wmax = p + 1;
+    A.n1 = n[0];
+    A.n2 = n[1];
+    A.n3 = n[2];
+    A.S1 = S->hpre[0][n[0]];
+    A.S2 = S->hpre[1][n[1]];
+    A.geo.id = geometry_id;
+    for (int k = 0; k < 4; ++k) A.geo.prm[k] = 0;
+    const int np = geometry_id == FDIGA_GEOM_ANNULUS ? 2 : geometry_id == FDIGA_GEOM_DEFORMED_CUBE ? 1
+                                                         : geometry_id == FDIGA_GEOM_THICK_RING  ? 3 : 0;
+    FDIGA_CHECK(np == 0 || geo_params, FDIGA_ERR_INVALID_ARG, "geometry %d needs %d parameters", geometry_id, np);
+    for (int k = 0; k < np; ++k) A.geo.prm[k] = geo_params[k];
+    const double* taus[3] = {nullptr, nullptr, nullptr};
+    const double* tabs[3] = {nullptr, nullptr, nullptr};
+    for (int l = 0; l < d && s == FDIGA_OK; ++l) {
+      std::vector<double> tab;
+      for (int r = 0; r < 3; ++r) tab.insert(tab.end(), T[l].val[r].begin(), T[l].val[r].end());
+      void* dp = nullptr;
+      s = dev_copy(T[l].tau.data(), n[l] * 8, &dp);
+      taus[l] = (const double*)dp;
+      if (s == FDIGA_OK) s = dev_copy(tab.data(), tab.size() * 8, &dp);
+      tabs[l] = (const double*)dp;
+    }
+    A.tau1 = taus[0];
+    A.tau2 = taus[1];
+    A.tau3 = taus[2];
+    A.tab1 = tabs[0];
+    A.tab2 = tabs[1];
+    A.tab3 = tabs[2];
+    A.w1 = S->width[0];
+    A.w2 = S->width[1];
+    A.w3 = S->width[2];
+    A.pre1 = S->pre[0];
+    A.pre2 = S->pre[1];
+    A.pre3 = S->pre[2];
+  }
+  if (s == FDIGA_OK) {
+    cudaError_t e = cudaMalloc(&S->vals, (S->nnz + 2) * sizeof(double));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemsetAsync(S->vals, 0, (S->nnz + 2) * sizeof(double), ctx->stream);
+    if (e == cudaSuccess) {
+      A.vals = S->vals;
+      const int64_t blocks = (S->N + 127) / 128;
+      if (d == 3)
+        assemble_kernel<3><<<(unsigned)blocks, 128, 0, ctx->stream>>>(A);
+      else
+        assemble_kernel<2><<<(unsigned)blocks, 128, 0, ctx->stream>>>(A);
+      count_launch(ctx);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+      set_error("colloc_assemble: %s", cudaGetErrorString(e));
+      s = FDIGA_ERR_CUDA;
+    }
+  }
+  for (void* q : tmp) cudaFree(q);
+  if (s != FDIGA_OK) {
+    stencil_destroy(S);
+    return s;
+  }
+  *out = S;
+  return FDIGA_OK;
+}
+
+int stencil_matvec(fdiga_stencil* S, const double* x, double* y) {
+  FDIGA_CHECK(S && x && y, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_CHECK(x != y, FDIGA_ERR_INVALID_ARG, "stencil_matvec: x and y must not alias");
+  fdiga_ctx* ctx = S->ctx;
+  FDIGA_TRY(bind(ctx));
+  MvArgs A = make_mv_args(S, x, y);
+  const size_t smem = 2 * (size_t)S->max_chunk_vals * sizeof(double);
+  auto kern = S->tpr == 4 ? matvec_kernel<4> : matvec_kernel<2>;
+  FDIGA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  FDIGA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S->threads, smem));
+  per_sm = std::max(per_sm, 1);
+  const int64_t grid = std::min<int64_t>(S->nchunks, (int64_t)per_sm * ctx->sm_count);
+  kern<<<(unsigned)grid, S->threads, smem, ctx->stream>>>(A);
+  count_launch(ctx);
+  FDIGA_CUDA(cudaGetLastError());
+  return FDIGA_OK;
+}
+
+int stencil_info(const fdiga_stencil* S, int64_t* nnz, int64_t* n_out, int32_t* start_l0, int32_t* width_l0) {
+  FDIGA_CHECK(S, FDIGA_ERR_INVALID_ARG, "NULL stencil");
+  if (nnz) *nnz = S->nnz;
+  if (n_out)
+    for (int l = 0; l < S->d; ++l) n_out[l] = S->n[l];
+  if (start_l0) std::memcpy(start_l0, S->hstart[0].data(), S->n[0] * sizeof(int32_t));
+  if (width_l0) std::memcpy(width_l0, S->hwidth[0].data(), S->n[0] * sizeof(int32_t));
+  return FDIGA_OK;
+}
+
+int stencil_get_values(const fdiga_stencil* S, double* values_host) {
+  FDIGA_CHECK(S && values_host, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_TRY(bind(S->ctx));
+  FDIGA_CUDA(cudaStreamSynchronize(S->ctx->stream));
+  FDIGA_CUDA(cudaMemcpy(values_host, S->vals, S->nnz * sizeof(double), cudaMemcpyDeviceToHost));
+  return FDIGA_OK;
+}
+
+int colloc_1d_factors(int p, int64_t ne, double* M, double* K) {
+  FDIGA_CHECK(M && K && p >= 1 && ne >= 1, FDIGA_ERR_INVALID_ARG, "bad colloc_1d_factors arguments");
+  Table1D T;
+  build_table(p, ne, T);
+  const int64_t n = T.n;
+  std::memset(M, 0, n * n * sizeof(double));
+  std::memset(K, 0, n * n * sizeof(double));
+  for (int64_t i = 0; i < n; ++i)
+    for (int c = 0; c < T.width[i]; ++c) {
+      M[i * n + T.start[i] + c] = T.val[0][i * T.wmax + c];
+      K[i * n + T.start[i] + c] = -T.val[2][i * T.wmax + c];
+    }
+  return FDIGA_OK;
+}
+
+}  // extern "C"
