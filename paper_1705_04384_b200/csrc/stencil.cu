@@ -33,11 +33,14 @@ struct fdiga_stencil {
   int32_t* start[3] = {nullptr, nullptr, nullptr};
   int32_t* width[3] = {nullptr, nullptr, nullptr};
   int64_t* pre[3] = {nullptr, nullptr, nullptr};
-  double* vals = nullptr;         // nnz (+2 padding) values, canonical layout
-  // matvec launch plan
-  int rows_per_chunk = 0, tpr = 0, threads = 0;
-  int64_t nchunks = 0;
-  int64_t max_chunk_vals = 0;     // doubles staged per chunk (incl. alignment slack)
+  double* vals = nullptr;         // nnz values, INTERNAL layout (see below)
+  // internal "line-SoA" layout: the values of line (i3, i2) occupy the same range as in the canonical
+  // layout, ordered [q = a*w2 + b][c][i1 among the rows of the line with w1(i1) > c], so a warp of
+  // consecutive rows reads consecutive addresses for every (q, c).  voff1[i1 * wm1 + c] is the offset
+  // of (i1, c) inside one q-block of S1 values.
+  int wm1 = 0;                    // max window width in direction 1
+  int32_t* voff1 = nullptr;       // device, n1 x wm1
+  std::vector<int32_t> hvoff1;
 };
 
 namespace {
@@ -242,6 +245,8 @@ struct AsmArgs {
   const int32_t *w1, *w2, *w3;
   const int64_t *pre1, *pre2, *pre3;
   const double *tab1, *tab2, *tab3;  // tab_l[(r * n_l + i) * wmax + c] = B^{(r)}_{start_l(i)+c}(tau_{l,i})
+  const int32_t* voff1;              // internal layout offsets (n1 x wm1)
+  int wm1;
   Geo geo;
   double* vals;
 };
@@ -285,8 +290,8 @@ __global__ void assemble_kernel(AsmArgs A) {
   const int w1 = A.w1[i1];
   const int w2 = A.w2[i2];
   const int w3 = (D == 3) ? A.w3[i3] : 1;
-  const int64_t off = (D == 3 ? A.pre3[i3] * A.S2 * A.S1 : 0) + (int64_t)w3 * A.pre2[i2] * A.S1 +
-                      (int64_t)w3 * w2 * A.pre1[i1];
+  const int64_t line = (D == 3 ? A.pre3[i3] * A.S2 * A.S1 : 0) + (int64_t)w3 * A.pre2[i2] * A.S1;
+  const int32_t* vo = A.voff1 + i1 * A.wm1;
   // 1D factor rows at this point: f_l[r] = &tab_l[(r n_l + i_l) W]
   const double* f1[3];
   const double* f2[3];
@@ -297,7 +302,7 @@ __global__ void assemble_kernel(AsmArgs A) {
     f2[r] = A.tab2 + (r * A.n2 + i2) * W;
     f3[r] = (D == 3) ? A.tab3 + (r * A.n3 + i3) * W : nullptr;
   }
-  double* out = A.vals + off;
+  double* out = A.vals + line;
   for (int a = 0; a < w3; ++a)
     for (int b = 0; b < w2; ++b)
       for (int c = 0; c < w1; ++c) {
@@ -319,106 +324,94 @@ __global__ void assemble_kernel(AsmArgs A) {
           if (D == 3) prod *= f3[t3][a];
           v += prod;
         }
-        out[((int64_t)a * w2 + b) * w1 + c] = v;
+        out[((int64_t)a * w2 + b) * A.S1 + vo[c]] = v;
       }
 }
 
 // ------------------------------------------------------------------ matvec
 struct MvArgs {
   int64_t n1, n2, n3, N, S1, S2;
-  int rows_per_chunk;
-  int64_t nchunks;
-  int64_t buf_elems;  // doubles per smem buffer
-  int64_t nnz;
   const int32_t *st1, *st2, *st3, *w1, *w2, *w3;
-  const int64_t *pre1, *pre2, *pre3;
+  const int64_t *pre2, *pre3;
+  const int32_t* voff1;
   const double* vals;
   const double* x;
   double* y;
 };
 
-__device__ __forceinline__ int64_t row_offset(const MvArgs& A, int64_t row) {
-  const int64_t i1 = row % A.n1, t = row / A.n1;
-  const int64_t i2 = t % A.n2, i3 = t / A.n2;
-  const int64_t w3 = A.w3[i3], w2 = A.w2[i2];
-  return A.pre3[i3] * A.S2 * A.S1 + w3 * A.pre2[i2] * A.S1 + w3 * w2 * A.pre1[i1];
-}
-
-// y = A x.  Persistent CTAs walk chunks of `rows_per_chunk` consecutive rows.  The chunk's values
-// are one contiguous range of the canonical layout, staged global->shared by a single bulk copy
-// (TMA engine, UBLKCP) into a 2-deep ring, so the HBM stream is fully coalesced and prefetched one
-// chunk ahead.  TPR threads share a row (its (a,b) window pairs round-robin) and reduce by shuffles;
-// x is read through L1/L2 (the x window of a row block is reused by its neighbours).
-template <int TPR>
+// y = A x, one thread per row (flattened, i1 fastest).  For every window pair q = (a, b) the thread
+// reads its w1 <= WM values at vals[line + q S1 + voff1(i1, c)] -- consecutive rows hit consecutive
+// addresses, so every warp load is a full 256-byte coalesced stream (values are read exactly once,
+// streaming / evict-first) -- and the matching x window x[(s3+a) n1 n2 + (s2+b) n1 + s1 + c]
+// through L1/L2 (x of neighbouring rows overlaps).  Bytes moved: 8 nnz + 16 N.
+template <int WM>
 __global__ void __launch_bounds__(256) matvec_kernel(MvArgs A) {
-  extern __shared__ __align__(16) double sv[];
-  __shared__ __align__(8) uint64_t bar[2];
-  const int tid = threadIdx.x;
-  const int R = A.rows_per_chunk;
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  const int64_t nnz_total = A.nnz;
-  auto chunk_range = [&](int64_t c, int64_t& a0, int64_t& a1) {
-    const int64_t r0 = c * R;
-    const int64_t r1 = min(r0 + R, A.N);
-    const int64_t o0 = row_offset(A, r0);
-    const int64_t o1 = (r1 >= A.N) ? nnz_total : row_offset(A, r1);
-    a0 = o0 & ~int64_t(1);
-    a1 = (o1 + 1) & ~int64_t(1);
-  };
-  auto issue = [&](int64_t c, int buf) {
-    int64_t a0, a1;
-    chunk_range(c, a0, a1);
-    const uint32_t bytes = (uint32_t)((a1 - a0) * 8);
-    mbar_arrive_expect_tx(&bar[buf], bytes);
-    bulk_g2s(sv + buf * A.buf_elems, A.vals + a0, bytes, &bar[buf]);
-  };
-  int64_t c = blockIdx.x;
-  if (tid == 0 && c < A.nchunks) issue(c, 0);
-  uint32_t phase[2] = {0, 0};
-  const int rloc = tid / TPR, sub = tid % TPR;
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= A.N) return;
+  const int64_t i1 = r % A.n1, line = r / A.n1;
+  const int64_t i2 = line % A.n2, i3 = line / A.n2;
+  const int w1 = A.w1[i1], w2 = A.w2[i2], w3 = A.w3[i3];
+  int vo[WM];
+#pragma unroll
+  for (int c = 0; c < WM; ++c) vo[c] = (c < w1) ? A.voff1[i1 * WM + c] : 0;
   const int64_t n12 = A.n1 * A.n2;
-  for (int buf = 0; c < A.nchunks; c += gridDim.x, buf ^= 1) {
-    const int64_t cn = c + gridDim.x;
-    if (tid == 0 && cn < A.nchunks) issue(cn, buf ^ 1);
-    mbar_wait(&bar[buf], phase[buf]);
-    phase[buf] ^= 1;
-    int64_t a0, a1;
-    chunk_range(c, a0, a1);
-    const double* s = sv + buf * A.buf_elems;
-    const int64_t row = c * R + rloc;
-    double acc = 0.0;
-    if (rloc < R && row < A.N) {
-      const int64_t i1 = row % A.n1, t = row / A.n1;
-      const int64_t i2 = t % A.n2, i3 = t / A.n2;
-      const int w1 = A.w1[i1], w2 = A.w2[i2], w3 = A.w3[i3];
-      const int64_t off = A.pre3[i3] * A.S2 * A.S1 + (int64_t)w3 * A.pre2[i2] * A.S1 + (int64_t)w3 * w2 * A.pre1[i1] - a0;
-      const int64_t xb = (int64_t)A.st3[i3] * n12 + (int64_t)A.st2[i2] * A.n1 + A.st1[i1];
-      const int npair = w3 * w2;
-      for (int q = sub; q < npair; q += TPR) {
-        const int a = q / w2, b = q - a * w2;
-        const double* xv = A.x + xb + (int64_t)a * n12 + (int64_t)b * A.n1;
-        const double* vv = s + off + (int64_t)q * w1;
-        for (int cc = 0; cc < w1; ++cc) acc = fma(vv[cc], __ldg(xv + cc), acc);
+  const double* vb = A.vals + A.pre3[i3] * A.S2 * A.S1 + (int64_t)w3 * A.pre2[i2] * A.S1;
+  const double* xb = A.x + (int64_t)A.st3[i3] * n12 + (int64_t)A.st2[i2] * A.n1 + A.st1[i1];
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int a = 0; a < w3; ++a) {
+    const double* xa = xb + a * n12;
+    int b = 0;
+    for (; b + 1 < w2; b += 2) {
+      const double* v0 = vb + (int64_t)(a * w2 + b) * A.S1;
+      const double* v1 = v0 + A.S1;
+      const double* x0 = xa + (int64_t)b * A.n1;
+      const double* x1 = x0 + A.n1;
+#pragma unroll
+      for (int c = 0; c < WM; ++c) {
+        if (c < w1) {
+          acc0 = fma(__ldcs(v0 + vo[c]), __ldg(x0 + c), acc0);
+          acc1 = fma(__ldcs(v1 + vo[c]), __ldg(x1 + c), acc1);
+        }
       }
     }
+    if (b < w2) {
+      const double* v0 = vb + (int64_t)(a * w2 + b) * A.S1;
+      const double* x0 = xa + (int64_t)b * A.n1;
 #pragma unroll
-    for (int o = TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (sub == 0 && rloc < R && row < A.N) A.y[row] = acc;
-    __syncthreads();
+      for (int c = 0; c < WM; ++c)
+        if (c < w1) acc0 = fma(__ldcs(v0 + vo[c]), __ldg(x0 + c), acc0);
+    }
   }
+  A.y[r] = acc0 + acc1;
 }
 
-int64_t host_row_offset(const fdiga_stencil* S, int64_t row) {
-  const int64_t i1 = row % S->n[0], t = row / S->n[0];
-  const int64_t i2 = t % S->n[1], i3 = t / S->n[1];
-  const int64_t S1 = S->hpre[0][S->n[0]], S2 = S->hpre[1][S->n[1]];
-  const int64_t w3 = S->hwidth[2][i3], w2 = S->hwidth[1][i2];
-  return S->hpre[2][i3] * S2 * S1 + w3 * S->hpre[1][i2] * S1 + w3 * w2 * S->hpre[0][i1];
+// canonical <-> internal value layouts (one thread per row)
+struct PermArgs {
+  int64_t n1, n2, n3, N, S1, S2;
+  const int32_t *w1, *w2, *w3;
+  const int64_t *pre1, *pre2, *pre3;
+  const int32_t* voff1;
+  int wm1;
+  const double* src;
+  double* dst;
+  int to_internal;
+};
+
+__global__ void permute_kernel(PermArgs P) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= P.N) return;
+  const int64_t i1 = r % P.n1, line = r / P.n1;
+  const int64_t i2 = line % P.n2, i3 = line / P.n2;
+  const int w1 = P.w1[i1], w2 = P.w2[i2], w3 = P.w3[i3];
+  const int64_t lb = P.pre3[i3] * P.S2 * P.S1 + (int64_t)w3 * P.pre2[i2] * P.S1;
+  const int64_t cb = lb + (int64_t)w3 * w2 * P.pre1[i1];
+  for (int q = 0; q < w3 * w2; ++q)
+    for (int c = 0; c < w1; ++c) {
+      const int64_t ci = cb + (int64_t)q * w1 + c;
+      const int64_t ii = lb + (int64_t)q * P.S1 + P.voff1[i1 * P.wm1 + c];
+      if (P.to_internal) P.dst[ii] = P.src[ci];
+      else P.dst[ci] = P.src[ii];
+    }
 }
 
 MvArgs make_mv_args(const fdiga_stencil* S, const double* x, double* y) {
@@ -429,26 +422,48 @@ MvArgs make_mv_args(const fdiga_stencil* S, const double* x, double* y) {
   A.N = S->N;
   A.S1 = S->hpre[0][S->n[0]];
   A.S2 = S->hpre[1][S->n[1]];
-  A.rows_per_chunk = S->rows_per_chunk;
-  A.nchunks = S->nchunks;
-  A.buf_elems = S->max_chunk_vals;
-  A.nnz = S->nnz;
   A.st1 = S->start[0];
   A.st2 = S->start[1];
   A.st3 = S->start[2];
   A.w1 = S->width[0];
   A.w2 = S->width[1];
   A.w3 = S->width[2];
-  A.pre1 = S->pre[0];
   A.pre2 = S->pre[1];
   A.pre3 = S->pre[2];
+  A.voff1 = S->voff1;
   A.vals = S->vals;
   A.x = x;
   A.y = y;
   return A;
 }
 
-// Common tail of stencil_create / colloc_assemble: tables on the device, launch plan.
+int permute_values(fdiga_stencil* S, const double* src, double* dst, int to_internal) {
+  PermArgs P{};
+  P.n1 = S->n[0];
+  P.n2 = S->n[1];
+  P.n3 = S->n[2];
+  P.N = S->N;
+  P.S1 = S->hpre[0][S->n[0]];
+  P.S2 = S->hpre[1][S->n[1]];
+  P.w1 = S->width[0];
+  P.w2 = S->width[1];
+  P.w3 = S->width[2];
+  P.pre1 = S->pre[0];
+  P.pre2 = S->pre[1];
+  P.pre3 = S->pre[2];
+  P.voff1 = S->voff1;
+  P.wm1 = S->wm1;
+  P.src = src;
+  P.dst = dst;
+  P.to_internal = to_internal;
+  permute_kernel<<<(unsigned)((S->N + 255) / 256), 256, 0, S->ctx->stream>>>(P);
+  count_launch(S->ctx);
+  FDIGA_CUDA(cudaGetLastError());
+  FDIGA_CUDA(cudaStreamSynchronize(S->ctx->stream));
+  return FDIGA_OK;
+}
+
+// Common tail of stencil_create / colloc_assemble: tables on the device, internal-layout offsets.
 int finish_stencil(fdiga_stencil* S) {
   for (int l = 0; l < 3; ++l) {
     const int64_t nl = S->n[l];
@@ -467,21 +482,24 @@ int finish_stencil(fdiga_stencil* S) {
     FDIGA_CUDA(cudaMemcpy(S->pre[l], S->hpre[l].data(), (nl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
   S->nnz = S->hpre[0][S->n[0]] * S->hpre[1][S->n[1]] * S->hpre[2][S->n[2]];
-  // launch plan: rows per chunk and threads per row from the mean row length
-  const double per_row = (double)S->nnz / (double)S->N;
-  S->threads = 256;
-  S->tpr = per_row > 48 ? 4 : 2;
-  S->rows_per_chunk = S->threads / S->tpr;
-  S->nchunks = (S->N + S->rows_per_chunk - 1) / S->rows_per_chunk;
-  int64_t mx = 0;
-  for (int64_t c = 0; c < S->nchunks; ++c) {
-    const int64_t r0 = c * S->rows_per_chunk, r1 = std::min<int64_t>(r0 + S->rows_per_chunk, S->N);
-    const int64_t o0 = host_row_offset(S, r0), o1 = (r1 >= S->N) ? S->nnz : host_row_offset(S, r1);
-    mx = std::max(mx, ((o1 + 1) & ~int64_t(1)) - (o0 & ~int64_t(1)));
+  FDIGA_CHECK(S->hpre[0][S->n[0]] < (int64_t(1) << 31), FDIGA_ERR_NOT_SUPPORTED, "direction-1 windows too large");
+  // internal layout: column-major over c within each q-block, rows of the line compacted per column
+  const int64_t n1 = S->n[0];
+  int wm1 = 0;
+  for (int64_t i = 0; i < n1; ++i) wm1 = std::max<int>(wm1, S->hwidth[0][i]);
+  FDIGA_CHECK(wm1 <= 9, FDIGA_ERR_NOT_SUPPORTED, "direction-1 window width %d > 9", wm1);
+  S->wm1 = wm1;
+  S->hvoff1.assign(n1 * wm1, 0);
+  int64_t colpre = 0;
+  for (int c = 0; c < wm1; ++c) {
+    int64_t rank = 0;
+    for (int64_t i = 0; i < n1; ++i)
+      if (S->hwidth[0][i] > c) S->hvoff1[i * wm1 + c] = (int32_t)(colpre + rank++);
+    colpre += rank;
   }
-  S->max_chunk_vals = mx;
+  FDIGA_CUDA(cudaMalloc(&S->voff1, S->hvoff1.size() * sizeof(int32_t)));
+  FDIGA_CUDA(cudaMemcpy(S->voff1, S->hvoff1.data(), S->hvoff1.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   FDIGA_CUDA(cudaDeviceSynchronize());
-  FDIGA_CHECK(2 * mx * 8 <= 220 * 1024, FDIGA_ERR_NOT_SUPPORTED, "matvec chunk too large for shared memory");
   return FDIGA_OK;
 }
 
@@ -514,6 +532,7 @@ int stencil_destroy(fdiga_stencil* S) {
     cudaFree(S->pre[l]);
   }
   cudaFree(S->vals);
+  cudaFree(S->voff1);
   delete S;
   return FDIGA_OK;
 }
@@ -531,11 +550,12 @@ int stencil_create(fdiga_ctx* ctx, int d, const int64_t* n, const int32_t* const
     S->hwidth[l].assign(width[l], width[l] + n[l]);
   }
   int s = finish_stencil(S);
+  double* canon = nullptr;
   if (s == FDIGA_OK) {
     cudaError_t e = cudaMalloc(&S->vals, (S->nnz + 2) * sizeof(double));
-    if (e == cudaSuccess) e = cudaMemset(S->vals, 0, (S->nnz + 2) * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&canon, S->nnz * sizeof(double));
     if (e == cudaSuccess)
-      e = cudaMemcpy(S->vals, values, S->nnz * sizeof(double),
+      e = cudaMemcpy(canon, values, S->nnz * sizeof(double),
                      values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -543,6 +563,8 @@ int stencil_create(fdiga_ctx* ctx, int d, const int64_t* n, const int32_t* const
       s = FDIGA_ERR_CUDA;
     }
   }
+  if (s == FDIGA_OK) s = permute_values(S, canon, S->vals, 1);
+  cudaFree(canon);
   if (s != FDIGA_OK) {
     stencil_destroy(S);
     return s;
@@ -619,6 +641,8 @@ int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometr
     A.pre1 = S->pre[0];
     A.pre2 = S->pre[1];
     A.pre3 = S->pre[2];
+    A.voff1 = S->voff1;
+    A.wm1 = S->wm1;
   }
   if (s == FDIGA_OK) {
     cudaError_t e = cudaMalloc(&S->vals, (S->nnz + 2) * sizeof(double));
@@ -655,14 +679,25 @@ int stencil_matvec(fdiga_stencil* S, const double* x, double* y) {
   fdiga_ctx* ctx = S->ctx;
   FDIGA_TRY(bind(ctx));
   MvArgs A = make_mv_args(S, x, y);
-  const size_t smem = 2 * (size_t)S->max_chunk_vals * sizeof(double);
-  auto kern = S->tpr == 4 ? matvec_kernel<4> : matvec_kernel<2>;
-  FDIGA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  FDIGA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S->threads, smem));
-  per_sm = std::max(per_sm, 1);
-  const int64_t grid = std::min<int64_t>(S->nchunks, (int64_t)per_sm * ctx->sm_count);
-  kern<<<(unsigned)grid, S->threads, smem, ctx->stream>>>(A);
+  const unsigned grid = (unsigned)((S->N + 255) / 256);
+  switch (S->wm1) {
+#define FDIGA_MV_CASE(W) \
+  case W:                \
+    matvec_kernel<W><<<grid, 256, 0, ctx->stream>>>(A); \
+    break;
+    FDIGA_MV_CASE(1)
+    FDIGA_MV_CASE(2)
+    FDIGA_MV_CASE(3)
+    FDIGA_MV_CASE(4)
+    FDIGA_MV_CASE(5)
+    FDIGA_MV_CASE(6)
+    FDIGA_MV_CASE(7)
+    FDIGA_MV_CASE(8)
+    FDIGA_MV_CASE(9)
+#undef FDIGA_MV_CASE
+    default:
+      FDIGA_CHECK(false, FDIGA_ERR_NOT_SUPPORTED, "window width %d", S->wm1);
+  }
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());
   return FDIGA_OK;
@@ -681,9 +716,18 @@ int stencil_info(const fdiga_stencil* S, int64_t* nnz, int64_t* n_out, int32_t* 
 int stencil_get_values(const fdiga_stencil* S, double* values_host) {
   FDIGA_CHECK(S && values_host, FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_TRY(bind(S->ctx));
-  FDIGA_CUDA(cudaStreamSynchronize(S->ctx->stream));
-  FDIGA_CUDA(cudaMemcpy(values_host, S->vals, S->nnz * sizeof(double), cudaMemcpyDeviceToHost));
-  return FDIGA_OK;
+  double* canon = nullptr;
+  FDIGA_CUDA(cudaMalloc(&canon, S->nnz * sizeof(double)));
+  int s = permute_values(const_cast<fdiga_stencil*>(S), S->vals, canon, 0);
+  if (s == FDIGA_OK) {
+    cudaError_t e = cudaMemcpy(values_host, canon, S->nnz * sizeof(double), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      set_error("stencil_get_values: %s", cudaGetErrorString(e));
+      s = FDIGA_ERR_CUDA;
+    }
+  }
+  cudaFree(canon);
+  return s;
 }
 
 int colloc_1d_factors(int p, int64_t ne, double* M, double* K) {
