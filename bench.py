@@ -315,7 +315,7 @@ def main():
     traffic = None
     if os.path.exists(NCU_SUMMARY):
         try:
-            traffic = json.load(open(NCU_SUMMARY)).get("fd_apply_dram_bytes_per_launch")
+            traffic = json.load(open(NCU_SUMMARY)).get("fd_apply_dram_bytes_per_apply")
         except Exception:
             traffic = None
 
