@@ -69,7 +69,8 @@ struct fdiga_ctx {
   int64_t launches = 0;       // kernels launched by this context
   double* pinned = nullptr;   // small pinned host scratch (scalars coming back from reductions)
   size_t pinned_cap = 0;
-  fdiga::DevBuf ws[4];        // GMRES workspace: basis V, z/w vectors, reduction partials, small results
+  fdiga::DevBuf ws[4];        // GMRES workspace: basis V, z/w vectors, reduction partials, device state
+  void* gmres_graph = nullptr; // cached captured GMRES cycle (krylov.cu)
 };
 
 namespace fdiga {
@@ -80,4 +81,10 @@ inline int bind(const fdiga_ctx* c) {
   return FDIGA_OK;
 }
 int ensure_pinned(fdiga_ctx* c, size_t n_doubles);
+// Internal variants with a device "skip" flag (nonzero: every launch is a no-op), used by the
+// captured GMRES cycle graph for early exit.
+int fd_apply_ex(fd_plan* P, const double* r, double* s, const int* skip);
+int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* skip);
+// Drop the cached GMRES graph (it captures pointers of A, P and the workspace).
+void destroy_gmres_graph(fdiga_ctx* ctx);
 }  // namespace fdiga

@@ -93,6 +93,7 @@ int fdiga_ctx_destroy(fdiga_ctx* c) {
   if (!c) return FDIGA_OK;
   cudaSetDevice(c->device);
   if (c->nccl_comm) fdiga_comm_destroy(c);
+  destroy_gmres_graph(c);
   if (c->pinned) cudaFreeHost(c->pinned);
   for (auto& b : c->ws) b.release();
   if (c->own_stream) cudaStreamDestroy(c->stream);

@@ -2,19 +2,27 @@
 //
 // On sm_100a the only FP64 tensor instruction is the warp-level DMMA.8x8x4 (PTX
 // mma.sync.aligned.m8n8k4.row.col.f64); tcgen05.mma has no f64 kind, so there is no TMEM/UMMA
-// path for FP64 and accumulators live in registers (DESIGN.md "FP64 on Blackwell").
+// path for FP64 and accumulators live in registers (DESIGN.md §5).
 // Measured on the pool's B200: 37.1 TFLOP/s for a register-resident DMMA loop (profiles/r01_peaks_fp64.jsonl).
 //
-//   C[M x N] = A[M x K] * B[K x N]   (+ optional epilogue C /= lam_m[m] + lam_n[n]), batched over blockIdx.z
+//   C[M x N] = A[M x K] * B[K x N]   (+ optional epilogue C /= lam_m[m] + lam_n[n % inner])
 //   A: row-major, k contiguous (lda)
-//   B: BLayout::KN -> B[k*ldb + n] (n contiguous)       used by modes 2..d (left-multiply by the factor)
-//      BLayout::NK -> B[n*ldb + k] (k contiguous)       used by mode 1 (right-multiply by factor^T)
+//   B: BLayout::KN (modes 2..d: left-multiply a strided axis by the factor A = F_l):
+//        column n of B and C lives at colOff(n) = (n / inner) * bstride + n % inner, i.e. the batch of
+//        slices X[i_{l+1}..][0..n_l)[0..inner) is flattened into one long N = inner * batch, so a tile
+//        never straddles padding and ragged n_l only costs the M (= n_l) edge.
+//        B[k][n] = B[colOff(n) + k ldb],  C[m][n] = C[colOff(n) + m ldc]
+//      BLayout::NK (mode 1: right-multiply the contiguous axis by F_1^T):
+//        B[k][n] = B[n ldb + k] (the factor, k contiguous),  C[m][n] = C[m ldc + n]
 //
-// Tiles are staged global->shared with cp.async (16 B when the rows are 16 B aligned, else 8 B),
-// zero-filled outside [M,N,K], into a STAGES-deep ring; shared rows are padded so that the
-// m8n8k4 fragment loads (8 rows x 4 k, or 4 k x 8 cols) are bank-conflict free.
+// One CTA per output tile, 1-D grid ordered so that the tiles sharing the big operand are adjacent
+// (the few tiles along the factor dimension run together and hit the same L2 lines).  Tiles are
+// staged global->shared with cp.async (16 B when rows are 16 B aligned, else 8 B), zero-filled outside
+// [M,N,K], into a STAGES-deep ring; shared rows are padded (stride == 4 mod 16 doubles) so the m8n8k4
+// fragment loads (8 rows x 4 k, or 4 k x 8 cols) are bank-conflict free.
 #pragma once
 #include <cuda_runtime.h>
+
 #include <cstdint>
 
 #include "ptx.cuh"
@@ -26,20 +34,23 @@ enum class BLayout { KN, NK };
 struct GemmParams {
   int M, N, K;
   const double* A;
-  int64_t lda, strideA;
+  int64_t lda;
   const double* B;
-  int64_t ldb, strideB;
+  int64_t ldb;
   double* C;
-  int64_t ldc, strideC;
-  const double* lam_m;  // epilogue divide (nullptr: none): C[m][n] = acc / (lam_m[m] + lam_n[n])
+  int64_t ldc;
+  int64_t inner;        // KN: columns per batch slice (== N when there is a single slice)
+  int64_t bstride;      // KN: elements between consecutive slices of B and C
+  const double* lam_m;  // epilogue divide (nullptr: none): C[m][n] = acc / (lam_m[m] + lam_n[n % inner])
   const double* lam_n;
-  int64_t strideLamN;   // per-batch offset of lam_n (0: shared)
+  const int* skip;      // device flag: nonzero -> the launch does nothing (GMRES graph early exit)
+  int tiles_m, tiles_n;
 };
 
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
 }
 
 template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
@@ -48,9 +59,9 @@ struct TileCfg {
   static constexpr int THREADS = WM * WN * 32;
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int MI = WTM / 8, NJ = WTN / 8;
-  static constexpr int SA = BK + 4;          // A row stride (doubles): == 4 (mod 16) when BK % 16 == 0
-  static constexpr int SBkn = BN + 4;        // B [k][n] row stride
-  static constexpr int SBnk = BK + 4;        // B [n][k] row stride
+  static constexpr int SA = BK + 4;    // A row stride (doubles): == 4 (mod 16) for BK % 16 == 0
+  static constexpr int SBkn = BN + 4;  // B [k][n] row stride (BN % 16 == 0 -> == 4 mod 16; else 8-way split phases)
+  static constexpr int SBnk = BK + 4;  // B [n][k] row stride
   static_assert(WTM % 8 == 0 && WTN % 8 == 0 && BK % 4 == 0, "tile shape");
   static constexpr int A_ELEMS = BM * SA;
   static constexpr int B_ELEMS_KN = BK * SBkn;
@@ -58,12 +69,15 @@ struct TileCfg {
   template <BLayout L>
   __host__ __device__ static constexpr int b_elems() { return L == BLayout::KN ? B_ELEMS_KN : B_ELEMS_NK; }
   template <BLayout L>
-  __host__ __device__ static constexpr size_t smem_bytes() { return size_t(STAGES) * (A_ELEMS + b_elems<L>()) * sizeof(double); }
+  __host__ __device__ static constexpr size_t smem_bytes() {
+    return size_t(STAGES) * (A_ELEMS + b_elems<L>()) * sizeof(double);
+  }
 };
 
 // VA / VB: doubles per cp.async chunk for A / B (2 needs 16-byte aligned rows, else 1).
 template <class T, BLayout BL, int VA, int VB>
 __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) {
+  if (p.skip && *p.skip) return;
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;
   double* sB = smem + T::STAGES * T::A_ELEMS;
@@ -72,19 +86,39 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int warp_m = warp / T::WN, warp_n = warp % T::WN;
-  const int m0 = blockIdx.x * T::BM, n0 = blockIdx.y * T::BN;
-  const int64_t bz = blockIdx.z;
-  const double* __restrict__ A = p.A + bz * p.strideA;
-  const double* __restrict__ B = p.B + bz * p.strideB;
-  double* __restrict__ C = p.C + bz * p.strideC;
+  // tile order: the factor dimension (M for KN, N for NK) runs fastest
+  int mt, nt;
+  if (BL == BLayout::KN) {
+    mt = blockIdx.x % p.tiles_m;
+    nt = blockIdx.x / p.tiles_m;
+  } else {
+    nt = blockIdx.x % p.tiles_n;
+    mt = blockIdx.x / p.tiles_n;
+  }
+  const int m0 = mt * T::BM, n0 = nt * T::BN;
+  const double* __restrict__ A = p.A;
+  const double* __restrict__ B = p.B;
+  double* __restrict__ C = p.C;
   const int M = p.M, N = p.N, K = p.K;
   const int KT = (K + T::BK - 1) / T::BK;
 
+  // KN: per-thread B column offsets are the same for every k-stage (THREADS % (BN / VB) == 0)
+  constexpr int CPR_B_KN = T::BN / VB;
+  static_assert(BL != BLayout::KN || T::THREADS % CPR_B_KN == 0, "B loader mapping");
+  int64_t b_col_off = 0;
+  int b_col_bytes = 0;
+  if (BL == BLayout::KN) {
+    const int gn = n0 + (tid % CPR_B_KN) * VB;
+    if (gn < N) {
+      b_col_off = (int64_t)(gn / p.inner) * p.bstride + gn % p.inner;
+      b_col_bytes = (VB == 2 && gn + 1 >= N) ? 8 : VB * 8;
+    }
+  }
+
   auto load_tile = [&](int stage, int kt) {
     const int k0 = kt * T::BK;
-    // ---- A tile: BM x BK, rows m, cols k
-    {
-      constexpr int CPR = T::BK / VA;  // chunks per row
+    {  // A tile: BM x BK, rows m, cols k
+      constexpr int CPR = T::BK / VA;
       constexpr int CH = T::BM * CPR;
       double* dst = sA + stage * T::A_ELEMS;
 #pragma unroll
@@ -101,21 +135,20 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
         if (VA == 2) cp_async16(d, src, bytes); else cp_async8(d, src, bytes);
       }
     }
-    // ---- B tile
     double* dstB = sB + stage * BE;
     if (BL == BLayout::KN) {
-      constexpr int CPR = T::BN / VB;
-      constexpr int CH = T::BK * CPR;
+      constexpr int CH = T::BK * CPR_B_KN;
+      const int cc = tid % CPR_B_KN;
 #pragma unroll
       for (int c = tid; c < CH; c += T::THREADS) {
-        const int r = c / CPR, cc = c % CPR;
-        const int gk = k0 + r, gn = n0 + cc * VB;
+        const int r = c / CPR_B_KN;
+        const int gk = k0 + r;
         const uint32_t d = smem_u32(dstB + r * T::SBkn + cc * VB);
         int bytes = 0;
         const double* src = B;
-        if (gk < K && gn < N) {
-          bytes = (VB == 2 && gn + 1 >= N) ? 8 : VB * 8;
-          src = B + (int64_t)gk * p.ldb + gn;
+        if (gk < K && b_col_bytes) {
+          bytes = b_col_bytes;
+          src = B + b_col_off + (int64_t)gk * p.ldb;
         }
         if (VB == 2) cp_async16(d, src, bytes); else cp_async8(d, src, bytes);
       }
@@ -183,27 +216,47 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
   cp_async_wait<0>();
 
   // ---- epilogue: optional eigenvalue-sum divide (eq:FD3D diagonal term), store
-  const double* lam_n = p.lam_n ? p.lam_n + bz * p.strideLamN : nullptr;
-  const bool vec_ok = ((p.ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+  const bool c_vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((p.ldc & 1) == 0) &&
+                     (BL == BLayout::NK || ((p.inner & 1) == 0 && (p.bstride & 1) == 0));
 #pragma unroll
-  for (int i = 0; i < T::MI; ++i) {
-    const int row = m0 + warp_m * T::WTM + i * 8 + lr;
-    if (row >= M) continue;
-    const double lm = p.lam_m ? p.lam_m[row] : 0.0;
+  for (int j = 0; j < T::NJ; ++j) {
+    const int col = n0 + warp_n * T::WTN + j * 8 + 2 * lc;
+    if (col >= N) continue;
+    int64_t coff;
+    int64_t lidx = col;
+    if (BL == BLayout::KN) {
+      const int64_t sl = col / p.inner;
+      lidx = col - sl * p.inner;
+      coff = sl * p.bstride + lidx;
+    } else {
+      coff = col;
+    }
+    const bool two = col + 1 < N;
+    // the pair (col, col+1) stays in one slice when inner is even; otherwise recompute for col+1
+    int64_t coff1 = coff + 1, lidx1 = lidx + 1;
+    if (BL == BLayout::KN && two && (p.inner & 1)) {
+      const int64_t sl = (col + 1) / p.inner;
+      lidx1 = (col + 1) - sl * p.inner;
+      coff1 = sl * p.bstride + lidx1;
+    }
+    const double ln0 = p.lam_m ? p.lam_n[lidx] : 0.0;
+    const double ln1 = (p.lam_m && two) ? p.lam_n[lidx1] : 0.0;
 #pragma unroll
-    for (int j = 0; j < T::NJ; ++j) {
-      const int col = n0 + warp_n * T::WTN + j * 8 + 2 * lc;
+    for (int i = 0; i < T::MI; ++i) {
+      const int row = m0 + warp_m * T::WTM + i * 8 + lr;
+      if (row >= M) continue;
       double v0 = acc[i][j][0], v1 = acc[i][j][1];
       if (p.lam_m) {
-        if (col < N) v0 = v0 / (lm + lam_n[col]);
-        if (col + 1 < N) v1 = v1 / (lm + lam_n[col + 1]);
+        const double lm = p.lam_m[row];
+        v0 = v0 / (lm + ln0);
+        v1 = v1 / (lm + ln1);
       }
-      double* dst = C + (int64_t)row * p.ldc + col;
-      if (vec_ok && col + 1 < N) {
-        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+      double* dst = C + (int64_t)row * p.ldc;
+      if (c_vec && two) {
+        *reinterpret_cast<double2*>(dst + coff) = make_double2(v0, v1);
       } else {
-        if (col < N) dst[0] = v0;
-        if (col + 1 < N) dst[1] = v1;
+        dst[coff] = v0;
+        if (two) dst[coff1] = v1;
       }
     }
   }

@@ -13,12 +13,13 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
 
 #include "common.cuh"
-#include "dmma_gemm.cuh"
+#include "fd_gemm.cuh"
 
 using namespace fdiga;
 
@@ -34,45 +35,18 @@ struct fd_plan {
   double* lam_inner = nullptr;  // sum of the eigenvalues of directions 1..d-1 over the flattened inner index
   DevBuf t0, t1;                // ping-pong scratch
   DevBuf host_io;               // device staging for fd_apply_host
+  int cfg[3] = {0, 0, 0};       // autotuned GEMM tile configuration per mode (fd_gemm.cu)
+  float cfg_ms[3] = {0, 0, 0};
   std::vector<double> hU[3], hW[3], hlam[3], hlam_im[3];
 };
 
 namespace {
 
-using Cfg128 = TileCfg<128, 128, 16, 2, 4, 4>;
-
-template <class T, BLayout BL, int VA, int VB>
-int launch_variant(fdiga_ctx* ctx, const GemmParams& p, int batch) {
-  auto kern = dmma_gemm_kernel<T, BL, VA, VB>;
-  constexpr size_t smem = T::template smem_bytes<BL>();
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    FDIGA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
-  dim3 grid((p.M + T::BM - 1) / T::BM, (p.N + T::BN - 1) / T::BN, batch);
-  FDIGA_CHECK(grid.y <= 65535 && grid.z <= 65535, FDIGA_ERR_NOT_SUPPORTED, "GEMM grid too large");
-  kern<<<grid, T::THREADS, smem, ctx->stream>>>(p);
-  count_launch(ctx);
-  FDIGA_CUDA(cudaGetLastError());
-  return FDIGA_OK;
-}
-
-inline bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
-
-template <class T, BLayout BL>
-int launch_gemm(fdiga_ctx* ctx, const GemmParams& p, int batch) {
-  const bool va = aligned16(p.A) && (p.lda % 2 == 0) && (batch == 1 || p.strideA % 2 == 0);
-  const bool vb = aligned16(p.B) && (p.ldb % 2 == 0) && (batch == 1 || p.strideB % 2 == 0);
-  if (va && vb) return launch_variant<T, BL, 2, 2>(ctx, p, batch);
-  if (va) return launch_variant<T, BL, 2, 1>(ctx, p, batch);
-  if (vb) return launch_variant<T, BL, 1, 2>(ctx, p, batch);
-  return launch_variant<T, BL, 1, 1>(ctx, p, batch);
-}
-
-// mode 1: Y(R x n1) = X(R x n1) * F^T
-int mode1(fd_plan* P, const double* F, int64_t ldf, const double* X, double* Y, int64_t R) {
+// mode 1 (contiguous axis): Y(R x n1) = X(R x n1) * F^T
+GemmParams mode1_params(fd_plan* P, const double* F, int64_t ldf, const double* X, double* Y, int64_t R,
+                        const int* skip) {
   GemmParams g{};
+  g.skip = skip;
   g.M = (int)R;
   g.N = (int)P->n[0];
   g.K = (int)P->n[0];
@@ -82,27 +56,68 @@ int mode1(fd_plan* P, const double* F, int64_t ldf, const double* X, double* Y, 
   g.ldb = ldf;
   g.C = Y;
   g.ldc = P->n[0];
-  return launch_gemm<Cfg128, BLayout::NK>(P->ctx, g, 1);
+  g.inner = g.N;
+  return g;
 }
 
-// mode l (>=2): for each of `batch` outer slices, Y(n_l x inner) = F(n_l x n_l) * X(n_l x inner)
-int model(fd_plan* P, int l, const double* F, int64_t ldf, const double* X, double* Y, int64_t inner,
-          int64_t batch, const double* lam_m, const double* lam_n) {
+// mode l >= 2: for every outer slice, Y(n_l x inner) = F(n_l x n_l) * X(n_l x inner); the slices are
+// flattened into one N = inner * batch (dmma_gemm.cuh, BLayout::KN)
+GemmParams model_params(fd_plan* P, int l, const double* F, int64_t ldf, const double* X, double* Y,
+                        int64_t inner, int64_t batch, const double* lam_m, const double* lam_n, const int* skip) {
   GemmParams g{};
+  g.skip = skip;
   g.M = (int)P->n[l];
-  g.N = (int)inner;
+  g.N = (int)(inner * batch);
   g.K = (int)P->n[l];
   g.A = F;
   g.lda = ldf;
   g.B = X;
   g.ldb = inner;
-  g.strideB = inner * P->n[l];
   g.C = Y;
   g.ldc = inner;
-  g.strideC = inner * P->n[l];
+  g.inner = inner;
+  g.bstride = inner * P->n[l];
   g.lam_m = lam_m;
   g.lam_n = lam_n;
-  return launch_gemm<Cfg128, BLayout::KN>(P->ctx, g, (int)batch);
+  return g;
+}
+
+int mode1(fd_plan* P, const double* F, int64_t ldf, const double* X, double* Y, int64_t R, const int* skip) {
+  return gemm_launch(P->ctx, P->ctx->stream, BLayout::NK, P->cfg[0], mode1_params(P, F, ldf, X, Y, R, skip));
+}
+
+int model(fd_plan* P, int l, const double* F, int64_t ldf, const double* X, double* Y, int64_t inner,
+          int64_t batch, const double* lam_m, const double* lam_n, const int* skip) {
+  return gemm_launch(P->ctx, P->ctx->stream, BLayout::KN, P->cfg[l],
+                     model_params(P, l, F, ldf, X, Y, inner, batch, lam_m, lam_n, skip));
+}
+
+// Pick the tile configuration of every mode product of this plan by timing them on the plan's scratch.
+int autotune_plan(fd_plan* P) {
+  const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
+  double* a = P->t0.p;
+  double* b = P->t1.p;
+  FDIGA_CUDA(cudaMemsetAsync(a, 0, P->N * sizeof(double), P->ctx->stream));
+  const int64_t rows1 = (P->d == 2) ? n2 : n2 * n3;
+  FDIGA_TRY(gemm_autotune(P->ctx, BLayout::NK, mode1_params(P, P->W[0], P->ld[0], a, b, rows1, nullptr), &P->cfg[0],
+                          &P->cfg_ms[0]));
+  if (P->d == 2) {
+    FDIGA_TRY(gemm_autotune(P->ctx, BLayout::KN, model_params(P, 1, P->W[1], P->ld[1], a, b, n1, 1, nullptr, nullptr,
+                                                              nullptr), &P->cfg[1], &P->cfg_ms[1]));
+  } else {
+    FDIGA_TRY(gemm_autotune(P->ctx, BLayout::KN, model_params(P, 1, P->W[1], P->ld[1], a, b, n1, n3, nullptr,
+                                                              nullptr, nullptr), &P->cfg[1], &P->cfg_ms[1]));
+    FDIGA_TRY(gemm_autotune(P->ctx, BLayout::KN, model_params(P, 2, P->W[2], P->ld[2], a, b, n1 * n2, 1, nullptr,
+                                                              nullptr, nullptr), &P->cfg[2], &P->cfg_ms[2]));
+  }
+  FDIGA_CUDA(cudaStreamSynchronize(P->ctx->stream));
+  if (getenv("FDIGA_VERBOSE")) {
+    for (int l = 0; l < P->d; ++l)
+      fprintf(stderr, "[fdiga] fd plan n=(%lld,%lld,%lld) mode %d: tile %s, %.1f us\n", (long long)n1,
+              (long long)n2, (long long)n3, l + 1, gemm_config_name(l == 0 ? BLayout::NK : BLayout::KN, P->cfg[l]),
+              1e3 * P->cfg_ms[l]);
+  }
+  return FDIGA_OK;
 }
 
 int upload_factor(const double* h, int64_t n, int64_t ld, double** dptr) {
@@ -149,6 +164,7 @@ int finish_plan(fd_plan* P) {
   FDIGA_TRY(P->t0.ensure(P->N));
   FDIGA_TRY(P->t1.ensure(P->N));
   FDIGA_CUDA(cudaDeviceSynchronize());  // uploads complete before any stream uses the plan
+  FDIGA_TRY(autotune_plan(P));
   return FDIGA_OK;
 }
 
@@ -303,6 +319,32 @@ int compute_W(Solver& S, cudaStream_t st, int64_t n, const double* M, const std:
 }
 
 }  // namespace
+
+namespace fdiga {
+int fd_apply_ex(fd_plan* P, const double* r, double* s, const int* skip) {
+  FDIGA_CHECK(P && r && s, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  fdiga_ctx* ctx = P->ctx;
+  FDIGA_TRY(bind(ctx));
+  double* a = P->t0.p;
+  double* b = P->t1.p;
+  const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
+  if (P->d == 2) {
+    // fwd: mode 1 (W_1), mode 2 (W_2) + divide by lam_2[i2] + lam_1[i1]; bwd: mode 2 (U_2), mode 1 (U_1)
+    FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2, skip));
+    FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, 1, P->lam[1], P->lam_inner, skip));
+    FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, 1, nullptr, nullptr, skip));
+    FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2, skip));
+  } else {
+    FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2 * n3, skip));
+    FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, n3, nullptr, nullptr, skip));
+    FDIGA_TRY(model(P, 2, P->W[2], P->ld[2], b, a, n1 * n2, 1, P->lam[2], P->lam_inner, skip));
+    FDIGA_TRY(model(P, 2, P->U[2], P->ld[2], a, b, n1 * n2, 1, nullptr, nullptr, skip));
+    FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, n3, nullptr, nullptr, skip));
+    FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2 * n3, skip));
+  }
+  return FDIGA_OK;
+}
+}  // namespace fdiga
 
 extern "C" {
 
@@ -467,29 +509,7 @@ int fd_get_factors(const fd_plan* P, int l, double* U, double* W, double* lam_re
   return FDIGA_OK;
 }
 
-int fd_apply(fd_plan* P, const double* r, double* s) {
-  FDIGA_CHECK(P && r && s, FDIGA_ERR_INVALID_ARG, "NULL argument");
-  fdiga_ctx* ctx = P->ctx;
-  FDIGA_TRY(bind(ctx));
-  double* a = P->t0.p;
-  double* b = P->t1.p;
-  const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
-  if (P->d == 2) {
-    // fwd: mode 1 (W_1), mode 2 (W_2) + divide by lam_2[i2] + lam_1[i1]; bwd: mode 2 (U_2), mode 1 (U_1)
-    FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2));
-    FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, 1, P->lam[1], P->lam_inner));
-    FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, 1, nullptr, nullptr));
-    FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2));
-  } else {
-    FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2 * n3));
-    FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, n3, nullptr, nullptr));
-    FDIGA_TRY(model(P, 2, P->W[2], P->ld[2], b, a, n1 * n2, 1, P->lam[2], P->lam_inner));
-    FDIGA_TRY(model(P, 2, P->U[2], P->ld[2], a, b, n1 * n2, 1, nullptr, nullptr));
-    FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, n3, nullptr, nullptr));
-    FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2 * n3));
-  }
-  return FDIGA_OK;
-}
+int fd_apply(fd_plan* P, const double* r, double* s) { return fdiga::fd_apply_ex(P, r, s, nullptr); }
 
 int fd_apply_host(fd_plan* P, const double* r_host, double* s_host) {
   FDIGA_CHECK(P && r_host && s_host, FDIGA_ERR_INVALID_ARG, "NULL argument");
@@ -513,6 +533,7 @@ double fd_apply_flops(const fd_plan* P) {
 int fd_plan_destroy(fd_plan* P) {
   if (!P) return FDIGA_OK;
   cudaSetDevice(P->ctx->device);
+  destroy_gmres_graph(P->ctx);
   for (int l = 0; l < 3; ++l) {
     cudaFree(P->U[l]);
     cudaFree(P->W[l]);

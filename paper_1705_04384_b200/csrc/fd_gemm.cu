@@ -1,0 +1,135 @@
+// Tile configurations of the DMMA mode-product GEMM and their dispatch (see dmma_gemm.cuh).
+//
+// The factor dimension n_l (M for KN, N for NK) is ragged in the Poisson configs (65, 131, 257), so the
+// tile along it comes in several heights (72, 88, 128, 144) and the autotuner picks, per mode shape,
+// the one that wastes least work and keeps the 148 SMs busy; small problems get 4-warp 64-wide tiles.
+#include <algorithm>
+#include <vector>
+
+#include "fd_gemm.cuh"
+
+namespace fdiga {
+namespace {
+
+inline bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
+
+template <class T, BLayout BL, int VA, int VB>
+int launch_variant(fdiga_ctx* ctx, cudaStream_t stream, GemmParams p) {
+  auto kern = dmma_gemm_kernel<T, BL, VA, VB>;
+  constexpr size_t smem = T::template smem_bytes<BL>();
+  static bool attr_set = false;  // per instantiation (single device per process is assumed here)
+  if (!attr_set) {
+    FDIGA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  p.tiles_m = (p.M + T::BM - 1) / T::BM;
+  p.tiles_n = (p.N + T::BN - 1) / T::BN;
+  const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n;
+  FDIGA_CHECK(tiles >= 1 && tiles < (int64_t(1) << 31), FDIGA_ERR_NOT_SUPPORTED, "GEMM grid too large");
+  kern<<<(unsigned)tiles, T::THREADS, smem, stream>>>(p);
+  count_launch(ctx);
+  FDIGA_CUDA(cudaGetLastError());
+  return FDIGA_OK;
+}
+
+template <class T, BLayout BL>
+int launch_cfg(fdiga_ctx* ctx, cudaStream_t stream, const GemmParams& p) {
+  if (BL == BLayout::KN) {
+    // A = the (padded, even-ld) factor: always 16-byte chunks.  B/C = the flattened slices.
+    const bool vb = aligned16(p.B) && (p.ldb % 2 == 0) && (p.inner % 2 == 0) &&
+                    (p.inner == p.N || p.bstride % 2 == 0);
+    return vb ? launch_variant<T, BL, 2, 2>(ctx, stream, p) : launch_variant<T, BL, 2, 1>(ctx, stream, p);
+  } else {
+    const bool va = aligned16(p.A) && (p.lda % 2 == 0);
+    return va ? launch_variant<T, BL, 2, 2>(ctx, stream, p) : launch_variant<T, BL, 1, 2>(ctx, stream, p);
+  }
+}
+
+// ---- configuration tables: TileCfg<BM, BN, BK, WM, WN, STAGES>
+using KN0 = TileCfg<128, 128, 16, 2, 4, 4>;  // warp 64x32
+using KN1 = TileCfg<144, 128, 16, 2, 4, 4>;  // warp 72x32   (n in (128, 144])
+using KN2 = TileCfg<72, 128, 16, 1, 8, 4>;   // warp 72x16   (n <= 72)
+using KN3 = TileCfg<88, 128, 16, 1, 8, 4>;   // warp 88x16   (n = 3 x 88 - 7 = 257)
+using KN4 = TileCfg<64, 64, 16, 2, 2, 4>;    // warp 32x32, 4 warps (small grids)
+using KN5 = TileCfg<72, 64, 16, 1, 4, 4>;    // warp 72x16, 4 warps
+using NK0 = TileCfg<128, 128, 16, 2, 4, 4>;
+using NK1 = TileCfg<128, 144, 16, 4, 2, 4>;  // warp 32x72
+using NK2 = TileCfg<128, 72, 16, 8, 1, 4>;   // warp 16x72
+using NK3 = TileCfg<128, 88, 16, 8, 1, 4>;   // warp 16x88
+using NK4 = TileCfg<64, 64, 16, 2, 2, 4>;
+using NK5 = TileCfg<64, 72, 16, 4, 1, 4>;    // warp 16x72, 4 warps
+
+const char* kKnNames[] = {"128x128", "144x128", "72x128", "88x128", "64x64", "72x64"};
+const char* kNkNames[] = {"128x128", "128x144", "128x72", "128x88", "64x64", "64x72"};
+
+}  // namespace
+
+int gemm_num_configs(BLayout) { return 6; }
+
+const char* gemm_config_name(BLayout L, int cfg) {
+  if (cfg < 0 || cfg >= 6) return "?";
+  return L == BLayout::KN ? kKnNames[cfg] : kNkNames[cfg];
+}
+
+int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmParams p) {
+  if (L == BLayout::KN) {
+    switch (cfg) {
+      case 0: return launch_cfg<KN0, BLayout::KN>(ctx, stream, p);
+      case 1: return launch_cfg<KN1, BLayout::KN>(ctx, stream, p);
+      case 2: return launch_cfg<KN2, BLayout::KN>(ctx, stream, p);
+      case 3: return launch_cfg<KN3, BLayout::KN>(ctx, stream, p);
+      case 4: return launch_cfg<KN4, BLayout::KN>(ctx, stream, p);
+      case 5: return launch_cfg<KN5, BLayout::KN>(ctx, stream, p);
+    }
+  } else {
+    switch (cfg) {
+      case 0: return launch_cfg<NK0, BLayout::NK>(ctx, stream, p);
+      case 1: return launch_cfg<NK1, BLayout::NK>(ctx, stream, p);
+      case 2: return launch_cfg<NK2, BLayout::NK>(ctx, stream, p);
+      case 3: return launch_cfg<NK3, BLayout::NK>(ctx, stream, p);
+      case 4: return launch_cfg<NK4, BLayout::NK>(ctx, stream, p);
+      case 5: return launch_cfg<NK5, BLayout::NK>(ctx, stream, p);
+    }
+  }
+  set_error("bad GEMM configuration %d", cfg);
+  return FDIGA_ERR_INVALID_ARG;
+}
+
+int gemm_autotune(fdiga_ctx* ctx, BLayout L, const GemmParams& p, int* best_cfg, float* best_ms) {
+  cudaStream_t s = ctx->stream;
+  cudaEvent_t e0, e1;
+  FDIGA_CUDA(cudaEventCreate(&e0));
+  FDIGA_CUDA(cudaEventCreate(&e1));
+  int best = 0;
+  float best_t = 1e30f;
+  GemmParams q = p;
+  q.skip = nullptr;
+  for (int c = 0; c < gemm_num_configs(L); ++c) {
+    int rc = gemm_launch(ctx, s, L, c, q);  // warm-up (module load, attributes)
+    if (rc != FDIGA_OK) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      return rc;
+    }
+    const int reps = 3;
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < reps; ++r) gemm_launch(ctx, s, L, c, q);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    if (ms < best_t * 0.98f) {  // prefer the earlier (larger-tile) config on near ties
+      best_t = ms;
+      best = c;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  FDIGA_CUDA(cudaGetLastError());
+  *best_cfg = best;
+  if (best_ms) *best_ms = best_t;
+  return FDIGA_OK;
+}
+
+}  // namespace fdiga

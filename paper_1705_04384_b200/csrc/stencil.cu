@@ -337,6 +337,7 @@ struct MvArgs {
   const double* vals;
   const double* x;
   double* y;
+  const int* skip;  // device flag: nonzero -> no-op (GMRES graph early exit)
 };
 
 // y = A x, one thread per row (flattened, i1 fastest).  For every window pair q = (a, b) the thread
@@ -347,7 +348,7 @@ struct MvArgs {
 template <int WM>
 __global__ void __launch_bounds__(256) matvec_kernel(MvArgs A) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= A.N) return;
+  if (r >= A.N || (A.skip && *A.skip)) return;
   const int64_t i1 = r % A.n1, line = r / A.n1;
   const int64_t i2 = line % A.n2, i3 = line / A.n2;
   const int w1 = A.w1[i1], w2 = A.w2[i2], w3 = A.w3[i3];
@@ -526,6 +527,7 @@ extern "C" {
 int stencil_destroy(fdiga_stencil* S) {
   if (!S) return FDIGA_OK;
   cudaSetDevice(S->ctx->device);
+  destroy_gmres_graph(S->ctx);
   for (int l = 0; l < 3; ++l) {
     cudaFree(S->start[l]);
     cudaFree(S->width[l]);
@@ -673,12 +675,18 @@ int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometr
   return FDIGA_OK;
 }
 
-int stencil_matvec(fdiga_stencil* S, const double* x, double* y) {
+int stencil_matvec(fdiga_stencil* S, const double* x, double* y) { return fdiga::stencil_matvec_ex(S, x, y, nullptr); }
+
+}  // extern "C"
+
+namespace fdiga {
+int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* skip) {
   FDIGA_CHECK(S && x && y, FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_CHECK(x != y, FDIGA_ERR_INVALID_ARG, "stencil_matvec: x and y must not alias");
   fdiga_ctx* ctx = S->ctx;
   FDIGA_TRY(bind(ctx));
   MvArgs A = make_mv_args(S, x, y);
+  A.skip = skip;
   const unsigned grid = (unsigned)((S->N + 255) / 256);
   switch (S->wm1) {
 #define FDIGA_MV_CASE(W) \
@@ -702,6 +710,10 @@ int stencil_matvec(fdiga_stencil* S, const double* x, double* y) {
   FDIGA_CUDA(cudaGetLastError());
   return FDIGA_OK;
 }
+
+}  // namespace fdiga
+
+extern "C" {
 
 int stencil_info(const fdiga_stencil* S, int64_t* nnz, int64_t* n_out, int32_t* start_l0, int32_t* width_l0) {
   FDIGA_CHECK(S, FDIGA_ERR_INVALID_ARG, "NULL stencil");
