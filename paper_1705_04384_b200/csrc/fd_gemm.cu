@@ -52,22 +52,26 @@ using KN2 = TileCfg<72, 128, 16, 1, 8, 4>;   // warp 72x16   (n <= 72)
 using KN3 = TileCfg<88, 128, 16, 1, 8, 4>;   // warp 88x16   (n = 3 x 88 - 7 = 257)
 using KN4 = TileCfg<64, 64, 16, 2, 2, 4>;    // warp 32x32, 4 warps (small grids)
 using KN5 = TileCfg<72, 64, 16, 1, 4, 4>;    // warp 72x16, 4 warps
+using KN6 = TileCfg<128, 64, 16, 2, 2, 3>;   // warp 64x32, 4 warps, 2 CTAs/SM
+using KN7 = TileCfg<128, 128, 32, 2, 4, 3>;  // BK = 32: half the barriers
 using NK0 = TileCfg<128, 128, 16, 2, 4, 4>;
 using NK1 = TileCfg<128, 144, 16, 4, 2, 4>;  // warp 32x72
 using NK2 = TileCfg<128, 72, 16, 8, 1, 4>;   // warp 16x72
 using NK3 = TileCfg<128, 88, 16, 8, 1, 4>;   // warp 16x88
 using NK4 = TileCfg<64, 64, 16, 2, 2, 4>;
 using NK5 = TileCfg<64, 72, 16, 4, 1, 4>;    // warp 16x72, 4 warps
+using NK6 = TileCfg<64, 128, 16, 2, 2, 3>;   // warp 32x64, 4 warps, 2 CTAs/SM
+using NK7 = TileCfg<128, 128, 32, 2, 4, 3>;
 
-const char* kKnNames[] = {"128x128", "144x128", "72x128", "88x128", "64x64", "72x64"};
-const char* kNkNames[] = {"128x128", "128x144", "128x72", "128x88", "64x64", "64x72"};
+const char* kKnNames[] = {"128x128", "144x128", "72x128", "88x128", "64x64", "72x64", "128x64", "128x128k32"};
+const char* kNkNames[] = {"128x128", "128x144", "128x72", "128x88", "64x64", "64x72", "64x128", "128x128k32"};
 
 }  // namespace
 
-int gemm_num_configs(BLayout) { return 6; }
+int gemm_num_configs(BLayout) { return 8; }
 
 const char* gemm_config_name(BLayout L, int cfg) {
-  if (cfg < 0 || cfg >= 6) return "?";
+  if (cfg < 0 || cfg >= 8) return "?";
   return L == BLayout::KN ? kKnNames[cfg] : kNkNames[cfg];
 }
 
@@ -80,6 +84,8 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 3: return launch_cfg<KN3, BLayout::KN>(ctx, stream, p);
       case 4: return launch_cfg<KN4, BLayout::KN>(ctx, stream, p);
       case 5: return launch_cfg<KN5, BLayout::KN>(ctx, stream, p);
+      case 6: return launch_cfg<KN6, BLayout::KN>(ctx, stream, p);
+      case 7: return launch_cfg<KN7, BLayout::KN>(ctx, stream, p);
     }
   } else {
     switch (cfg) {
@@ -89,6 +95,8 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 3: return launch_cfg<NK3, BLayout::NK>(ctx, stream, p);
       case 4: return launch_cfg<NK4, BLayout::NK>(ctx, stream, p);
       case 5: return launch_cfg<NK5, BLayout::NK>(ctx, stream, p);
+      case 6: return launch_cfg<NK6, BLayout::NK>(ctx, stream, p);
+      case 7: return launch_cfg<NK7, BLayout::NK>(ctx, stream, p);
     }
   }
   set_error("bad GEMM configuration %d", cfg);

@@ -14,6 +14,7 @@
 // and the matvec moves exactly 8 nnz + 16 N bytes.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -345,45 +346,57 @@ struct MvArgs {
 // addresses, so every warp load is a full 256-byte coalesced stream (values are read exactly once,
 // streaming / evict-first) -- and the matching x window x[(s3+a) n1 n2 + (s2+b) n1 + s1 + c]
 // through L1/L2 (x of neighbouring rows overlaps).  Bytes moved: 8 nnz + 16 N.
-template <int WM>
-__global__ void __launch_bounds__(256) matvec_kernel(MvArgs A) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= A.N || (A.skip && *A.skip)) return;
-  const int64_t i1 = r % A.n1, line = r / A.n1;
-  const int64_t i2 = line % A.n2, i3 = line / A.n2;
-  const int w1 = A.w1[i1], w2 = A.w2[i2], w3 = A.w3[i3];
-  int vo[WM];
+template <int WM, int UB, int MINB>
+__global__ void __launch_bounds__(256, MINB) matvec_kernel(MvArgs A) {
+  const uint32_t r = blockIdx.x * 256u + threadIdx.x;
+  if (r >= (uint32_t)A.N || (A.skip && *A.skip)) return;
+  const uint32_t n1 = (uint32_t)A.n1, n2 = (uint32_t)A.n2;
+  const uint32_t i1 = r % n1, line = r / n1;
+  const uint32_t i2 = line % n2, i3 = line / n2;
+  const int w1 = __ldg(A.w1 + i1), w2 = __ldg(A.w2 + i2), w3 = __ldg(A.w3 + i3);
+  const int64_t S1 = A.S1;
+  const int64_t n12 = (int64_t)n1 * n2;
+  // per-thread value pointers for every column c of the window; advanced by UB * S1 per batch of
+  // UB window pairs q = a * w2 + b
+  const double* __restrict__ vbase =
+      A.vals + __ldg(A.pre3 + i3) * A.S2 * S1 + (int64_t)w3 * __ldg(A.pre2 + i2) * S1;
+  const double* pv[WM];
 #pragma unroll
-  for (int c = 0; c < WM; ++c) vo[c] = (c < w1) ? A.voff1[i1 * WM + c] : 0;
-  const int64_t n12 = A.n1 * A.n2;
-  const double* vb = A.vals + A.pre3[i3] * A.S2 * A.S1 + (int64_t)w3 * A.pre2[i2] * A.S1;
-  const double* xb = A.x + (int64_t)A.st3[i3] * n12 + (int64_t)A.st2[i2] * A.n1 + A.st1[i1];
-  double acc0 = 0.0, acc1 = 0.0;
-  for (int a = 0; a < w3; ++a) {
-    const double* xa = xb + a * n12;
-    int b = 0;
-    for (; b + 1 < w2; b += 2) {
-      const double* v0 = vb + (int64_t)(a * w2 + b) * A.S1;
-      const double* v1 = v0 + A.S1;
-      const double* x0 = xa + (int64_t)b * A.n1;
-      const double* x1 = x0 + A.n1;
+  for (int c = 0; c < WM; ++c) pv[c] = vbase + ((c < w1) ? __ldg(A.voff1 + i1 * WM + c) : 0);
+  const double* __restrict__ xb =
+      A.x + (int64_t)__ldg(A.st3 + i3) * n12 + (int64_t)__ldg(A.st2 + i2) * n1 + __ldg(A.st1 + i1);
+  const int nq = w3 * w2;
+  int a = 0, b = 0;
+  double acc[UB];
 #pragma unroll
-      for (int c = 0; c < WM; ++c) {
-        if (c < w1) {
-          acc0 = fma(__ldcs(v0 + vo[c]), __ldg(x0 + c), acc0);
-          acc1 = fma(__ldcs(v1 + vo[c]), __ldg(x1 + c), acc1);
+  for (int u = 0; u < UB; ++u) acc[u] = 0.0;
+  for (int q0 = 0; q0 < nq; q0 += UB) {
+    // issue every value load of the batch first (memory-level parallelism), then the x loads + FMAs
+    double vv[UB][WM];
+#pragma unroll
+    for (int u = 0; u < UB; ++u)
+#pragma unroll
+      for (int c = 0; c < WM; ++c) vv[u][c] = (q0 + u < nq && c < w1) ? __ldcs(pv[c] + u * S1) : 0.0;
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      if (q0 + u < nq) {
+        const double* xq = xb + a * n12 + (int64_t)b * n1;
+#pragma unroll
+        for (int c = 0; c < WM; ++c)
+          if (c < w1) acc[u] = fma(vv[u][c], __ldg(xq + c), acc[u]);
+        if (++b == w2) {
+          b = 0;
+          ++a;
         }
       }
     }
-    if (b < w2) {
-      const double* v0 = vb + (int64_t)(a * w2 + b) * A.S1;
-      const double* x0 = xa + (int64_t)b * A.n1;
 #pragma unroll
-      for (int c = 0; c < WM; ++c)
-        if (c < w1) acc0 = fma(__ldcs(v0 + vo[c]), __ldg(x0 + c), acc0);
-    }
+    for (int c = 0; c < WM; ++c) pv[c] += UB * S1;
   }
-  A.y[r] = acc0 + acc1;
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < UB; ++u) s += acc[u];
+  A.y[r] = s;
 }
 
 // canonical <-> internal value layouts (one thread per row)
@@ -484,6 +497,7 @@ int finish_stencil(fdiga_stencil* S) {
   }
   S->nnz = S->hpre[0][S->n[0]] * S->hpre[1][S->n[1]] * S->hpre[2][S->n[2]];
   FDIGA_CHECK(S->hpre[0][S->n[0]] < (int64_t(1) << 31), FDIGA_ERR_NOT_SUPPORTED, "direction-1 windows too large");
+  FDIGA_CHECK(S->N < (int64_t(1) << 31) - 256, FDIGA_ERR_NOT_SUPPORTED, "more than 2^31 rows per rank");
   // internal layout: column-major over c within each q-block, rows of the line compacted per column
   const int64_t n1 = S->n[0];
   int wm1 = 0;
@@ -688,10 +702,25 @@ int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* s
   MvArgs A = make_mv_args(S, x, y);
   A.skip = skip;
   const unsigned grid = (unsigned)((S->N + 255) / 256);
-  switch (S->wm1) {
-#define FDIGA_MV_CASE(W) \
-  case W:                \
-    matvec_kernel<W><<<grid, 256, 0, ctx->stream>>>(A); \
+  // variant: batch UB window pairs per load phase; selectable for experiments with FDIGA_MV_VARIANT
+  static int variant = -1;
+  if (variant < 0) {
+    const char* v = getenv("FDIGA_MV_VARIANT");
+    variant = v ? atoi(v) : 1;
+  }
+  switch (S->wm1 * 10 + variant) {
+#define FDIGA_MV_CASE(W)                                                     \
+  case W * 10 + 0:                                                          \
+    matvec_kernel<W, 1, 4><<<grid, 256, 0, ctx->stream>>>(A);               \
+    break;                                                                  \
+  case W * 10 + 1:                                                          \
+    matvec_kernel<W, 2, 3><<<grid, 256, 0, ctx->stream>>>(A);               \
+    break;                                                                  \
+  case W * 10 + 2:                                                          \
+    matvec_kernel<W, 3, 2><<<grid, 256, 0, ctx->stream>>>(A);               \
+    break;                                                                  \
+  case W * 10 + 3:                                                          \
+    matvec_kernel<W, 4, 2><<<grid, 256, 0, ctx->stream>>>(A);               \
     break;
     FDIGA_MV_CASE(1)
     FDIGA_MV_CASE(2)
@@ -704,7 +733,7 @@ int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* s
     FDIGA_MV_CASE(9)
 #undef FDIGA_MV_CASE
     default:
-      FDIGA_CHECK(false, FDIGA_ERR_NOT_SUPPORTED, "window width %d", S->wm1);
+      FDIGA_CHECK(false, FDIGA_ERR_NOT_SUPPORTED, "window width %d / variant %d", S->wm1, variant);
   }
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());
