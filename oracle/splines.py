@@ -115,3 +115,33 @@ def colloc_1d(ne: int, p: int):
 def flatten_index(mi, n: int) -> int:
     """1-based multi-index (i_1..i_d) -> scalar i = 1 + sum_l n^{l-1}(i_l - 1)."""
     return 1 + sum((n ** l) * (il - 1) for l, il in enumerate(mi))
+
+
+def galerkin_1d(ne: int, p: int, wind: float = 0.0):
+    """Univariate Galerkin factors on the interior functions (eq:univariateG P:357):
+
+      M_ij = int_0^1 B_i B_j,   K_ij = int_0^1 B'_i B'_j,   H_ij = int_0^1 w B_i B'_j  (constant wind w),
+
+    by Gauss-Legendre quadrature with p+1 points per element (exact: the integrands are polynomials of
+    degree <= 2p on every element).  Used for the convection-diffusion preconditioner eq:convec_prec_2
+    (P:363), whose pencils (K + H, M) have complex eigenvalue pairs for strong wind.
+    """
+    knots = open_uniform_knots(ne, p)
+    m = len(knots) - p - 1
+    n = m - 2
+    gx, gw = np.polynomial.legendre.leggauss(p + 1)
+    M = np.zeros((n, n))
+    K = np.zeros((n, n))
+    H = np.zeros((n, n))
+    breaks = np.unique(knots)
+    for e in range(len(breaks) - 1):
+        a, b = breaks[e], breaks[e + 1]
+        for xq, wq in zip(gx, gw):
+            x = 0.5 * (a + b) + 0.5 * (b - a) * xq
+            w = 0.5 * (b - a) * wq
+            B = basis_all(knots, p, x, 0)[1:n + 1]
+            D = basis_all(knots, p, x, 1)[1:n + 1]
+            M += w * np.outer(B, B)
+            K += w * np.outer(D, D)
+            H += w * wind * np.outer(B, D)
+    return M, K, H

@@ -116,7 +116,7 @@ def test_fd_setup_pencils_by_residuals(ctx, ne, p, d):
     # the library's own generalized eigendecomposition (cuSOLVER) on the collocation pencils
     _, M, K, _ = splines.colloc_1d(ne, p)
     plan = fd.fd_setup(ctx, [M] * d, [K] * d)
-    _, _, lam_o = fastdiag.setup_direction(M, K)
+    _, _, lam_o, _ = fastdiag.setup_direction(M, K)
     for l in range(d):
         U, W, lam, lam_im = plan.factors(l)
         assert np.all(lam_im == 0) and np.all(np.diff(lam) >= 0)
