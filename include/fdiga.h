@@ -91,6 +91,13 @@ int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, co
 /* Setup from explicit real factors (host, row-major): U[l], W[l] = (M_l U_l)^{-1}, lam[l]. */
 int fd_setup_from_factors(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* U,
                           const double* const* W, const double* const* lam, fd_plan** out);
+/* Same with complex pairs in real 2x2-block form: a pair a +- ib with eigenvector p + iq is
+ * stored in adjacent columns (p, q) of U[l] with lam_re = (a, a), lam_im = (+b, -b) (b > 0), i.e. the
+ * block [[a, b], [-b, a]] of D_l.  lam_im (or lam_im[l]) NULL means a real spectrum.  The divide step
+ * then solves the (<= 2^d x 2^d) diagonal blocks of Lambda.  INVALID_ARG on a malformed pair. */
+int fd_setup_from_blocks(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* U,
+                         const double* const* W, const double* const* lam_re, const double* const* lam_im,
+                         fd_plan** out);
 /* Setup from an eigenbasis: W_l = (M_l U_l)^{-1} computed on the device (M = NULL means M_l = I,
  * i.e. W_l = U_l^{-1}: BASELINE.json configs[3] "U_k^{-1} computed exactly in setup"). */
 int fd_setup_from_eig(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* U,

@@ -37,6 +37,9 @@ SIGNATURES = {
                            C.POINTER(FdSetupOpts), C.POINTER(C.c_void_p)]),
     "fd_setup_from_factors": (C.c_int, [C.c_void_p, C.c_int, c_int64_p, C.POINTER(c_double_p),
                                         C.POINTER(c_double_p), C.POINTER(c_double_p), C.POINTER(C.c_void_p)]),
+    "fd_setup_from_blocks": (C.c_int, [C.c_void_p, C.c_int, c_int64_p, C.POINTER(c_double_p),
+                                       C.POINTER(c_double_p), C.POINTER(c_double_p), C.POINTER(c_double_p),
+                                       C.POINTER(C.c_void_p)]),
     "fd_setup_from_eig": (C.c_int, [C.c_void_p, C.c_int, c_int64_p, C.POINTER(c_double_p), C.POINTER(c_double_p),
                                     C.POINTER(c_double_p), C.POINTER(C.c_void_p)]),
     "fd_get_factors": (C.c_int, [C.c_void_p, C.c_int, c_double_p, c_double_p, c_double_p, c_double_p]),

@@ -168,6 +168,20 @@ def fd_setup_from_factors(ctx, U, W, lam):
     return FDPlan(ctx, h, ns)
 
 
+def fd_setup_from_blocks(ctx, U, W, lam_re, lam_im):
+    """Factors with complex pairs in real 2x2-block form; see include/fdiga.h."""
+    d = len(U)
+    ns = [np.asarray(u).shape[0] for u in U]
+    n = (C.c_int64 * d)(*ns)
+    au, pu = _mat_array(U, ns)
+    aw, pw = _mat_array(W, ns)
+    al, pl = _vec_array(lam_re, ns)
+    ai, pi = _vec_array(lam_im, ns)
+    h = C.c_void_p()
+    check(ctx._lib.fd_setup_from_blocks(ctx.handle, d, n, pu, pw, pl, pi, C.byref(h)), "fd_setup_from_blocks")
+    return FDPlan(ctx, h, ns)
+
+
 def fd_setup_from_eig(ctx, U, lam, M=None):
     d = len(U)
     ns = [np.asarray(u).shape[0] for u in U]

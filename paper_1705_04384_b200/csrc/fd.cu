@@ -37,10 +37,106 @@ struct fd_plan {
   DevBuf host_io;               // device staging for fd_apply_host
   int cfg[3] = {0, 0, 0};       // autotuned GEMM tile configuration per mode (fd_gemm.cu)
   float cfg_ms[3] = {0, 0, 0};
+  // complex pairs: D_l has 2x2 blocks [[a, b], [-b, a]]; the divide becomes small block solves
+  bool has_pairs = false;
+  double* lam_im[3] = {nullptr, nullptr, nullptr};
+  int32_t* lead[3] = {nullptr, nullptr, nullptr};  // first index of every 1x1 / 2x2 block of D_l
+  int64_t nlead[3] = {1, 1, 1};
   std::vector<double> hU[3], hW[3], hlam[3], hlam_im[3];
 };
 
 namespace {
+
+// Lambda^{-1} on the block-diagonal Lambda = sum_l I (x)..(x) D_l (x)..(x) I: one thread per
+// product of D_l blocks (size 1, 2, 4 or 8), a small dense solve with partial pivoting, in place.
+struct BlockArgs {
+  int64_t n1, n2, n3;
+  int64_t L1, L2, L3;
+  const int32_t *lead1, *lead2, *lead3;
+  const double *re1, *re2, *re3, *im1, *im2, *im3;
+  double* x;
+  const int* skip;
+};
+
+__device__ __forceinline__ int blk_size(const double* im, int64_t i) { return im[i] != 0.0 ? 2 : 1; }
+
+// D_l[i + a][i + b] for a block starting at i
+__device__ __forceinline__ double blk_entry(const double* re, const double* im, int64_t i, int a, int b) {
+  if (a == b) return re[i + a];
+  return a == 0 ? im[i] : im[i + 1];  // [[a, +b], [-b, a]] with im[i] = +b, im[i+1] = -b
+}
+
+__global__ void block_solve_kernel(BlockArgs B) {
+  if (B.skip && *B.skip) return;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= B.L1 * B.L2 * B.L3) return;
+  const int64_t k1 = t % B.L1, k2 = (t / B.L1) % B.L2, k3 = t / (B.L1 * B.L2);
+  const int64_t i1 = B.lead1[k1], i2 = B.lead2[k2], i3 = B.lead3[k3];
+  const int s1 = blk_size(B.im1, i1), s2 = blk_size(B.im2, i2), s3 = blk_size(B.im3, i3);
+  const int S = s1 * s2 * s3;
+  double A[8][9];  // augmented system
+  int64_t idx[8];
+  for (int e = 0; e < S; ++e) {
+    const int e1 = e % s1, e2 = (e / s1) % s2, e3 = e / (s1 * s2);
+    idx[e] = (i1 + e1) + B.n1 * ((i2 + e2) + B.n2 * (i3 + e3));
+    for (int f = 0; f < S; ++f) {
+      const int f1 = f % s1, f2 = (f / s1) % s2, f3 = f / (s1 * s2);
+      double v = 0.0;
+      if (e2 == f2 && e3 == f3) v += blk_entry(B.re1, B.im1, i1, e1, f1);
+      if (e1 == f1 && e3 == f3) v += blk_entry(B.re2, B.im2, i2, e2, f2);
+      if (e1 == f1 && e2 == f2) v += blk_entry(B.re3, B.im3, i3, e3, f3);
+      A[e][f] = v;
+    }
+    A[e][S] = B.x[idx[e]];
+  }
+  for (int c = 0; c < S; ++c) {  // Gaussian elimination, partial pivoting
+    int piv = c;
+    for (int r = c + 1; r < S; ++r)
+      if (fabs(A[r][c]) > fabs(A[piv][c])) piv = r;
+    if (piv != c)
+      for (int k = 0; k <= S; ++k) {
+        const double tmp = A[c][k];
+        A[c][k] = A[piv][k];
+        A[piv][k] = tmp;
+      }
+    for (int r = c + 1; r < S; ++r) {
+      const double f = A[r][c] / A[c][c];
+      for (int k = c; k <= S; ++k) A[r][k] -= f * A[c][k];
+    }
+  }
+  for (int r = S - 1; r >= 0; --r) {
+    double s = A[r][S];
+    for (int k = r + 1; k < S; ++k) s -= A[r][k] * A[k][S];
+    A[r][S] = s / A[r][r];
+  }
+  for (int e = 0; e < S; ++e) B.x[idx[e]] = A[e][S];
+}
+
+int block_solve(fd_plan* P, double* x, const int* skip) {
+  BlockArgs B{};
+  B.n1 = P->n[0];
+  B.n2 = P->n[1];
+  B.n3 = P->n[2];
+  B.L1 = P->nlead[0];
+  B.L2 = P->nlead[1];
+  B.L3 = P->nlead[2];
+  B.lead1 = P->lead[0];
+  B.lead2 = P->lead[1];
+  B.lead3 = P->lead[2];
+  B.re1 = P->lam[0];
+  B.re2 = P->lam[1];
+  B.re3 = P->lam[2];
+  B.im1 = P->lam_im[0];
+  B.im2 = P->lam_im[1];
+  B.im3 = P->lam_im[2];
+  B.x = x;
+  B.skip = skip;
+  const int64_t T = B.L1 * B.L2 * B.L3;
+  block_solve_kernel<<<(unsigned)((T + 127) / 128), 128, 0, P->ctx->stream>>>(B);
+  count_launch(P->ctx);
+  FDIGA_CUDA(cudaGetLastError());
+  return FDIGA_OK;
+}
 
 // mode 1 (contiguous axis): Y(R x n1) = X(R x n1) * F^T
 GemmParams mode1_params(fd_plan* P, const double* F, int64_t ldf, const double* X, double* Y, int64_t R,
@@ -129,23 +225,45 @@ int upload_factor(const double* h, int64_t n, int64_t ld, double** dptr) {
 }
 
 int finish_plan(fd_plan* P) {
-  // singularity guard on the eigenvalue sums: min |Lambda| <= 1e3 eps max |Lambda|
+  const int d = P->d;
+  // complex pairs: validate the block structure (lam_im = +b, -b on adjacent indices, equal real parts)
+  for (int l = 0; l < d; ++l) {
+    const auto& im = P->hlam_im[l];
+    const auto& re = P->hlam[l];
+    for (int64_t i = 0; i < P->n[l]; ++i) {
+      if (im[i] == 0.0) continue;
+      FDIGA_CHECK(i + 1 < P->n[l] && im[i] > 0.0 && im[i + 1] == -im[i] && re[i + 1] == re[i],
+                  FDIGA_ERR_INVALID_ARG, "direction %d: lam_im must hold +b, -b pairs with equal real parts", l);
+      P->has_pairs = true;
+      ++i;
+    }
+  }
+  // singularity guard on the eigenvalues of Lambda: min |Lambda| <= 1e3 eps max |Lambda|, with
+  // mu = lam_re + i lam_im per index (the eigenvalues of the 2x2 blocks are a +- ib)
   double mn = INFINITY, mx = 0.0;
   {
-    const int d = P->d;
-    const auto& l1 = P->hlam[0];
-    const auto& l2 = P->hlam[1];
-    std::vector<double> inner;  // lam_1 + ... + lam_{d-1}
+    const auto& r1 = P->hlam[0];
+    const auto& r2 = P->hlam[1];
+    const auto& m1 = P->hlam_im[0];
+    const auto& m2 = P->hlam_im[1];
+    std::vector<double> inner, inner_im;  // lam_1 + ... + lam_{d-1}
     if (d == 2) {
-      inner = l1;
+      inner = r1;
+      inner_im = m1;
     } else {
-      inner.resize(l1.size() * l2.size());
-      for (size_t b = 0; b < l2.size(); ++b)
-        for (size_t a = 0; a < l1.size(); ++a) inner[b * l1.size() + a] = l1[a] + l2[b];
+      inner.resize(r1.size() * r2.size());
+      inner_im.resize(r1.size() * r2.size());
+      for (size_t b = 0; b < r2.size(); ++b)
+        for (size_t a = 0; a < r1.size(); ++a) {
+          inner[b * r1.size() + a] = r1[a] + r2[b];
+          inner_im[b * r1.size() + a] = m1[a] + m2[b];
+        }
     }
-    for (double lo : P->hlam[d - 1])
-      for (double v : inner) {
-        const double s = std::fabs(lo + v);
+    const auto& rl = P->hlam[d - 1];
+    const auto& ml = P->hlam_im[d - 1];
+    for (size_t k = 0; k < rl.size(); ++k)
+      for (size_t j = 0; j < inner.size(); ++j) {
+        const double s = std::hypot(rl[k] + inner[j], ml[k] + inner_im[j]);
         mn = std::min(mn, s);
         mx = std::max(mx, s);
       }
@@ -154,12 +272,32 @@ int finish_plan(fd_plan* P) {
     FDIGA_CUDA(cudaMalloc(&P->lam_inner, inner.size() * sizeof(double)));
     FDIGA_CUDA(cudaMemcpy(P->lam_inner, inner.data(), inner.size() * sizeof(double), cudaMemcpyHostToDevice));
   }
-  for (int l = 0; l < P->d; ++l) {
+  for (int l = 0; l < d; ++l) {
     P->ld[l] = (P->n[l] + 1) & ~int64_t(1);
     FDIGA_TRY(upload_factor(P->hU[l].data(), P->n[l], P->ld[l], &P->U[l]));
     FDIGA_TRY(upload_factor(P->hW[l].data(), P->n[l], P->ld[l], &P->W[l]));
     FDIGA_CUDA(cudaMalloc(&P->lam[l], P->n[l] * sizeof(double)));
     FDIGA_CUDA(cudaMemcpy(P->lam[l], P->hlam[l].data(), P->n[l] * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  if (P->has_pairs) {
+    for (int l = 0; l < 3; ++l) {
+      std::vector<double> re = l < d ? P->hlam[l] : std::vector<double>(1, 0.0);  // dummy direction: D = [0]
+      std::vector<double> im = l < d ? P->hlam_im[l] : std::vector<double>(1, 0.0);
+      std::vector<int32_t> lead;
+      for (int64_t i = 0; i < (int64_t)re.size(); ++i) {
+        lead.push_back((int32_t)i);
+        if (im[i] != 0.0) ++i;
+      }
+      P->nlead[l] = (int64_t)lead.size();
+      if (l >= d) {
+        FDIGA_CUDA(cudaMalloc(&P->lam[l], sizeof(double)));
+        FDIGA_CUDA(cudaMemcpy(P->lam[l], re.data(), sizeof(double), cudaMemcpyHostToDevice));
+      }
+      FDIGA_CUDA(cudaMalloc(&P->lam_im[l], im.size() * sizeof(double)));
+      FDIGA_CUDA(cudaMemcpy(P->lam_im[l], im.data(), im.size() * sizeof(double), cudaMemcpyHostToDevice));
+      FDIGA_CUDA(cudaMalloc(&P->lead[l], lead.size() * sizeof(int32_t)));
+      FDIGA_CUDA(cudaMemcpy(P->lead[l], lead.data(), lead.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
   }
   FDIGA_TRY(P->t0.ensure(P->N));
   FDIGA_TRY(P->t1.ensure(P->N));
@@ -328,16 +466,21 @@ int fd_apply_ex(fd_plan* P, const double* r, double* s, const int* skip) {
   double* a = P->t0.p;
   double* b = P->t1.p;
   const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
+  // real spectra: the Lambda-divide rides in the epilogue of the last forward product; complex pairs
+  // (P:434): plain last forward product, then the small block solves in place
+  const bool fused = !P->has_pairs;
   if (P->d == 2) {
     // fwd: mode 1 (W_1), mode 2 (W_2) + divide by lam_2[i2] + lam_1[i1]; bwd: mode 2 (U_2), mode 1 (U_1)
     FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2, skip));
-    FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, 1, P->lam[1], P->lam_inner, skip));
+    FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, 1, fused ? P->lam[1] : nullptr, P->lam_inner, skip));
+    if (!fused) FDIGA_TRY(block_solve(P, b, skip));
     FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, 1, nullptr, nullptr, skip));
     FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2, skip));
   } else {
     FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2 * n3, skip));
     FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, n3, nullptr, nullptr, skip));
-    FDIGA_TRY(model(P, 2, P->W[2], P->ld[2], b, a, n1 * n2, 1, P->lam[2], P->lam_inner, skip));
+    FDIGA_TRY(model(P, 2, P->W[2], P->ld[2], b, a, n1 * n2, 1, fused ? P->lam[2] : nullptr, P->lam_inner, skip));
+    if (!fused) FDIGA_TRY(block_solve(P, a, skip));
     FDIGA_TRY(model(P, 2, P->U[2], P->ld[2], a, b, n1 * n2, 1, nullptr, nullptr, skip));
     FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, n3, nullptr, nullptr, skip));
     FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2 * n3, skip));
@@ -350,15 +493,27 @@ extern "C" {
 
 int fd_setup_from_factors(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* U, const double* const* W,
                           const double* const* lam, fd_plan** out) {
+  return fd_setup_from_blocks(ctx, d, n, U, W, lam, nullptr, out);
+}
+
+int fd_setup_from_blocks(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* U, const double* const* W,
+                         const double* const* lam_re, const double* const* lam_im, fd_plan** out) {
   FDIGA_TRY(check_common(ctx, d, n, out));
-  FDIGA_CHECK(U && W && lam, FDIGA_ERR_INVALID_ARG, "NULL factor array");
+  FDIGA_CHECK(U && W && lam_re, FDIGA_ERR_INVALID_ARG, "NULL factor array");
   fd_plan* P = new_plan(ctx, d, n);
   for (int l = 0; l < d; ++l) {
-    FDIGA_CHECK(U[l] && W[l] && lam[l], FDIGA_ERR_INVALID_ARG, "NULL factor for direction %d", l);
+    if (!(U[l] && W[l] && lam_re[l])) {
+      fd_plan_destroy(P);
+      set_error("NULL factor for direction %d", l);
+      return FDIGA_ERR_INVALID_ARG;
+    }
     P->hU[l].assign(U[l], U[l] + n[l] * n[l]);
     P->hW[l].assign(W[l], W[l] + n[l] * n[l]);
-    P->hlam[l].assign(lam[l], lam[l] + n[l]);
-    P->hlam_im[l].assign(n[l], 0.0);
+    P->hlam[l].assign(lam_re[l], lam_re[l] + n[l]);
+    if (lam_im && lam_im[l])
+      P->hlam_im[l].assign(lam_im[l], lam_im[l] + n[l]);
+    else
+      P->hlam_im[l].assign(n[l], 0.0);
   }
   int s = finish_plan(P);
   if (s != FDIGA_OK) {
@@ -461,25 +616,62 @@ int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, co
       rho = std::max(rho, std::abs(z));
       maxim = std::max(maxim, std::fabs(z.imag()));
     }
+    std::vector<char> is_c(nl, 0);
     if (maxim > tol_imag * rho) {
       if (!allow_cplx) {
         set_error("complex spectrum in direction %d: max |Im lambda| = %g (rho = %g)", l, maxim, rho);
         return fail(FDIGA_ERR_COMPLEX_SPECTRUM);
       }
-      set_error("complex-pair (2x2 block) FD apply is not built in this version");
-      return fail(FDIGA_ERR_NOT_SUPPORTED);
+      for (int64_t j = 0; j < nl; ++j) is_c[j] = std::fabs(ev[j].imag()) > tol_imag * rho;
     }
-    std::vector<int64_t> order(nl);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return ev[a].real() < ev[b].real(); });
-    std::vector<double> Ul((size_t)nl * nl), laml(nl);
-    for (int64_t c = 0; c < nl; ++c) {
-      const int64_t src = order[c];
-      laml[c] = ev[src].real();
-      double nrm = 0;
-      for (int64_t i = 0; i < nl; ++i) nrm += VR[src * nl + i] * VR[src * nl + i];
-      nrm = std::sqrt(nrm);
-      for (int64_t i = 0; i < nl; ++i) Ul[i * nl + c] = VR[src * nl + i] / nrm;  // row-major U
+    // Xgeev packs a conjugate pair (j, j+1) LAPACK-style: eigenvalue ev[j] = a + ib (b > 0),
+    // eigenvector VR[:,j] + i VR[:,j+1].  Keep one key per real eigenvalue / per pair, sort by real part,
+    // and store pairs as adjacent real columns (p, q) with D block [[a, b], [-b, a]].
+    std::vector<int64_t> keys;
+    for (int64_t j = 0; j < nl; ++j) {
+      if (is_c[j]) {
+        if (j + 1 >= nl || !is_c[j + 1]) {
+          set_error("direction %d: unpaired complex eigenvalue", l);
+          return fail(FDIGA_ERR_CUSOLVER);
+        }
+        keys.push_back(ev[j].imag() > 0 ? j : -(j + 1));  // negative: the pair's first column has b < 0
+        ++j;
+      } else {
+        keys.push_back(j);
+      }
+    }
+    auto kidx = [](int64_t k) { return k >= 0 ? k : -k - 1; };
+    std::stable_sort(keys.begin(), keys.end(), [&](int64_t a, int64_t b) {
+      const double ra = ev[kidx(a)].real(), rb = ev[kidx(b)].real();
+      if (ra != rb) return ra < rb;
+      return !is_c[kidx(a)] && is_c[kidx(b)];
+    });
+    std::vector<double> Ul((size_t)nl * nl), laml(nl), laml_im(nl, 0.0);
+    int64_t c = 0;
+    for (int64_t k : keys) {
+      const int64_t j = kidx(k);
+      if (!is_c[j]) {
+        laml[c] = ev[j].real();
+        double nrm = 0;
+        for (int64_t i = 0; i < nl; ++i) nrm += VR[j * nl + i] * VR[j * nl + i];
+        nrm = std::sqrt(nrm);
+        for (int64_t i = 0; i < nl; ++i) Ul[i * nl + c] = VR[j * nl + i] / nrm;  // row-major U
+        ++c;
+      } else {
+        const double a = ev[j].real(), b = std::fabs(ev[j].imag());
+        const double qs = (k >= 0) ? 1.0 : -1.0;  // eigenvector for a + i|b| is p + i qs q
+        double nrm = 0;
+        for (int64_t i = 0; i < nl; ++i) nrm += VR[j * nl + i] * VR[j * nl + i] + VR[(j + 1) * nl + i] * VR[(j + 1) * nl + i];
+        nrm = std::sqrt(nrm / 2);
+        for (int64_t i = 0; i < nl; ++i) {
+          Ul[i * nl + c] = VR[j * nl + i] / nrm;
+          Ul[i * nl + c + 1] = qs * VR[(j + 1) * nl + i] / nrm;
+        }
+        laml[c] = laml[c + 1] = a;
+        laml_im[c] = b;
+        laml_im[c + 1] = -b;
+        c += 2;
+      }
     }
     // 4. W = (M U)^{-1} and cond_1(U)
     double condU = 0;
@@ -491,7 +683,7 @@ int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, co
     }
     P->hU[l] = std::move(Ul);
     P->hlam[l] = std::move(laml);
-    P->hlam_im[l].assign(nl, 0.0);
+    P->hlam_im[l] = std::move(laml_im);
   }
   int s = finish_plan(P);
   if (s != FDIGA_OK) return fail(s);
@@ -540,6 +732,10 @@ int fd_plan_destroy(fd_plan* P) {
     cudaFree(P->lam[l]);
   }
   cudaFree(P->lam_inner);
+  for (int l = 0; l < 3; ++l) {
+    cudaFree(P->lam_im[l]);
+    cudaFree(P->lead[l]);
+  }
   P->t0.release();
   P->t1.release();
   P->host_io.release();

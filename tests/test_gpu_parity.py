@@ -147,6 +147,76 @@ def test_fd_setup_rejects_singular_sums(ctx):
     assert e.value.status == -7
 
 
+# ---- complex pairs in real 2x2-block form: convection-diffusion pencils (eq:convec_prec_2)
+
+def _fd_tol(f):
+    """FP64 forward error of the apply grows with prod_l cond(U_l) (the Kronecker transforms, DESIGN.md
+    "Tolerances"): the north-star 1e-12 bar is kept up to prod cond = 1e4 (the Poisson pencils have
+    prod cond <= 9.2^3) and scaled linearly beyond."""
+    kappa = float(np.prod([np.linalg.cond(u) for u in f.U]))
+    return 1e-12 * max(1.0, kappa / 1e4)
+
+
+@pytest.mark.parametrize("d,wind,ne", [(2, 100.0, 6), (3, 100.0, 5), (2, 1000.0, 33), (3, 200.0, 12),
+                                       (2, 10000.0, 128), (3, 1000.0, 40), (2, 25.0, 9), (3, 60.0, 7),
+                                       (3, 100.0, 17)])
+def test_fd_apply_complex_pairs_shared_factors(ctx, d, wind, ne):
+    M, K, H = splines.galerkin_1d(ne, 2, wind)
+    f = fastdiag.setup([M] * d, [K + H] * d, allow_complex=True)
+    assert f.has_pairs
+    plan = fd.fd_setup_from_blocks(ctx, f.U, f.W, f.lam, f.lam_im)
+    b = np.random.default_rng(ne + d).standard_normal(ne ** d)
+    s = torch.empty(b.size, dtype=torch.float64, device=DEV)
+    fd.fd_apply(plan, gpu(b), s)
+    assert rel(host(s), fastdiag.apply(f, b)) <= _fd_tol(f)
+
+
+def test_fd_apply_complex_pairs_mixed_directions(ctx):
+    # one direction all-complex, one mixed, one real: blocks of size 1, 2 and 4 side by side
+    M1, K1, H1 = splines.galerkin_1d(12, 2, 200.0)
+    M2, K2, H2 = splines.galerkin_1d(9, 2, 25.0)
+    M3, K3, _ = splines.galerkin_1d(7, 2, 0.0)
+    f = fastdiag.setup([M1, M2, M3], [K1 + H1, K2 + H2, K3], allow_complex=True)
+    plan = fd.fd_setup_from_blocks(ctx, f.U, f.W, f.lam, f.lam_im)
+    b = np.random.default_rng(3).standard_normal(12 * 9 * 7)
+    s = torch.empty(b.size, dtype=torch.float64, device=DEV)
+    fd.fd_apply(plan, gpu(b), s)
+    assert rel(host(s), fastdiag.apply(f, b)) <= _fd_tol(f)
+
+
+@pytest.mark.parametrize("d,wind,ne", [(2, 100.0, 16), (3, 100.0, 8), (2, 1000.0, 40), (2, 25.0, 9)])
+def test_fd_setup_complex_pairs_by_residuals(ctx, d, wind, ne):
+    # the library's own complex-pair setup: M^{-1}(K+H) U = U D with real 2x2 blocks, W M U = I, and the
+    # apply solves P s = b (P materialised by Kronecker products, brute force)
+    M, K, H = splines.galerkin_1d(ne, 2, wind)
+    with pytest.raises(fd.FdigaError) as e:
+        fd.fd_setup(ctx, [M] * d, [K + H] * d)
+    assert e.value.status == -5
+    plan = fd.fd_setup(ctx, [M] * d, [K + H] * d, allow_complex_pairs=True)
+    for l in range(d):
+        U, W, lr, li = plan.factors(l)
+        assert np.any(li != 0)
+        D = fastdiag.FDFactors([U], [W], [lr], [li]).D(0)
+        assert np.linalg.norm((K + H) @ U - M @ U @ D) / (np.linalg.norm(K + H) * np.linalg.norm(U)) < 1e-13
+        assert np.linalg.norm(W @ M @ U - np.eye(ne)) < 1e-10
+        # the spectrum agrees with the oracle's QZ as a multiset a +- ib
+        _, _, lo, lio = fastdiag.setup_direction(M, K + H, allow_complex=True)
+        np.testing.assert_allclose(np.sort_complex(lr + 1j * li), np.sort_complex(lo + 1j * lio), rtol=1e-9)
+    P = assembly.kron_preconditioner_dense([M] * d, [K + H] * d)
+    b = rhs(0, ne ** d)
+    s = torch.empty(b.size, dtype=torch.float64, device=DEV)
+    fd.fd_apply(plan, gpu(b), s)
+    assert np.linalg.norm(P @ host(s) - b) / np.linalg.norm(b) <= 1e-11
+
+
+def test_fd_setup_from_blocks_rejects_malformed_pairs(ctx):
+    U = [np.eye(3)] * 2
+    bad = [np.array([1.0, 0.0, 0.0]), np.zeros(3)]           # +b without its -b partner
+    with pytest.raises(fd.FdigaError) as e:
+        fd.fd_setup_from_blocks(ctx, U, U, [np.array([2.0, 2.0, 5.0])] * 2, bad)
+    assert e.value.status == -1
+
+
 # ----------------------------------------------------------------------------- matvec / assembly
 
 def _disc(cfg, ne=None):
