@@ -56,20 +56,51 @@ enum {
 typedef struct fdiga_ctx fdiga_ctx;
 typedef struct fd_plan fd_plan;
 typedef struct fdiga_stencil fdiga_stencil;
+typedef struct fdiga_loopback fdiga_loopback;
 
 /* ---------------------------------------------------------------- context ---- */
 
 /* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t to run on (caller-owned,
  * must outlive the context), or NULL for the legacy default stream.  nranks/rank/nccl_unique_id: the process group
- * (nccl_unique_id = 128-byte ncclUniqueId, NULL iff nranks == 1). */
+ * (nccl_unique_id = 128-byte ncclUniqueId from fdiga_nccl_unique_id; required when nranks > 1).  A unique id
+ * selects the NCCL transport and the slab-sharded code path: vectors hold the rank's
+ * slab of the last axis, the FD mode-d pass runs after an all-to-all slab transpose, the matvec
+ * exchanges halo planes and GMRES all-reduces its dot products.  With nranks == 1 and a unique id the
+ * same path runs over a one-rank NCCL communicator (self messages); NULL runs the single-GPU path.
+ * Sharded operators are 3D only (2D problems run as replicas); complex-pair FD is single-GPU only. */
 int fdiga_ctx_create(int device, void* cuda_stream, int nranks, int rank, const void* nccl_unique_id,
                      fdiga_ctx** out);
-int fdiga_ctx_destroy(fdiga_ctx* ctx); /* NULL -> no-op */
+int fdiga_ctx_destroy(fdiga_ctx* ctx); /* NULL -> no-op; collective when nranks > 1 */
 /* This rank's slab [begin, end) of the last tensor index for a last-axis length n_last
  * (balanced: the first n_last % nranks ranks own one extra plane). */
 int fdiga_slab(const fdiga_ctx* ctx, int64_t n_last, int64_t* begin, int64_t* end);
-/* Fill a 128-byte buffer with a fresh ncclUniqueId (call on rank 0, broadcast it). */
+/* Fill a 128-byte buffer with a fresh ncclUniqueId (call on rank 0, broadcast it).  libnccl.so.2 is
+ * resolved at run time (the copy torch loaded); FDIGA_ERR_NCCL if it cannot be found. */
 int fdiga_nccl_unique_id(void* out128);
+/* Loopback transport: `nranks` contexts in ONE process on ONE device, each used from its own host
+ * thread with its own stream; collectives exchange device pointers and CUDA events through the hub
+ * (no kernel waits on another rank).  Runs the sharded path of every rank on a single GPU.
+ * Destroy the hub after all of its contexts. */
+int fdiga_loopback_create(int nranks, fdiga_loopback** out);
+int fdiga_loopback_destroy(fdiga_loopback* hub);
+int fdiga_ctx_create_loopback(int device, void* cuda_stream, fdiga_loopback* hub, int rank, fdiga_ctx** out);
+/* Balanced split of [0, n) into nparts contiguous ranges; part's range is [begin, end) (host only).
+ * Slabs of the last axis (fdiga_slab) and the mode-d transpose chunks use it. */
+int fdiga_partition(int64_t n, int nparts, int part, int64_t* begin, int64_t* end);
+/* Exchange schedule of the sharded FD mode-d pass (host only; what fd_apply uses).  n_inner =
+ * n_1..n_{d-1}, n_last = n_d.  Rank r owns slab planes [o_r, e_r) and, after the transpose, the inner
+ * chunk [q_r, q_r + len_r) of all n_last planes as T(n_last x len_r).  For every peer q (arrays of
+ * length nranks, in doubles): slab_off/slab_cnt = my (e_r - o_r) x len_q block of chunk q in the
+ * staging buffer; tr_off/tr_cnt = rows [o_q, e_q) of my T.  Forward pass: send the slab blocks,
+ * receive the T rows; backward pass: the reverse. */
+int fdiga_transpose_plan(int64_t n_inner, int64_t n_last, int nranks, int rank, int64_t* slab_off, int64_t* slab_cnt,
+                         int64_t* tr_off, int64_t* tr_cnt);
+/* Halo schedule of the sharded matvec (host only; what stencil_matvec uses).  start/width: the
+ * last-axis column windows (length n_last).  Out: the planes [lo, hi) this rank's rows read, and for
+ * every peer q the planes [send_b[q], send_e[q]) it sends to q and [recv_b[q], recv_e[q]) it
+ * receives from q (global plane indices; empty when b == e).  At most one message per pair. */
+int fdiga_halo_plan(int64_t n_last, const int32_t* start, const int32_t* width, int nranks, int rank, int64_t* lo,
+                    int64_t* hi, int64_t* send_b, int64_t* send_e, int64_t* recv_b, int64_t* recv_e);
 const char* fdiga_status_string(int status);
 const char* fdiga_last_error(void);
 
@@ -141,6 +172,9 @@ int stencil_destroy(fdiga_stencil* A);
 /* Univariate collocation factors of the same discretisation (host out, row-major n x n):
  * M[i][j] = B_j(tau_i), K[i][j] = -B''_j(tau_i) (eq:univariatecolloc). */
 int colloc_1d_factors(int p, int64_t ne, double* M, double* K);
+/* The 1D column windows of the stored operator (host only): row i of direction l couples to columns
+ * [start[i], start[i] + width[i]) (length n = ne + p - 2). */
+int colloc_1d_windows(int p, int64_t ne, int32_t* start, int32_t* width);
 
 /* -------------------------------------------------------------------- GMRES ---- */
 

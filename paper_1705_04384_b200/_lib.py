@@ -31,6 +31,15 @@ SIGNATURES = {
     "fdiga_ctx_destroy": (C.c_int, [C.c_void_p]),
     "fdiga_slab": (C.c_int, [C.c_void_p, C.c_int64, c_int64_p, c_int64_p]),
     "fdiga_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "fdiga_loopback_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "fdiga_loopback_destroy": (C.c_int, [C.c_void_p]),
+    "fdiga_ctx_create_loopback": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "fdiga_partition": (C.c_int, [C.c_int64, C.c_int, C.c_int, c_int64_p, c_int64_p]),
+    "fdiga_transpose_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int, C.c_int, c_int64_p, c_int64_p, c_int64_p,
+                                       c_int64_p]),
+    "fdiga_halo_plan": (C.c_int, [C.c_int64, c_int32_p, c_int32_p, C.c_int, C.c_int, c_int64_p, c_int64_p,
+                                  c_int64_p, c_int64_p, c_int64_p, c_int64_p]),
+    "colloc_1d_windows": (C.c_int, [C.c_int, C.c_int64, c_int32_p, c_int32_p]),
     "fdiga_status_string": (C.c_char_p, [C.c_int]),
     "fdiga_last_error": (C.c_char_p, []),
     "fd_setup": (C.c_int, [C.c_void_p, C.c_int, c_int64_p, C.POINTER(c_double_p), C.POINTER(c_double_p),

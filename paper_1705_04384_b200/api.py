@@ -8,7 +8,7 @@ import ctypes as C
 
 import numpy as np
 
-from ._lib import (FdSetupOpts, GmresOpts, GmresReport, c_double_p, c_int32_p, check, load)
+from ._lib import (FdSetupOpts, GmresOpts, GmresReport, c_double_p, c_int32_p, c_int64_p, check, load)
 
 ORTH_CGS_DGKS = 0
 ORTH_CGS2 = 1
@@ -34,18 +34,83 @@ def _devptr(t, n=None):
     return C.c_void_p(t.data_ptr())
 
 
-class Context:
-    """fdiga_ctx: a device, a stream and (optionally) an NCCL process group."""
+def nccl_unique_id():
+    """A fresh 128-byte ncclUniqueId (rank 0 creates it, every rank passes it to Context)."""
+    buf = C.create_string_buffer(128)
+    check(load().fdiga_nccl_unique_id(buf), "fdiga_nccl_unique_id")
+    return buf.raw
 
-    def __init__(self, device=0, stream=None, nranks=1, rank=0, nccl_unique_id=None):
+
+def partition(n, nparts, part):
+    """Balanced split of [0, n) into nparts ranges (fdiga_partition): the range [begin, end) of `part`."""
+    b, e = C.c_int64(), C.c_int64()
+    check(load().fdiga_partition(int(n), int(nparts), int(part), C.byref(b), C.byref(e)), "fdiga_partition")
+    return b.value, e.value
+
+
+def transpose_plan(n_inner, n_last, nranks, rank):
+    """Exchange schedule of the sharded FD mode-d pass (fdiga_transpose_plan): four int64 arrays
+    (slab_off, slab_cnt, tr_off, tr_cnt) of length nranks, in doubles."""
+    arrs = [np.zeros(nranks, np.int64) for _ in range(4)]
+    check(load().fdiga_transpose_plan(int(n_inner), int(n_last), int(nranks), int(rank),
+                                      *[a.ctypes.data_as(c_int64_p) for a in arrs]), "fdiga_transpose_plan")
+    return tuple(arrs)
+
+
+def halo_plan(start, width, nranks, rank):
+    """Halo schedule of the sharded matvec (fdiga_halo_plan): (lo, hi, send_b, send_e, recv_b, recv_e)."""
+    st = np.ascontiguousarray(start, dtype=np.int32)
+    wd = np.ascontiguousarray(width, dtype=np.int32)
+    lo, hi = C.c_int64(), C.c_int64()
+    arrs = [np.zeros(nranks, np.int64) for _ in range(4)]
+    check(load().fdiga_halo_plan(st.size, st.ctypes.data_as(c_int32_p), wd.ctypes.data_as(c_int32_p), int(nranks),
+                                 int(rank), C.byref(lo), C.byref(hi), *[a.ctypes.data_as(c_int64_p) for a in arrs]),
+          "fdiga_halo_plan")
+    return (lo.value, hi.value) + tuple(arrs)
+
+
+def colloc_1d_windows(p, ne):
+    """The 1D column windows (start, width) of the stored operator (host only)."""
+    n = ne + p - 2
+    st, wd = np.empty(n, np.int32), np.empty(n, np.int32)
+    check(load().colloc_1d_windows(int(p), int(ne), st.ctypes.data_as(c_int32_p), wd.ctypes.data_as(c_int32_p)),
+          "colloc_1d_windows")
+    return st, wd
+
+
+class LoopbackHub:
+    """fdiga_loopback: nranks contexts in one process on one device (one host thread per rank)."""
+
+    def __init__(self, nranks):
+        self._lib = load()
+        h = C.c_void_p()
+        check(self._lib.fdiga_loopback_create(int(nranks), C.byref(h)), "fdiga_loopback_create")
+        self.handle, self.nranks = h, nranks
+
+    def close(self):
+        if self.handle:
+            check(self._lib.fdiga_loopback_destroy(self.handle), "fdiga_loopback_destroy")
+            self.handle = None
+
+
+class Context:
+    """fdiga_ctx: a device, a stream and (optionally) a process group (NCCL, or a loopback hub)."""
+
+    def __init__(self, device=0, stream=None, nranks=1, rank=0, nccl_unique_id=None, hub=None):
         lib = load()
         self._lib = lib
         h = C.c_void_p()
         s = C.c_void_p(stream) if stream is not None else None
-        uid = C.c_char_p(bytes(nccl_unique_id)) if nccl_unique_id is not None else None
-        check(lib.fdiga_ctx_create(int(device), s, int(nranks), int(rank), uid, C.byref(h)), "fdiga_ctx_create")
+        if hub is not None:
+            check(lib.fdiga_ctx_create_loopback(int(device), s, hub.handle, int(rank), C.byref(h)),
+                  "fdiga_ctx_create_loopback")
+            nranks = hub.nranks
+        else:
+            uid = C.c_char_p(bytes(nccl_unique_id)) if nccl_unique_id is not None else None
+            check(lib.fdiga_ctx_create(int(device), s, int(nranks), int(rank), uid, C.byref(h)), "fdiga_ctx_create")
         self.handle = h
         self.device = device
+        self.nranks, self.rank = int(nranks), int(rank)
 
     def slab(self, n_last):
         b, e = C.c_int64(), C.c_int64()
@@ -72,7 +137,9 @@ class FDPlan:
 
     def __init__(self, ctx, handle, ns):
         self.ctx, self.handle, self.n = ctx, handle, list(ns)
-        self.N = int(np.prod(self.n))
+        self.N_global = int(np.prod(self.n))
+        self.slab = ctx.slab(self.n[-1])           # this rank's planes of the last axis
+        self.N = (self.slab[1] - self.slab[0]) * (self.N_global // self.n[-1])   # local vector length
 
     def factors(self, l):
         n = self.n[l]
@@ -105,9 +172,11 @@ class Stencil:
         nnz = C.c_int64()
         n = (C.c_int64 * 3)(1, 1, 1)
         check(ctx._lib.stencil_info(handle, C.byref(nnz), n, None, None), "stencil_info")
-        self.nnz = nnz.value
+        self.nnz = nnz.value                       # values stored on this rank
         self.n = [n[0], n[1], n[2]]
-        self.N = n[0] * n[1] * n[2]
+        self.N_global = n[0] * n[1] * n[2]
+        self.slab = ctx.slab(n[2]) if ctx.nranks > 1 else (0, n[2])
+        self.N = (self.slab[1] - self.slab[0]) * n[0] * n[1]   # local rows
 
     def windows(self):
         """(start, width) of the column windows of direction 1 (int32 arrays of length n_1)."""
@@ -205,7 +274,7 @@ def fd_apply(plan, r, s):
 def fd_apply_host(plan, r_host, s_host):
     """Same with host (numpy, ideally pinned) buffers; H2D + apply + D2H inside the call."""
     if r_host.dtype != np.float64 or s_host.dtype != np.float64 or r_host.size != plan.N or s_host.size != plan.N:
-        raise ValueError("fd_apply_host: float64 host arrays of length N expected")
+        raise ValueError("fd_apply_host: float64 host arrays of the local length expected")
     check(plan.ctx._lib.fd_apply_host(plan.handle, _dptr(r_host), _dptr(s_host)), "fd_apply_host")
     return s_host
 

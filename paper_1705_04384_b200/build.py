@@ -29,24 +29,42 @@ def _stale():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+def nccl_include():
+    """Directory of nccl.h (types only: libnccl.so.2 is dlopen'ed at run time, the copy torch loads)."""
+    import glob
+    for cand in glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "nvidia", "nccl", "include")) + \
+            ["/usr/include"]:
+        if os.path.exists(os.path.join(cand, "nccl.h")):
+            return cand
+    raise RuntimeError("nccl.h not found")
+
+
 def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     objs = []
     nvcc = nvcc_path()
-    common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+    common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
+                     "-I", nccl_include()]
     build_dir = os.path.join(PKG, "build")
     os.makedirs(build_dir, exist_ok=True)
+    cmds = []
     for src in SOURCES:
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
-        cmd = [nvcc] + common + ["-c", os.path.join(CSRC, src), "-o", obj]
+        cmds.append([nvcc] + common + ["-c", os.path.join(CSRC, src), "-o", obj])
+        objs.append(obj)
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(cmd):
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-        objs.append(obj)
+
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        list(ex.map(run, cmds))
     tmp = LIB + ".tmp"
-    cmd = [nvcc] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcusolver"]
+    cmd = [nvcc] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcusolver", "-ldl"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
     return LIB

@@ -57,6 +57,15 @@ struct DevBuf {
   }
 };
 
+// One point-to-point message of an exchange (comm.cu): peer rank, device buffer, size in bytes.
+struct P2PMsg {
+  int peer;
+  void* ptr;
+  size_t bytes;
+};
+
+constexpr int FDIGA_MAX_RANKS = 64;
+
 }  // namespace fdiga
 
 struct fdiga_ctx {
@@ -64,7 +73,9 @@ struct fdiga_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int nranks = 1, rank = 0;
-  void* nccl_comm = nullptr;  // ncclComm_t when nranks > 1
+  void* nccl_comm = nullptr;  // ncclComm_t when nranks > 1 (NCCL transport)
+  fdiga_loopback* hub = nullptr;  // loopback transport (nranks contexts in one process), else NULL
+  bool sharded = false;           // slab-sharded code path (a process group was given, even of 1 rank)
   int sm_count = 148;
   int64_t launches = 0;       // kernels launched by this context
   double* pinned = nullptr;   // small pinned host scratch (scalars coming back from reductions)
@@ -85,6 +96,16 @@ int ensure_pinned(fdiga_ctx* c, size_t n_doubles);
 // captured GMRES cycle graph for early exit.
 int fd_apply_ex(fd_plan* P, const double* r, double* s, const int* skip);
 int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* skip);
+// Balanced split of [0, n) into nparts ranges; the first n % nparts get one extra element.
+void partition(int64_t n, int nparts, int part, int64_t* begin, int64_t* end);
+// Collectives on ctx->stream (comm.cu).  Every rank calls them in the same order.
+int comm_exchange(fdiga_ctx* ctx, const std::vector<P2PMsg>& sends, const std::vector<P2PMsg>& recvs);
+int comm_allreduce(fdiga_ctx* ctx, const double* send, double* recv, size_t count);  // sum, same bits on all ranks
+bool comm_capturable(const fdiga_ctx* ctx);  // false for the loopback transport (host barriers)
+int loopback_attach(fdiga_ctx* ctx, fdiga_loopback* hub);
+// Rows of this rank's slab of a (possibly sharded) stencil.
+int64_t stencil_local_rows(const fdiga_stencil* S);
+int64_t fd_plan_local_size(const fd_plan* P);
 // Drop the cached GMRES graph (it captures pointers of A, P and the workspace).
 void destroy_gmres_graph(fdiga_ctx* ctx);
 }  // namespace fdiga

@@ -51,15 +51,14 @@ const char* fdiga_status_string(int s) {
 
 int fdiga_comm_init(fdiga_ctx* ctx, const void* uid);      // comm.cu
 int fdiga_comm_destroy(fdiga_ctx* ctx);                     // comm.cu
+int fdiga_loopback_nranks(const fdiga_loopback* hub, int* n); // comm.cu
 
-int fdiga_ctx_create(int device, void* cuda_stream, int nranks, int rank, const void* nccl_unique_id,
-                     fdiga_ctx** out) {
+namespace {
+int ctx_new(int device, void* cuda_stream, int nranks, int rank, fdiga_ctx** out) {
   FDIGA_CHECK(out != nullptr, FDIGA_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
-  FDIGA_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, FDIGA_ERR_INVALID_ARG, "bad nranks/rank %d/%d",
-              nranks, rank);
-  FDIGA_CHECK(nranks == 1 || nccl_unique_id != nullptr, FDIGA_ERR_INVALID_ARG,
-              "nccl_unique_id required when nranks > 1");
+  FDIGA_CHECK(nranks >= 1 && nranks <= FDIGA_MAX_RANKS && rank >= 0 && rank < nranks, FDIGA_ERR_INVALID_ARG,
+              "bad nranks/rank %d/%d", nranks, rank);
   int ndev = 0;
   FDIGA_CUDA(cudaGetDeviceCount(&ndev));
   FDIGA_CHECK(device >= 0 && device < ndev, FDIGA_ERR_INVALID_ARG, "device %d out of range (%d devices)", device,
@@ -77,10 +76,22 @@ int fdiga_ctx_create(int device, void* cuda_stream, int nranks, int rank, const 
   // NULL selects the legacy default stream (ordered with every blocking stream, e.g. torch's default)
   c->stream = (cudaStream_t)cuda_stream;
   c->own_stream = false;
-  if (nranks > 1) {
+  *out = c;
+  return FDIGA_OK;
+}
+}  // namespace
+
+int fdiga_ctx_create(int device, void* cuda_stream, int nranks, int rank, const void* nccl_unique_id,
+                     fdiga_ctx** out) {
+  FDIGA_CHECK(nranks == 1 || nccl_unique_id != nullptr, FDIGA_ERR_INVALID_ARG,
+              "nccl_unique_id required when nranks > 1");
+  // a unique id (even with nranks == 1) selects the NCCL transport and the sharded code path
+  fdiga_ctx* c = nullptr;
+  FDIGA_TRY(ctx_new(device, cuda_stream, nranks, rank, &c));
+  if (nccl_unique_id != nullptr) {
+    c->sharded = true;
     int s = fdiga_comm_init(c, nccl_unique_id);
     if (s != FDIGA_OK) {
-      if (c->own_stream) cudaStreamDestroy(c->stream);
       delete c;
       return s;
     }
@@ -89,10 +100,25 @@ int fdiga_ctx_create(int device, void* cuda_stream, int nranks, int rank, const 
   return FDIGA_OK;
 }
 
+int fdiga_ctx_create_loopback(int device, void* cuda_stream, fdiga_loopback* hub, int rank, fdiga_ctx** out) {
+  FDIGA_CHECK(hub != nullptr, FDIGA_ERR_INVALID_ARG, "hub is NULL");
+  int nr = 0;
+  FDIGA_TRY(fdiga_loopback_nranks(hub, &nr));
+  fdiga_ctx* c = nullptr;
+  FDIGA_TRY(ctx_new(device, cuda_stream, nr, rank, &c));
+  int s = loopback_attach(c, hub);
+  if (s != FDIGA_OK) {
+    delete c;
+    return s;
+  }
+  *out = c;
+  return FDIGA_OK;
+}
+
 int fdiga_ctx_destroy(fdiga_ctx* c) {
   if (!c) return FDIGA_OK;
   cudaSetDevice(c->device);
-  if (c->nccl_comm) fdiga_comm_destroy(c);
+  if (c->nccl_comm || c->hub) fdiga_comm_destroy(c);
   destroy_gmres_graph(c);
   if (c->pinned) cudaFreeHost(c->pinned);
   for (auto& b : c->ws) b.release();
@@ -103,9 +129,7 @@ int fdiga_ctx_destroy(fdiga_ctx* c) {
 
 int fdiga_slab(const fdiga_ctx* c, int64_t n_last, int64_t* begin, int64_t* end) {
   FDIGA_CHECK(c && begin && end && n_last >= 0, FDIGA_ERR_INVALID_ARG, "bad fdiga_slab arguments");
-  int64_t q = n_last / c->nranks, r = n_last % c->nranks;
-  *begin = c->rank * q + (c->rank < r ? c->rank : r);
-  *end = *begin + q + (c->rank < r ? 1 : 0);
+  partition(n_last, c->nranks, c->rank, begin, end);
   return FDIGA_OK;
 }
 

@@ -43,6 +43,10 @@ struct fd_plan {
   int32_t* lead[3] = {nullptr, nullptr, nullptr};  // first index of every 1x1 / 2x2 block of D_l
   int64_t nlead[3] = {1, 1, 1};
   std::vector<double> hU[3], hW[3], hlam[3], hlam_im[3];
+  // slab sharding (nranks > 1): this rank owns the last-axis planes [o, e) of r and s
+  // (Nloc = (e - o) Nin values, Nin = n_1..n_{d-1}); the mode-d sandwich runs in the transposed layout
+  // T(n_d x len) over the inner-index chunk [q0, q0 + len).
+  int64_t Nin = 0, o = 0, e = 0, q0 = 0, len = 0, Nloc = 0;
 };
 
 namespace {
@@ -138,6 +142,32 @@ int block_solve(fd_plan* P, double* x, const int* skip) {
   return FDIGA_OK;
 }
 
+// Slab <-> transpose-chunk staging of the sharded mode-d pass.  Chunk s of the inner index J is
+// [q_s, q_s + len_s) (balanced split of Nin over nranks); the staging buffer holds, for each s in
+// order, the c x len_s block X[i][q_s .. q_s + len_s) (offset c q_s), i.e. what travels to / from s.
+__device__ __forceinline__ int64_t chunk_of(int64_t J, int64_t Nin, int nr, int64_t* qs, int64_t* ls) {
+  const int64_t q = Nin / nr, rr = Nin % nr, bnd = rr * (q + 1);
+  const int64_t s = J < bnd ? J / (q + 1) : rr + (J - bnd) / q;
+  *qs = s * q + (s < rr ? s : rr);
+  *ls = q + (s < rr ? 1 : 0);
+  return s;
+}
+
+__global__ void slab_pack_kernel(const double* __restrict__ x, double* __restrict__ stage, int64_t c, int64_t Nin,
+                                 int nr, int unpack, const int* skip) {
+  if (skip && *skip) return;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < c * Nin; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / Nin, J = t - i * Nin;
+    int64_t qs, ls;
+    chunk_of(J, Nin, nr, &qs, &ls);
+    const int64_t so = c * qs + i * ls + (J - qs);
+    if (unpack)
+      stage[t] = x[so];  // here x is the staging buffer and stage the slab
+    else
+      stage[so] = x[t];
+  }
+}
+
 // mode 1 (contiguous axis): Y(R x n1) = X(R x n1) * F^T
 GemmParams mode1_params(fd_plan* P, const double* F, int64_t ldf, const double* X, double* Y, int64_t R,
                         const int* skip) {
@@ -179,38 +209,40 @@ GemmParams model_params(fd_plan* P, int l, const double* F, int64_t ldf, const d
 }
 
 int mode1(fd_plan* P, const double* F, int64_t ldf, const double* X, double* Y, int64_t R, const int* skip) {
+  if (R == 0) return FDIGA_OK;
   return gemm_launch(P->ctx, P->ctx->stream, BLayout::NK, P->cfg[0], mode1_params(P, F, ldf, X, Y, R, skip));
 }
 
 int model(fd_plan* P, int l, const double* F, int64_t ldf, const double* X, double* Y, int64_t inner,
           int64_t batch, const double* lam_m, const double* lam_n, const int* skip) {
+  if (inner * batch == 0) return FDIGA_OK;
   return gemm_launch(P->ctx, P->ctx->stream, BLayout::KN, P->cfg[l],
                      model_params(P, l, F, ldf, X, Y, inner, batch, lam_m, lam_n, skip));
 }
 
 // Pick the tile configuration of every mode product of this plan by timing them on the plan's scratch.
 int autotune_plan(fd_plan* P) {
-  const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
+  const int64_t n1 = P->n[0], n2 = P->n[1];
+  const int64_t c = P->e - P->o;  // local planes of the last axis (all of them on one rank)
   double* a = P->t0.p;
   double* b = P->t1.p;
-  FDIGA_CUDA(cudaMemsetAsync(a, 0, P->N * sizeof(double), P->ctx->stream));
-  const int64_t rows1 = (P->d == 2) ? n2 : n2 * n3;
-  FDIGA_TRY(gemm_autotune(P->ctx, BLayout::NK, mode1_params(P, P->W[0], P->ld[0], a, b, rows1, nullptr), &P->cfg[0],
-                          &P->cfg_ms[0]));
-  if (P->d == 2) {
-    FDIGA_TRY(gemm_autotune(P->ctx, BLayout::KN, model_params(P, 1, P->W[1], P->ld[1], a, b, n1, 1, nullptr, nullptr,
-                                                              nullptr), &P->cfg[1], &P->cfg_ms[1]));
-  } else {
-    FDIGA_TRY(gemm_autotune(P->ctx, BLayout::KN, model_params(P, 1, P->W[1], P->ld[1], a, b, n1, n3, nullptr,
+  FDIGA_CUDA(cudaMemsetAsync(a, 0, P->t0.cap * sizeof(double), P->ctx->stream));
+  const int64_t rows1 = (P->d == 2) ? c : n2 * c;
+  if (rows1 > 0)
+    FDIGA_TRY(gemm_autotune(P->ctx, BLayout::NK, mode1_params(P, P->W[0], P->ld[0], a, b, rows1, nullptr),
+                            &P->cfg[0], &P->cfg_ms[0]));
+  if (P->d == 3 && c > 0)
+    FDIGA_TRY(gemm_autotune(P->ctx, BLayout::KN, model_params(P, 1, P->W[1], P->ld[1], a, b, n1, c, nullptr,
                                                               nullptr, nullptr), &P->cfg[1], &P->cfg_ms[1]));
-    FDIGA_TRY(gemm_autotune(P->ctx, BLayout::KN, model_params(P, 2, P->W[2], P->ld[2], a, b, n1 * n2, 1, nullptr,
-                                                              nullptr, nullptr), &P->cfg[2], &P->cfg_ms[2]));
-  }
+  if (P->len > 0)  // mode d over the (transposed) inner chunk
+    FDIGA_TRY(gemm_autotune(P->ctx, BLayout::KN, model_params(P, P->d - 1, P->W[P->d - 1], P->ld[P->d - 1], a, b,
+                                                              P->len, 1, nullptr, nullptr, nullptr),
+                            &P->cfg[P->d - 1], &P->cfg_ms[P->d - 1]));
   FDIGA_CUDA(cudaStreamSynchronize(P->ctx->stream));
   if (getenv("FDIGA_VERBOSE")) {
     for (int l = 0; l < P->d; ++l)
       fprintf(stderr, "[fdiga] fd plan n=(%lld,%lld,%lld) mode %d: tile %s, %.1f us\n", (long long)n1,
-              (long long)n2, (long long)n3, l + 1, gemm_config_name(l == 0 ? BLayout::NK : BLayout::KN, P->cfg[l]),
+              (long long)n2, (long long)P->n[2], l + 1, gemm_config_name(l == 0 ? BLayout::NK : BLayout::KN, P->cfg[l]),
               1e3 * P->cfg_ms[l]);
   }
   return FDIGA_OK;
@@ -224,8 +256,52 @@ int upload_factor(const double* h, int64_t n, int64_t ld, double** dptr) {
   return FDIGA_OK;
 }
 
+// Multi-rank: every rank uses rank 0's factors bit for bit (the sharded apply mixes the modes of
+// different ranks, and two correct setups differ by ~1e-11 through cond(P)).  A sum
+// all-reduce in which only rank 0 contributes is an exact broadcast.
+int broadcast_factors(fd_plan* P) {
+  fdiga_ctx* ctx = P->ctx;
+  std::vector<double> pack;
+  for (int l = 0; l < P->d; ++l) {
+    pack.insert(pack.end(), P->hU[l].begin(), P->hU[l].end());
+    pack.insert(pack.end(), P->hW[l].begin(), P->hW[l].end());
+    pack.insert(pack.end(), P->hlam[l].begin(), P->hlam[l].end());
+    pack.insert(pack.end(), P->hlam_im[l].begin(), P->hlam_im[l].end());
+  }
+  if (ctx->rank != 0) std::fill(pack.begin(), pack.end(), 0.0);
+  double* buf = nullptr;
+  FDIGA_CUDA(cudaMalloc(&buf, 2 * pack.size() * sizeof(double)));
+  int s = FDIGA_OK;
+  if (cudaMemcpy(buf, pack.data(), pack.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) s = FDIGA_ERR_CUDA;
+  const int s2 = comm_allreduce(ctx, buf, buf + pack.size(), pack.size());  // collective: always called
+  if (s == FDIGA_OK) s = s2;
+  if (s == FDIGA_OK && (cudaStreamSynchronize(ctx->stream) != cudaSuccess ||
+                        cudaMemcpy(pack.data(), buf + pack.size(), pack.size() * 8, cudaMemcpyDeviceToHost) !=
+                            cudaSuccess))
+    s = FDIGA_ERR_CUDA;
+  cudaFree(buf);
+  if (s != FDIGA_OK) {
+    set_error("broadcast of the FD factors failed");
+    return s;
+  }
+  size_t off = 0;
+  for (int l = 0; l < P->d; ++l) {
+    const size_t nn = (size_t)P->n[l] * P->n[l], n = (size_t)P->n[l];
+    std::copy(pack.begin() + off, pack.begin() + off + nn, P->hU[l].begin());
+    off += nn;
+    std::copy(pack.begin() + off, pack.begin() + off + nn, P->hW[l].begin());
+    off += nn;
+    std::copy(pack.begin() + off, pack.begin() + off + n, P->hlam[l].begin());
+    off += n;
+    std::copy(pack.begin() + off, pack.begin() + off + n, P->hlam_im[l].begin());
+    off += n;
+  }
+  return FDIGA_OK;
+}
+
 int finish_plan(fd_plan* P) {
   const int d = P->d;
+  if (P->ctx->sharded) FDIGA_TRY(broadcast_factors(P));
   // complex pairs: validate the block structure (lam_im = +b, -b on adjacent indices, equal real parts)
   for (int l = 0; l < d; ++l) {
     const auto& im = P->hlam_im[l];
@@ -238,6 +314,8 @@ int finish_plan(fd_plan* P) {
       ++i;
     }
   }
+  FDIGA_CHECK(!(P->has_pairs && P->ctx->sharded), FDIGA_ERR_NOT_SUPPORTED,
+              "complex-pair FD is single-rank only (blocks straddle the transpose chunks)");
   // singularity guard on the eigenvalues of Lambda: min |Lambda| <= 1e3 eps max |Lambda|, with
   // mu = lam_re + i lam_im per index (the eigenvalues of the 2x2 blocks are a +- ib)
   double mn = INFINITY, mx = 0.0;
@@ -299,8 +377,11 @@ int finish_plan(fd_plan* P) {
       FDIGA_CUDA(cudaMemcpy(P->lead[l], lead.data(), lead.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
   }
-  FDIGA_TRY(P->t0.ensure(P->N));
-  FDIGA_TRY(P->t1.ensure(P->N));
+  {
+    const size_t cap = (size_t)std::max<int64_t>(1, std::max(P->Nloc, P->n[d - 1] * P->len));
+    FDIGA_TRY(P->t0.ensure(cap));
+    FDIGA_TRY(P->t1.ensure(cap));
+  }
   FDIGA_CUDA(cudaDeviceSynchronize());  // uploads complete before any stream uses the plan
   FDIGA_TRY(autotune_plan(P));
   return FDIGA_OK;
@@ -311,7 +392,6 @@ int check_common(fdiga_ctx* ctx, int d, const int64_t* n, fd_plan** out) {
   FDIGA_CHECK(d == 2 || d == 3, FDIGA_ERR_INVALID_ARG, "d must be 2 or 3 (got %d)", d);
   for (int l = 0; l < d; ++l)
     FDIGA_CHECK(n[l] >= 1 && n[l] <= 65535, FDIGA_ERR_INVALID_ARG, "n[%d] = %lld out of range", l, (long long)n[l]);
-  FDIGA_CHECK(ctx->nranks == 1, FDIGA_ERR_NOT_SUPPORTED, "multi-rank FD apply is not built in this version");
   *out = nullptr;
   return bind(ctx);
 }
@@ -325,6 +405,12 @@ fd_plan* new_plan(fdiga_ctx* ctx, int d, const int64_t* n) {
     P->n[l] = n[l];
     P->N *= n[l];
   }
+  P->Nin = P->N / n[d - 1];
+  partition(n[d - 1], ctx->nranks, ctx->rank, &P->o, &P->e);
+  int64_t q1 = 0;
+  partition(P->Nin, ctx->nranks, ctx->rank, &P->q0, &q1);
+  P->len = q1 - P->q0;
+  P->Nloc = (P->e - P->o) * P->Nin;
   return P;
 }
 
@@ -459,8 +545,68 @@ int compute_W(Solver& S, cudaStream_t st, int64_t n, const double* M, const std:
 }  // namespace
 
 namespace fdiga {
+int64_t fd_plan_local_size(const fd_plan* P) { return P->Nloc; }
+}  // namespace fdiga
+
+namespace {
+// Sharded apply (nranks > 1): local modes 1..d-1 on the slab, NCCL/loopback slab -> chunk transpose,
+// the mode-d sandwich (W_d, Lambda-divide epilogue, U_d) on T(n_d x len), transpose back, local
+// backward modes.  r, s: this rank's slab (s may alias r).
+int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
+  fdiga_ctx* ctx = P->ctx;
+  double* a = P->t0.p;
+  double* b = P->t1.p;
+  const int d = P->d, nr = ctx->nranks;
+  const int64_t n1 = P->n[0], n2 = P->n[1], nd = P->n[d - 1];
+  const int64_t c = P->e - P->o, Nin = P->Nin, len = P->len;
+  // forward modes 1..d-1 -> b (slab layout)
+  if (d == 3) {
+    FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2 * c, skip));
+    FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, c, nullptr, nullptr, skip));
+  } else {
+    FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, b, c, skip));
+  }
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((c * Nin + 255) / 256, 8 * ctx->sm_count));
+  std::vector<int64_t> so(nr), sc(nr), to(nr), tc(nr);
+  FDIGA_TRY(fdiga_transpose_plan(Nin, nd, nr, ctx->rank, so.data(), sc.data(), to.data(), tc.data()));
+  std::vector<P2PMsg> snd, rcv;
+  auto plan_msgs = [&](double* slab_side, double* tr_side) {
+    snd.clear();
+    rcv.clear();
+    for (int q = 0; q < nr; ++q) {
+      snd.push_back({q, slab_side + so[q], (size_t)sc[q] * 8});
+      rcv.push_back({q, tr_side + to[q], (size_t)tc[q] * 8});
+    }
+  };
+  if (c > 0) {
+    slab_pack_kernel<<<g, 256, 0, ctx->stream>>>(b, a, c, Nin, nr, 0, skip);
+    count_launch(ctx);
+    FDIGA_CUDA(cudaGetLastError());
+  }
+  plan_msgs(a, b);
+  FDIGA_TRY(comm_exchange(ctx, snd, rcv));  // b = T(n_d x len)
+  FDIGA_TRY(model(P, d - 1, P->W[d - 1], P->ld[d - 1], b, a, len, 1, P->lam[d - 1], P->lam_inner + P->q0, skip));
+  FDIGA_TRY(model(P, d - 1, P->U[d - 1], P->ld[d - 1], a, b, len, 1, nullptr, nullptr, skip));
+  plan_msgs(a, b);
+  FDIGA_TRY(comm_exchange(ctx, rcv, snd));  // reverse: rows of T back to their slab owners, into a
+  if (c > 0) {
+    slab_pack_kernel<<<g, 256, 0, ctx->stream>>>(a, b, c, Nin, nr, 1, skip);
+    count_launch(ctx);
+    FDIGA_CUDA(cudaGetLastError());
+  }
+  if (d == 3) {
+    FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, c, nullptr, nullptr, skip));
+    FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2 * c, skip));
+  } else {
+    FDIGA_TRY(mode1(P, P->U[0], P->ld[0], b, s, c, skip));
+  }
+  return FDIGA_OK;
+}
+}  // namespace
+
+namespace fdiga {
 int fd_apply_ex(fd_plan* P, const double* r, double* s, const int* skip) {
-  FDIGA_CHECK(P && r && s, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_CHECK(P && ((r && s) || P->Nloc == 0), FDIGA_ERR_INVALID_ARG, "NULL argument");
   fdiga_ctx* ctx = P->ctx;
   FDIGA_TRY(bind(ctx));
   double* a = P->t0.p;
@@ -469,6 +615,7 @@ int fd_apply_ex(fd_plan* P, const double* r, double* s, const int* skip) {
   // real spectra: the Lambda-divide rides in the epilogue of the last forward product; complex pairs
   // (P:434): plain last forward product, then the small block solves in place
   const bool fused = !P->has_pairs;
+  if (ctx->sharded) return fd_apply_sharded(P, r, s, skip);
   if (P->d == 2) {
     // fwd: mode 1 (W_1), mode 2 (W_2) + divide by lam_2[i2] + lam_1[i1]; bwd: mode 2 (U_2), mode 1 (U_1)
     FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2, skip));
@@ -706,11 +853,11 @@ int fd_apply(fd_plan* P, const double* r, double* s) { return fdiga::fd_apply_ex
 int fd_apply_host(fd_plan* P, const double* r_host, double* s_host) {
   FDIGA_CHECK(P && r_host && s_host, FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_TRY(bind(P->ctx));
-  FDIGA_TRY(P->host_io.ensure(P->N));
+  FDIGA_TRY(P->host_io.ensure(std::max<int64_t>(1, P->Nloc)));
   cudaStream_t st = P->ctx->stream;
-  FDIGA_CUDA(cudaMemcpyAsync(P->host_io.p, r_host, P->N * 8, cudaMemcpyHostToDevice, st));
+  FDIGA_CUDA(cudaMemcpyAsync(P->host_io.p, r_host, P->Nloc * 8, cudaMemcpyHostToDevice, st));
   FDIGA_TRY(fd_apply(P, P->host_io.p, P->host_io.p));
-  FDIGA_CUDA(cudaMemcpyAsync(s_host, P->host_io.p, P->N * 8, cudaMemcpyDeviceToHost, st));
+  FDIGA_CUDA(cudaMemcpyAsync(s_host, P->host_io.p, P->Nloc * 8, cudaMemcpyDeviceToHost, st));
   FDIGA_CUDA(cudaStreamSynchronize(st));
   return FDIGA_OK;
 }

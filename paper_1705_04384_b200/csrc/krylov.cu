@@ -32,6 +32,8 @@ struct GmState {
   double H[(KMAX + 1) * KMAX];  // R of the rotated Hessenberg (row-major, stride KMAX)
   double cs[KMAX], sn[KMAX], g[KMAX + 1];
   double h1[KMAX + 1], h2[KMAX + 1], y[KMAX];
+  // sharded (nranks > 1): per-rank partial sums, all-reduced into h1 / h2 / wn2 / rs
+  double h1l[KMAX + 1], h2l[KMAX + 1], wn2l, wn2, rsl[2], rs[2];
   double beta, bnorm, target, invh, rel_implicit, rel_true;
   int stop;        // cycle stop flag: every remaining step launch of the cycle is a no-op
   int k;           // steps taken in the current cycle
@@ -96,7 +98,7 @@ __device__ __forceinline__ bool reduce_last(double (&acc)[CNT], int cnt, double*
 template <int K>
 __global__ void __launch_bounds__(RT) arnoldi_pass1(const double* __restrict__ V, int64_t ldv, int /*k (= K)*/,
                                                     const double* __restrict__ w, int64_t N, double* part,
-                                                    GmState* st) {
+                                                    GmState* st, double* hout) {
   constexpr int k = K;
   if (st->stop) return;
   double acc[KMAX + 1];
@@ -123,14 +125,15 @@ __global__ void __launch_bounds__(RT) arnoldi_pass1(const double* __restrict__ V
 #pragma unroll
   for (int i = 0; i < KMAX; ++i)
     if (i == k) acc[i] = acc[KMAX];  // w.w to slot k (static register indexing)
-  reduce_last<KMAX + 1>(acc, k + 1, part, &st->counter[0], st->h1);
+  reduce_last<KMAX + 1>(acc, k + 1, part, &st->counter[0], hout);
 }
 
 // pass 2: w <- w - V h1 ; h2[i] = V_i . w (new w), h2[k] = ||w||^2.  V_i is read twice per element
 // pair; the second read hits L1 (the block's working set is <= 256 threads x 32 x 16 B).
 template <int K>
 __global__ void __launch_bounds__(RT) arnoldi_pass2(const double* __restrict__ V, int64_t ldv, int /*k (= K)*/,
-                                                    double* __restrict__ w, int64_t N, double* part, GmState* st) {
+                                                    double* __restrict__ w, int64_t N, double* part, GmState* st,
+                                                    double* hout) {
   constexpr int k = K;
   if (st->stop) return;
   __shared__ double hs[KMAX];
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(RT) arnoldi_pass2(const double* __restrict__ V
 #pragma unroll
   for (int i = 0; i < KMAX; ++i)
     if (i == k) acc[i] = acc[KMAX];
-  reduce_last<KMAX + 1>(acc, k + 1, part, &st->counter[1], st->h2);
+  reduce_last<KMAX + 1>(acc, k + 1, part, &st->counter[1], hout);
 }
 
 // Givens rotations / convergence test for step j (one thread), once h = h1 + h2 and ||w''||^2 are known.
@@ -215,7 +218,7 @@ __device__ void arnoldi_close_step(GmState* st, int j, int m, double wn2, double
 template <int K>
 __global__ void __launch_bounds__(RT) arnoldi_pass3(const double* __restrict__ V, int64_t ldv, int /*k (= K)*/,
                                                     double* __restrict__ w, int64_t N, double* part, GmState* st,
-                                                    int j, int m, double* hist, int hist_cap) {
+                                                    int j, int m, double* hist, int hist_cap, int close) {
   constexpr int k = K;
   if (st->stop) return;
   __shared__ double hs[KMAX];
@@ -245,8 +248,19 @@ __global__ void __launch_bounds__(RT) arnoldi_pass3(const double* __restrict__ V
   }
   __shared__ double nrm[1];
   if (reduce_last<1>(acc, 1, part, &st->counter[2], nrm)) {
-    if (threadIdx.x == 0) arnoldi_close_step(st, j, m, nrm[0], hist, hist_cap);
+    if (threadIdx.x == 0) {
+      if (close)
+        arnoldi_close_step(st, j, m, nrm[0], hist, hist_cap);
+      else
+        st->wn2l = nrm[0];  // sharded: all-reduced into wn2, then close_step_kernel
+    }
   }
+}
+
+// sharded: close step j once ||w''||^2 is global
+__global__ void close_step_kernel(GmState* st, int j, int m, double* hist, int hist_cap) {
+  if (st->stop) return;
+  arnoldi_close_step(st, j, m, st->wn2, hist, hist_cap);
 }
 
 // v_{j+1} = w * invh (a no-op once the cycle stopped)
@@ -258,10 +272,30 @@ __global__ void next_basis_kernel(const double* __restrict__ w, double* __restri
     out[e] = s * w[e];
 }
 
-// r = b - Ax -> V_0 ; ||r||, (first call) ||b|| ; the last block starts the cycle
+// cycle start from ||r||^2 and ||b||^2 (one thread)
+__device__ void begin_cycle(GmState* st, double rr, double bb, double rtol) {
+  const double beta = sqrt(rr);
+  if (st->first) {
+    st->bnorm = sqrt(bb);
+    st->target = rtol * st->bnorm;
+    st->first = 0;
+  }
+  st->beta = beta;
+  st->rel_true = st->bnorm > 0 ? beta / st->bnorm : 0.0;
+  st->k = 0;
+  for (int i = 0; i <= KMAX; ++i) st->g[i] = 0.0;
+  st->g[0] = beta;
+  st->invh = beta > 0.0 ? 1.0 / beta : 0.0;
+  if (!isfinite(beta)) st->breakdown = 1;
+  st->stop = (beta <= st->target || st->bnorm == 0.0 || st->iters >= st->max_iters || st->breakdown) ? 1 : 0;
+}
+
+// r = b - Ax -> V_0 ; ||r||, (first call) ||b|| ; the last block starts the cycle (single rank) or
+// leaves the partial sums for the all-reduce (sharded)
 __global__ void __launch_bounds__(RT) residual_start_kernel(const double* __restrict__ b,
                                                             const double* __restrict__ Ax, double* __restrict__ r,
-                                                            int64_t N, double* part, GmState* st, double rtol) {
+                                                            int64_t N, double* part, GmState* st, double rtol,
+                                                            int close) {
   double acc[2] = {0.0, 0.0};
   for (int64_t e = blockIdx.x * (int64_t)RT + threadIdx.x; e < N; e += (int64_t)gridDim.x * RT) {
     const double bv = b[e];
@@ -272,22 +306,16 @@ __global__ void __launch_bounds__(RT) residual_start_kernel(const double* __rest
   }
   __shared__ double out[2];
   if (reduce_last<2>(acc, 2, part, &st->counter[3], out) && threadIdx.x == 0) {
-    const double beta = sqrt(out[0]);
-    if (st->first) {
-      st->bnorm = sqrt(out[1]);
-      st->target = rtol * st->bnorm;
-      st->first = 0;
+    if (close) {
+      begin_cycle(st, out[0], out[1], rtol);
+    } else {
+      st->rsl[0] = out[0];
+      st->rsl[1] = out[1];
     }
-    st->beta = beta;
-    st->rel_true = st->bnorm > 0 ? beta / st->bnorm : 0.0;
-    st->k = 0;
-    for (int i = 0; i <= KMAX; ++i) st->g[i] = 0.0;
-    st->g[0] = beta;
-    st->invh = beta > 0.0 ? 1.0 / beta : 0.0;
-    if (!isfinite(beta)) st->breakdown = 1;
-    st->stop = (beta <= st->target || st->bnorm == 0.0 || st->iters >= st->max_iters || st->breakdown) ? 1 : 0;
   }
 }
+
+__global__ void begin_cycle_kernel(GmState* st, double rtol) { begin_cycle(st, st->rs[0], st->rs[1], rtol); }
 
 // V_0 = r / beta in place
 __global__ void scale_start_kernel(double* __restrict__ v, int64_t N, const GmState* st) {
@@ -331,15 +359,26 @@ __global__ void axpy_kernel(const double* __restrict__ z, double* __restrict__ x
 struct Ws {
   int64_t N, ldv;
   int nblk;
+  bool sh;  // nranks > 1: reductions are all-reduced between the passes
   double *V, *z, *w, *part, *hist;
   GmState* st;
 };
 
 template <int K>
-void passes_k(fdiga_ctx* ctx, const Ws& W, int j, int m, int hist_cap) {
-  arnoldi_pass1<K><<<W.nblk, RT, 0, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, W.st);
-  arnoldi_pass2<K><<<W.nblk, RT, 0, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, W.st);
-  arnoldi_pass3<K><<<W.nblk, RT, 0, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, W.st, j, m, W.hist, hist_cap);
+int passes_k(fdiga_ctx* ctx, const Ws& W, int j, int m, int hist_cap) {
+  GmState* st = W.st;
+  arnoldi_pass1<K><<<W.nblk, RT, 0, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, W.sh ? st->h1l : st->h1);
+  if (W.sh) FDIGA_TRY(comm_allreduce(ctx, st->h1l, st->h1, K + 1));
+  arnoldi_pass2<K><<<W.nblk, RT, 0, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, W.sh ? st->h2l : st->h2);
+  if (W.sh) FDIGA_TRY(comm_allreduce(ctx, st->h2l, st->h2, K + 1));
+  arnoldi_pass3<K><<<W.nblk, RT, 0, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, j, m, W.hist, hist_cap,
+                                                   W.sh ? 0 : 1);
+  if (W.sh) {
+    FDIGA_TRY(comm_allreduce(ctx, &st->wn2l, &st->wn2, 1));
+    close_step_kernel<<<1, 1, 0, ctx->stream>>>(st, j, m, W.hist, hist_cap);
+    count_launch(ctx);
+  }
+  return FDIGA_OK;
 }
 
 // The three CGS2 passes of step j with k = j + 1 basis vectors (one instantiation per k: fully
@@ -348,7 +387,7 @@ int launch_passes(fdiga_ctx* ctx, const Ws& W, int k, int j, int m, int hist_cap
   switch (k) {
 #define FDIGA_K(K) \
   case K:          \
-    passes_k<K>(ctx, W, j, m, hist_cap); \
+    FDIGA_TRY(passes_k<K>(ctx, W, j, m, hist_cap)); \
     break;
     FDIGA_K(1) FDIGA_K(2) FDIGA_K(3) FDIGA_K(4) FDIGA_K(5) FDIGA_K(6) FDIGA_K(7) FDIGA_K(8)
     FDIGA_K(9) FDIGA_K(10) FDIGA_K(11) FDIGA_K(12) FDIGA_K(13) FDIGA_K(14) FDIGA_K(15) FDIGA_K(16)
@@ -409,7 +448,7 @@ void destroy_gmres_graph(fdiga_ctx* ctx) {
 
 extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const double* b, double* x,
                            const gmres_opts* opts, gmres_report* rep) {
-  FDIGA_CHECK(ctx && A && b && x, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_CHECK(ctx && A && ((b && x) || stencil_local_rows(A) == 0), FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_TRY(bind(ctx));
   const int m = opts ? opts->m : 30;
   const double rtol = opts ? opts->rtol : 1e-8;
@@ -420,7 +459,12 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   int64_t nnz = 0, nd[3] = {1, 1, 1};
   FDIGA_TRY(stencil_info(A, &nnz, nd, nullptr, nullptr));
   Ws W;
-  W.N = nd[0] * nd[1] * nd[2];
+  W.N = stencil_local_rows(A);
+  W.sh = ctx->sharded;
+  const bool use_graph = comm_capturable(ctx);
+  FDIGA_CHECK(!P || fd_plan_local_size(P) == W.N, FDIGA_ERR_INVALID_ARG,
+              "preconditioner and operator sizes differ (%lld vs %lld local rows)",
+              (long long)(P ? fd_plan_local_size(P) : 0), (long long)W.N);
   W.ldv = (W.N + 63) & ~int64_t(63);  // 512-byte aligned basis vectors
   W.nblk = (int)std::max<int64_t>(1, std::min<int64_t>((W.N + RT - 1) / RT, 4 * ctx->sm_count));
   const int hist_cap = std::max(max_iters, 1);
@@ -445,7 +489,7 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
     destroy_gmres_graph(ctx);
     G = nullptr;
   }
-  if (!G) {
+  if (!G && use_graph) {
     G = new GmresGraph();
     ctx->gmres_graph = G;
     G->A = A;
@@ -498,7 +542,12 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   while (true) {
     // true residual r = b - A x, cycle start (device decides whether to stop)
     FDIGA_TRY(stencil_matvec(A, x, W.w));
-    residual_start_kernel<<<W.nblk, RT, 0, st>>>(b, W.w, W.V, W.N, W.part, W.st, rtol);
+    residual_start_kernel<<<W.nblk, RT, 0, st>>>(b, W.w, W.V, W.N, W.part, W.st, rtol, W.sh ? 0 : 1);
+    if (W.sh) {
+      FDIGA_TRY(comm_allreduce(ctx, W.st->rsl, W.st->rs, 2));
+      begin_cycle_kernel<<<1, 1, 0, st>>>(W.st, rtol);
+      count_launch(ctx);
+    }
     scale_start_kernel<<<W.nblk, RT, 0, st>>>(W.V, W.N, W.st);
     count_launch(ctx, 2);
     FDIGA_CUDA(cudaGetLastError());
@@ -518,8 +567,12 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
     }
     ++cycles;
     // one cycle: the captured Arnoldi steps, then x += P^{-1}(V y)
-    FDIGA_CUDA(cudaGraphLaunch(G->exec, st));
-    count_launch(ctx, 1);
+    if (G) {
+      FDIGA_CUDA(cudaGraphLaunch(G->exec, st));
+      count_launch(ctx, 1);
+    } else {
+      FDIGA_TRY(enqueue_cycle(ctx, A, P, W, m, hist_cap));  // loopback transport: not capturable
+    }
     solve_y_kernel<<<1, 1, 0, st>>>(W.st);
     lincomb_kernel<<<W.nblk, RT, 0, st>>>(W.V, W.ldv, W.w, W.N, W.st);
     count_launch(ctx, 2);

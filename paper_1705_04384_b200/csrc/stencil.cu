@@ -42,6 +42,13 @@ struct fdiga_stencil {
   int wm1 = 0;                    // max window width in direction 1
   int32_t* voff1 = nullptr;       // device, n1 x wm1
   std::vector<int32_t> hvoff1;
+  // slab sharding of the rows (3D, nranks > 1): this rank stores the rows of planes
+  // i3 in [o, e) (Nloc rows, values from offset vbase of the global layout on) and reads x planes
+  // [lo, hi); the planes outside [o, e) arrive from their owners into halo_lo / halo_hi.
+  int64_t o = 0, e = 1, lo = 0, hi = 1, Nloc = 0, vbase = 0;
+  double* halo = nullptr;         // (o - lo + hi - e) planes: lower halo, then upper halo
+  std::vector<fdiga::P2PMsg> hsend, hrecv;  // halo messages (x pointers patched per call)
+  std::vector<int64_t> hsend_plane;         // first plane (global) of each send
 };
 
 namespace {
@@ -250,15 +257,16 @@ struct AsmArgs {
   int wm1;
   Geo geo;
   double* vals;
+  int64_t row0, nrows, vbase;  // sharded: global row of thread 0, rows to assemble, value offset of row0
 };
 
 // One thread per collocation row: geometry coefficients G = (J^T J)^{-1}, beta, then the w3*w2*w1
 // box of values  sum_t c_t prod_l B^{(t_l)}.  All small arrays are statically indexed (registers).
 template <int D>
 __global__ void assemble_kernel(AsmArgs A) {
-  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t N = A.n1 * A.n2 * A.n3;
-  if (row >= N) return;
+  const int64_t lrow = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (lrow >= A.nrows) return;
+  const int64_t row = A.row0 + lrow;
   const int64_t i1 = row % A.n1, i2 = (row / A.n1) % A.n2, i3 = row / (A.n1 * A.n2);
   const double x0 = A.tau1[i1], x1 = A.tau2[i2], x2 = (D == 3) ? A.tau3[i3] : 0.0;
   const JH g = geometry_jh(A.geo, x0, x1, x2);
@@ -303,7 +311,7 @@ __global__ void assemble_kernel(AsmArgs A) {
     f2[r] = A.tab2 + (r * A.n2 + i2) * W;
     f3[r] = (D == 3) ? A.tab3 + (r * A.n3 + i3) * W : nullptr;
   }
-  double* out = A.vals + line;
+  double* out = A.vals + (line - A.vbase);
   for (int a = 0; a < w3; ++a)
     for (int b = 0; b < w2; ++b)
       for (int c = 0; c < w1; ++c) {
@@ -339,32 +347,45 @@ struct MvArgs {
   const double* x;
   double* y;
   const int* skip;  // device flag: nonzero -> no-op (GMRES graph early exit)
+  // sharded rows (SH = true): local row r is global row r + o n1 n2; x holds planes [o, e), halo_lo
+  // planes [lo, o), halo_hi planes [e, hi)
+  int64_t o, e, lo, vbase;
+  const double *halo_lo, *halo_hi;
 };
+
+template <bool SH>
+__device__ __forceinline__ const double* x_plane(const MvArgs& A, int64_t g, int64_t n12) {
+  if (!SH) return A.x + g * n12;
+  if (g < A.o) return A.halo_lo + (g - A.lo) * n12;
+  if (g >= A.e) return A.halo_hi + (g - A.e) * n12;
+  return A.x + (g - A.o) * n12;
+}
 
 // y = A x, one thread per row (flattened, i1 fastest).  For every window pair q = (a, b) the thread
 // reads its w1 <= WM values at vals[line + q S1 + voff1(i1, c)] -- consecutive rows hit consecutive
 // addresses, so every warp load is a full 256-byte coalesced stream (values are read exactly once,
 // streaming / evict-first) -- and the matching x window x[(s3+a) n1 n2 + (s2+b) n1 + s1 + c]
 // through L1/L2 (x of neighbouring rows overlaps).  Bytes moved: 8 nnz + 16 N.
-template <int WM, int UB, int MINB>
+template <int WM, int UB, int MINB, bool SH>
 __global__ void __launch_bounds__(256, MINB) matvec_kernel(MvArgs A) {
   const uint32_t r = blockIdx.x * 256u + threadIdx.x;
   if (r >= (uint32_t)A.N || (A.skip && *A.skip)) return;
   const uint32_t n1 = (uint32_t)A.n1, n2 = (uint32_t)A.n2;
   const uint32_t i1 = r % n1, line = r / n1;
-  const uint32_t i2 = line % n2, i3 = line / n2;
+  const uint32_t i2 = line % n2, i3 = line / n2 + (SH ? (uint32_t)A.o : 0u);
   const int w1 = __ldg(A.w1 + i1), w2 = __ldg(A.w2 + i2), w3 = __ldg(A.w3 + i3);
   const int64_t S1 = A.S1;
   const int64_t n12 = (int64_t)n1 * n2;
   // per-thread value pointers for every column c of the window; advanced by UB * S1 per batch of
   // UB window pairs q = a * w2 + b
   const double* __restrict__ vbase =
-      A.vals + __ldg(A.pre3 + i3) * A.S2 * S1 + (int64_t)w3 * __ldg(A.pre2 + i2) * S1;
+      A.vals + (__ldg(A.pre3 + i3) * A.S2 * S1 - (SH ? A.vbase : 0)) + (int64_t)w3 * __ldg(A.pre2 + i2) * S1;
   const double* pv[WM];
 #pragma unroll
   for (int c = 0; c < WM; ++c) pv[c] = vbase + ((c < w1) ? __ldg(A.voff1 + i1 * WM + c) : 0);
-  const double* __restrict__ xb =
-      A.x + (int64_t)__ldg(A.st3 + i3) * n12 + (int64_t)__ldg(A.st2 + i2) * n1 + __ldg(A.st1 + i1);
+  const int64_t g0 = __ldg(A.st3 + i3);
+  const int64_t xoff = (int64_t)__ldg(A.st2 + i2) * n1 + __ldg(A.st1 + i1);
+  const double* __restrict__ xa = x_plane<SH>(A, g0, n12) + xoff;  // x window row of plane g0 + a
   const int nq = w3 * w2;
   int a = 0, b = 0;
   double acc[UB];
@@ -380,13 +401,14 @@ __global__ void __launch_bounds__(256, MINB) matvec_kernel(MvArgs A) {
 #pragma unroll
     for (int u = 0; u < UB; ++u) {
       if (q0 + u < nq) {
-        const double* xq = xb + a * n12 + (int64_t)b * n1;
+        const double* xq = xa + (int64_t)b * n1;
 #pragma unroll
         for (int c = 0; c < WM; ++c)
           if (c < w1) acc[u] = fma(vv[u][c], __ldg(xq + c), acc[u]);
         if (++b == w2) {
           b = 0;
           ++a;
+          xa = x_plane<SH>(A, g0 + a, n12) + xoff;
         }
       }
     }
@@ -409,15 +431,17 @@ struct PermArgs {
   const double* src;
   double* dst;
   int to_internal;
+  int64_t row0, vbase;  // sharded: first global row, value offset of that row (P.N = local rows)
 };
 
 __global__ void permute_kernel(PermArgs P) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= P.N) return;
+  const int64_t lr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (lr >= P.N) return;
+  const int64_t r = P.row0 + lr;
   const int64_t i1 = r % P.n1, line = r / P.n1;
   const int64_t i2 = line % P.n2, i3 = line / P.n2;
   const int w1 = P.w1[i1], w2 = P.w2[i2], w3 = P.w3[i3];
-  const int64_t lb = P.pre3[i3] * P.S2 * P.S1 + (int64_t)w3 * P.pre2[i2] * P.S1;
+  const int64_t lb = P.pre3[i3] * P.S2 * P.S1 + (int64_t)w3 * P.pre2[i2] * P.S1 - P.vbase;
   const int64_t cb = lb + (int64_t)w3 * w2 * P.pre1[i1];
   for (int q = 0; q < w3 * w2; ++q)
     for (int c = 0; c < w1; ++c) {
@@ -433,9 +457,16 @@ MvArgs make_mv_args(const fdiga_stencil* S, const double* x, double* y) {
   A.n1 = S->n[0];
   A.n2 = S->n[1];
   A.n3 = S->n[2];
-  A.N = S->N;
+  A.N = S->Nloc;
   A.S1 = S->hpre[0][S->n[0]];
   A.S2 = S->hpre[1][S->n[1]];
+  A.o = S->o;
+  A.e = S->e;
+  A.lo = S->lo;
+  A.vbase = S->vbase;
+  const int64_t plane = S->n[0] * S->n[1];
+  A.halo_lo = S->halo;
+  A.halo_hi = S->halo ? S->halo + (S->o - S->lo) * plane : nullptr;
   A.st1 = S->start[0];
   A.st2 = S->start[1];
   A.st3 = S->start[2];
@@ -456,7 +487,9 @@ int permute_values(fdiga_stencil* S, const double* src, double* dst, int to_inte
   P.n1 = S->n[0];
   P.n2 = S->n[1];
   P.n3 = S->n[2];
-  P.N = S->N;
+  P.N = S->Nloc;
+  P.row0 = S->o * S->n[0] * S->n[1];
+  P.vbase = S->vbase;
   P.S1 = S->hpre[0][S->n[0]];
   P.S2 = S->hpre[1][S->n[1]];
   P.w1 = S->width[0];
@@ -470,7 +503,8 @@ int permute_values(fdiga_stencil* S, const double* src, double* dst, int to_inte
   P.src = src;
   P.dst = dst;
   P.to_internal = to_internal;
-  permute_kernel<<<(unsigned)((S->N + 255) / 256), 256, 0, S->ctx->stream>>>(P);
+  if (S->Nloc == 0) return FDIGA_OK;
+  permute_kernel<<<(unsigned)((S->Nloc + 255) / 256), 256, 0, S->ctx->stream>>>(P);
   count_launch(S->ctx);
   FDIGA_CUDA(cudaGetLastError());
   FDIGA_CUDA(cudaStreamSynchronize(S->ctx->stream));
@@ -495,9 +529,42 @@ int finish_stencil(fdiga_stencil* S) {
     FDIGA_CUDA(cudaMemcpy(S->width[l], S->hwidth[l].data(), nl * sizeof(int32_t), cudaMemcpyHostToDevice));
     FDIGA_CUDA(cudaMemcpy(S->pre[l], S->hpre[l].data(), (nl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
-  S->nnz = S->hpre[0][S->n[0]] * S->hpre[1][S->n[1]] * S->hpre[2][S->n[2]];
+  // this rank's slab of planes (3D) and the x planes its rows read
+  fdiga_ctx* ctx = S->ctx;
+  const int64_t plane = S->n[0] * S->n[1];
+  partition(S->n[2], ctx->nranks, ctx->rank, &S->o, &S->e);
+  S->Nloc = (S->e - S->o) * plane;
+  const int64_t S12 = S->hpre[0][S->n[0]] * S->hpre[1][S->n[1]];
+  S->vbase = S->hpre[2][S->o] * S12;
+  S->nnz = (S->hpre[2][S->e] - S->hpre[2][S->o]) * S12;
+  const int nr = ctx->sharded ? ctx->nranks : 1;
+  std::vector<int64_t> sb(nr), se(nr), rb(nr), re(nr);
+  FDIGA_TRY(fdiga_halo_plan(S->n[2], S->hstart[2].data(), S->hwidth[2].data(), nr, ctx->sharded ? ctx->rank : 0,
+                            &S->lo, &S->hi, sb.data(), se.data(), rb.data(), re.data()));
+  if (ctx->sharded) {
+    // halo messages: my planes inside every other rank's needed range (one contiguous run per pair)
+    S->hsend.clear();
+    S->hrecv.clear();
+    S->hsend_plane.clear();
+    for (int q = 0; q < nr; ++q) {
+      if (se[q] > sb[q]) {
+        S->hsend.push_back({q, nullptr, (size_t)((se[q] - sb[q]) * plane) * 8});
+        S->hsend_plane.push_back(sb[q]);
+      }
+      if (re[q] > rb[q]) S->hrecv.push_back({q, (void*)(intptr_t)rb[q], (size_t)((re[q] - rb[q]) * plane) * 8});
+    }
+    const int64_t nh = (S->o - S->lo) + (S->hi - S->e);
+    if (nh > 0) {
+      FDIGA_CUDA(cudaMalloc(&S->halo, (size_t)nh * plane * sizeof(double)));
+      for (auto& m : S->hrecv) {  // patch the destinations: lower halo [lo, o), upper halo [e, hi)
+        const int64_t pl = (int64_t)(intptr_t)m.ptr;
+        const int64_t off = pl < S->o ? (pl - S->lo) : (S->o - S->lo) + (pl - S->e);
+        m.ptr = S->halo + off * plane;
+      }
+    }
+  }
   FDIGA_CHECK(S->hpre[0][S->n[0]] < (int64_t(1) << 31), FDIGA_ERR_NOT_SUPPORTED, "direction-1 windows too large");
-  FDIGA_CHECK(S->N < (int64_t(1) << 31) - 256, FDIGA_ERR_NOT_SUPPORTED, "more than 2^31 rows per rank");
+  FDIGA_CHECK(S->Nloc < (int64_t(1) << 31) - 256, FDIGA_ERR_NOT_SUPPORTED, "more than 2^31 rows per rank");
   // internal layout: column-major over c within each q-block, rows of the line compacted per column
   const int64_t n1 = S->n[0];
   int wm1 = 0;
@@ -549,6 +616,7 @@ int stencil_destroy(fdiga_stencil* S) {
   }
   cudaFree(S->vals);
   cudaFree(S->voff1);
+  cudaFree(S->halo);
   delete S;
   return FDIGA_OK;
 }
@@ -557,7 +625,7 @@ int stencil_create(fdiga_ctx* ctx, int d, const int64_t* n, const int32_t* const
                    const double* values, int values_on_device, fdiga_stencil** out) {
   FDIGA_CHECK(ctx && n && start && width && values && out, FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_CHECK(d == 2 || d == 3, FDIGA_ERR_INVALID_ARG, "d must be 2 or 3");
-  FDIGA_CHECK(ctx->nranks == 1, FDIGA_ERR_NOT_SUPPORTED, "multi-rank stencil is not built in this version");
+  FDIGA_CHECK(!ctx->sharded || d == 3, FDIGA_ERR_NOT_SUPPORTED, "2D operators are not sharded (replicas only)");
   *out = nullptr;
   FDIGA_TRY(bind(ctx));
   fdiga_stencil* S = new_stencil(ctx, d, n);
@@ -594,7 +662,7 @@ int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometr
   FDIGA_CHECK(ctx && ne && out, FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_CHECK(d == 2 || d == 3, FDIGA_ERR_INVALID_ARG, "d must be 2 or 3");
   FDIGA_CHECK(p >= 1 && p <= 8, FDIGA_ERR_INVALID_ARG, "degree p = %d out of range", p);
-  FDIGA_CHECK(ctx->nranks == 1, FDIGA_ERR_NOT_SUPPORTED, "multi-rank stencil is not built in this version");
+  FDIGA_CHECK(!ctx->sharded || d == 3, FDIGA_ERR_NOT_SUPPORTED, "2D operators are not sharded (replicas only)");
   const bool ok_geo = geometry_id == FDIGA_GEOM_IDENTITY || (geometry_id == FDIGA_GEOM_ANNULUS && d == 2) ||
                       ((geometry_id == FDIGA_GEOM_DEFORMED_CUBE || geometry_id == FDIGA_GEOM_THICK_RING) && d == 3);
   FDIGA_CHECK(ok_geo, FDIGA_ERR_INVALID_ARG, "geometry %d not available in %dD", geometry_id, d);
@@ -666,7 +734,10 @@ int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometr
     if (e == cudaSuccess) e = cudaMemsetAsync(S->vals, 0, (S->nnz + 2) * sizeof(double), ctx->stream);
     if (e == cudaSuccess) {
       A.vals = S->vals;
-      const int64_t blocks = (S->N + 127) / 128;
+      A.row0 = S->o * n[0] * n[1];
+      A.nrows = S->Nloc;
+      A.vbase = S->vbase;
+      const int64_t blocks = std::max<int64_t>(1, (S->Nloc + 127) / 128);
       if (d == 3)
         assemble_kernel<3><<<(unsigned)blocks, 128, 0, ctx->stream>>>(A);
       else
@@ -695,13 +766,21 @@ int stencil_matvec(fdiga_stencil* S, const double* x, double* y) { return fdiga:
 
 namespace fdiga {
 int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* skip) {
-  FDIGA_CHECK(S && x && y, FDIGA_ERR_INVALID_ARG, "NULL argument");
-  FDIGA_CHECK(x != y, FDIGA_ERR_INVALID_ARG, "stencil_matvec: x and y must not alias");
+  FDIGA_CHECK(S && ((x && y) || S->Nloc == 0), FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_CHECK(x != y || S->Nloc == 0, FDIGA_ERR_INVALID_ARG, "stencil_matvec: x and y must not alias");
   fdiga_ctx* ctx = S->ctx;
   FDIGA_TRY(bind(ctx));
+  const bool sh = ctx->sharded;
+  if (sh) {  // halo planes from the neighbouring slabs (collective: every rank takes part)
+    std::vector<P2PMsg> snd = S->hsend;
+    for (size_t i = 0; i < snd.size(); ++i)
+      snd[i].ptr = const_cast<double*>(x) + (S->hsend_plane[i] - S->o) * S->n[0] * S->n[1];
+    FDIGA_TRY(comm_exchange(ctx, snd, S->hrecv));
+  }
+  if (S->Nloc == 0) return FDIGA_OK;
   MvArgs A = make_mv_args(S, x, y);
   A.skip = skip;
-  const unsigned grid = (unsigned)((S->N + 255) / 256);
+  const unsigned grid = (unsigned)((S->Nloc + 255) / 256);
   // variant: batch UB window pairs per load phase; selectable for experiments with FDIGA_MV_VARIANT
   static int variant = -1;
   if (variant < 0) {
@@ -709,18 +788,23 @@ int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* s
     variant = v ? atoi(v) : 1;
   }
   switch (S->wm1 * 10 + variant) {
+#define FDIGA_MV_LAUNCH(W, UB, MB)                                                                      \
+  if (sh)                                                                                              \
+    matvec_kernel<W, UB, MB, true><<<grid, 256, 0, ctx->stream>>>(A);                                  \
+  else                                                                                                 \
+    matvec_kernel<W, UB, MB, false><<<grid, 256, 0, ctx->stream>>>(A);
 #define FDIGA_MV_CASE(W)                                                     \
   case W * 10 + 0:                                                          \
-    matvec_kernel<W, 1, 4><<<grid, 256, 0, ctx->stream>>>(A);               \
+    FDIGA_MV_LAUNCH(W, 1, 4)                                                \
     break;                                                                  \
   case W * 10 + 1:                                                          \
-    matvec_kernel<W, 2, 3><<<grid, 256, 0, ctx->stream>>>(A);               \
+    FDIGA_MV_LAUNCH(W, 2, 3)                                                \
     break;                                                                  \
   case W * 10 + 2:                                                          \
-    matvec_kernel<W, 3, 2><<<grid, 256, 0, ctx->stream>>>(A);               \
+    FDIGA_MV_LAUNCH(W, 3, 2)                                                \
     break;                                                                  \
   case W * 10 + 3:                                                          \
-    matvec_kernel<W, 4, 2><<<grid, 256, 0, ctx->stream>>>(A);               \
+    FDIGA_MV_LAUNCH(W, 4, 2)                                                \
     break;
     FDIGA_MV_CASE(1)
     FDIGA_MV_CASE(2)
@@ -732,6 +816,7 @@ int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* s
     FDIGA_MV_CASE(8)
     FDIGA_MV_CASE(9)
 #undef FDIGA_MV_CASE
+#undef FDIGA_MV_LAUNCH
     default:
       FDIGA_CHECK(false, FDIGA_ERR_NOT_SUPPORTED, "window width %d / variant %d", S->wm1, variant);
   }
@@ -739,6 +824,8 @@ int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* s
   FDIGA_CUDA(cudaGetLastError());
   return FDIGA_OK;
 }
+
+int64_t stencil_local_rows(const fdiga_stencil* S) { return S->Nloc; }
 
 }  // namespace fdiga
 
@@ -769,6 +856,16 @@ int stencil_get_values(const fdiga_stencil* S, double* values_host) {
   }
   cudaFree(canon);
   return s;
+}
+
+int colloc_1d_windows(int p, int64_t ne, int32_t* start, int32_t* width) {
+  FDIGA_CHECK(start && width && p >= 1 && ne >= 1 && ne + p - 2 >= 1, FDIGA_ERR_INVALID_ARG,
+              "bad colloc_1d_windows arguments");
+  Table1D T;
+  build_table(p, ne, T);
+  std::memcpy(start, T.start.data(), T.n * sizeof(int32_t));
+  std::memcpy(width, T.width.data(), T.n * sizeof(int32_t));
+  return FDIGA_OK;
 }
 
 int colloc_1d_factors(int p, int64_t ne, double* M, double* K) {
