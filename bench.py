@@ -109,6 +109,15 @@ def dist_init():
     return ws, rank, local
 
 
+def weak_shape(n, ws):
+    """Weak-scaling FD family: N/P fixed at n^3; directions doubled from the last one
+    (P = 1, 2, 4, 8 -> (n,n,n), (n,n,2n), (n,2n,2n), (2n,2n,2n)); other P stretch the last axis."""
+    if ws & (ws - 1) == 0 and ws <= 8:
+        k = ws.bit_length() - 1
+        return tuple(n * (2 if l >= 3 - k else 1) for l in range(3))
+    return (n, n, n * ws)
+
+
 def cpu_fd_sample(n, budget_s=12.0, max_reps=20):
     """Oracle FD apply (numpy mode products, all host BLAS threads) on cfg4 factors: GDOF/s."""
     from oracle import fastdiag
@@ -135,34 +144,47 @@ def cpu_fd_sample(n, budget_s=12.0, max_reps=20):
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle (numpy mode products) on this box's host cores, on the same
+    workload as our arm at this N (weak-scaling shape), rank 0 only.  Steps are capped so that the run
+    stays within ~1 minute of CPU work (a bounded sample; the JSON says how many applies were timed)."""
     ws, rank, _ = dist_init()
     if rank != 0:
         return
     n = args.n
+    ns = weak_shape(n, ws)
+    N = int(np.prod(ns))
     from oracle import fastdiag
     from synth import fd_sweep_factors, fd_sweep_vector
-    rng, U, lam = fd_sweep_factors(n)
+    rng, U, lam = fd_sweep_factors(ns)
     f = fastdiag.factors_from_eig(U, lam)
-    x = fd_sweep_vector(rng, n ** 3)
-    for _ in range(args.warmup):
-        fastdiag.apply(f, x)
+    x = fd_sweep_vector(rng, N)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    fastdiag.apply(f, x)
+    t_one = time.perf_counter() - t0
+    warm = max(0, min(args.warmup, int(20.0 / max(t_one, 1e-3))) - 1)
+    for _ in range(warm):
         fastdiag.apply(f, x)
-    dt = (time.perf_counter() - t0) / args.steps
+    steps = max(1, min(args.steps, int(60.0 / max(t_one, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        fastdiag.apply(f, x)
+    dt = (time.perf_counter() - t0) / steps
     try:
         from threadpoolctl import threadpool_info
         threads = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
     except Exception:
         threads = os.cpu_count()
-    val = n ** 3 / dt / 1e9
+    val = N / dt / 1e9
+    shape = "x".join(map(str, ns))
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": val, "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GDOF/s", "n_gpus": ws, "steps": steps,
+        "warmup": warm + 1, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg4 FD apply n={n} (oracle, CPU)", "n": n, "N": n ** 3},
+        "config": {"workload": f"cfg4 FD apply P^-1 r, d=3, n={shape} (oracle on the host CPU)", "n": n,
+                   "shape": list(ns), "N": N},
         "cpu_baseline": {"value": val, "unit": "GDOF/s", "cores": threads, "kind": "oracle",
-                         "sample": f"{args.steps} oracle FD applies at n={n} after {args.warmup} warm-up"},
+                         "sample": f"{steps} oracle FD applies at {shape} after {warm + 1} warm-up "
+                                   f"(requested --steps {args.steps}; capped at ~60 s of CPU work)"},
         "e2e": {"value": val, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -187,41 +209,55 @@ def timed(fn, stream, steps, warmup, sync_all=None):
     return e0.elapsed_time(e1) / steps
 
 
-def gmres_section(ctx, fd, steps):
+def gmres_section(ctx, fd, steps, ws=1, rank=0, sharded=False):
+    """GMRES(30) time-to-1e-8 on configs[1], [2], [4] (single GPU) or, sharded over ws > 1 ranks, on the
+    3D configs [2] and [4] (2D problems run as replicas only).  Device time, max over ranks."""
     import torch
+    import torch.distributed as dist
     from synth import get_config, rhs
     out = {}
     dev = torch.device("cuda", torch.cuda.current_device())
     hbm, hbm_src = hbm_peak()
-    for cfg in (2, 3, 5):
+
+    def gmax(v):
+        if ws == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for cfg in ((3, 5) if sharded else (2, 3, 5)):
         c = get_config(cfg)
         A = fd.colloc_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params)
         M, K = fd.colloc_1d_factors(c.p, c.ne)
         t0 = time.perf_counter()
         P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
         t_setup = time.perf_counter() - t0
-        b = torch.from_numpy(rhs(cfg, A.N)).to(dev)
+        lo = A.slab[0] * A.n[0] * A.n[1]
+        b = torch.from_numpy(rhs(cfg, A.N_global)[lo:lo + A.N].copy()).to(dev)
         x = torch.empty_like(b)
-        rep = fd.gmres_solve(ctx, A, P, b, x)  # warm-up
+        rep = fd.gmres_solve(ctx, A, P, b, x)  # warm-up (captures the cycle graph)
         times, iters = [], []
         for _ in range(max(3, min(steps, 10))):
             rep = fd.gmres_solve(ctx, A, P, b, x)
-            times.append(rep["t_total_ms"])
+            times.append(gmax(rep["t_total_ms"]))
             iters.append(rep["iters"])
         entry = {"time_to_tol_ms": float(np.median(times)), "iters": int(np.median(iters)),
-                 "rel_res_true": rep["rel_res_true"], "n": A.n[0], "N": A.N, "fd_setup_ms": t_setup * 1e3,
-                 "ms_per_iter": float(np.median(times)) / max(1, int(np.median(iters)))}
+                 "rel_res_true": rep["rel_res_true"], "n": A.n[0], "N": A.N_global, "fd_setup_ms": t_setup * 1e3,
+                 "ms_per_iter": float(np.median(times)) / max(1, int(np.median(iters))), "ranks": ws}
         if cfg == 5:
-            # stored-operator matvec roofline (HBM): bytes = 8 nnz + 16 N
+            # stored-operator matvec roofline (HBM): bytes = 8 nnz + 16 N (this rank's rows)
             stream = torch.cuda.current_stream()
             xv = torch.randn(A.N, dtype=torch.float64, device=dev)
             yv = torch.empty_like(xv)
-            ms = timed(lambda: fd.stencil_matvec(A, xv, yv), stream, 20, 3)
+            sync = (lambda: dist.barrier()) if ws > 1 else None
+            ms = gmax(timed(lambda: fd.stencil_matvec(A, xv, yv), stream, 20, 3, sync))
             byts = 8 * A.nnz + 16 * A.N
             entry["matvec"] = {"ms": ms, "nnz": A.nnz, "bytes": byts, "achieved_gbs": byts / ms / 1e6,
-                               "peak_gbs": hbm, "peak_source": hbm_src, "frac": byts / ms / 1e6 / hbm}
+                               "peak_gbs": hbm, "peak_source": hbm_src, "frac": byts / ms / 1e6 / hbm,
+                               "per": "rank" if ws > 1 else "gpu"}
             fd_flops = P.flops()
-            ms_fd = timed(lambda: fd.fd_apply(P, xv, yv), stream, 20, 3)
+            ms_fd = gmax(timed(lambda: fd.fd_apply(P, xv, yv), stream, 20, 3, sync))
             entry["fd_apply"] = {"ms": ms_fd, "tflops": fd_flops / ms_fd / 1e9}
         out[f"cfg{cfg}"] = entry
         P.close()
@@ -238,6 +274,8 @@ def main():
     ap.add_argument("--impl", default="fdiga", choices=["fdiga", "reference"])
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="at --gpus 1: run the slab-sharded path over a one-rank NCCL communicator (tests the N>1 code)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -250,22 +288,37 @@ def main():
 
     ws, rank, local = dist_init()
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    uid = None
+    if ws == 1 and args.sharded:
+        uid = fd.nccl_unique_id()
     if ws > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        # the library's own NCCL communicator: rank 0 draws the unique id, torch.distributed carries it
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            t.copy_(torch.tensor(list(fd.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        uid = bytes(t.cpu().tolist())
 
     def sync_all():
         if ws > 1:
             dist.barrier()
 
-    dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-    ctx = fd.Context(local, stream=stream.cuda_stream)
+    ctx = fd.Context(local, stream=stream.cuda_stream, nranks=ws, rank=rank, nccl_unique_id=uid)
     n = args.n
-    N = n ** 3
+    ns = weak_shape(n, ws)
+    N = int(np.prod(ns))
     # setup (not timed): W_l = U_l^{-1} on the device (fd_setup_from_eig, M = I), BASELINE.json configs[3]
-    rng, U, lam = fd_sweep_factors(n)
+    rng, U, lam = fd_sweep_factors(ns)
     plan = fd.fd_setup_from_eig(ctx, U, lam)
-    x = torch.from_numpy(fd_sweep_vector(rng, N)).to(dev)
+    if ws == 1:
+        x = torch.from_numpy(fd_sweep_vector(rng, N)).to(dev)
+    else:  # this rank's slab, N(0,1) drawn on the device (the full vector is never formed)
+        g = torch.Generator(device=dev)
+        g.manual_seed(4000 + rank)
+        x = torch.randn(plan.N, dtype=torch.float64, device=dev, generator=g)
     s = torch.empty_like(x)
 
     launches0 = ctx.kernel_launches()
@@ -290,14 +343,14 @@ def main():
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = ws * N / (ms * 1e-3) / 1e9
-    flops = plan.flops()
+    value = N / (ms * 1e-3) / 1e9           # all ranks' DOFs / max-over-ranks time
+    flops = plan.flops()                     # whole apply (all ranks)
     peak = fp64_peak()
-    achieved = flops / (ms * 1e-3) / 1e12
+    achieved = flops / ws / (ms * 1e-3) / 1e12   # per GPU
 
     # e2e: same metric through the C ABI with pinned host buffers (H2D + apply + D2H per step)
-    xh = torch.from_numpy(fd_sweep_vector(np.random.default_rng(4001), N)).pin_memory()
-    sh = torch.empty(N, dtype=torch.float64).pin_memory()
+    xh = torch.from_numpy(np.random.default_rng(4001 + rank).standard_normal(plan.N)).pin_memory()
+    sh = torch.empty(plan.N, dtype=torch.float64).pin_memory()
     xh_np, sh_np = xh.numpy(), sh.numpy()
     e2e_steps = max(3, min(args.steps, 20))
     for _ in range(2):
@@ -320,8 +373,8 @@ def main():
             traffic = None
 
     gm = None
-    if not args.no_gmres and rank == 0:
-        gm = gmres_section(ctx, fd, args.steps)
+    if not args.no_gmres:
+        gm = gmres_section(ctx, fd, args.steps, ws, rank, sharded=uid is not None)
     cpu = None
     if rank == 0 and not args.no_cpu and ws == 1:
         cpu = cpu_fd_sample(n)
@@ -331,18 +384,22 @@ def main():
             "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg4 FD apply P^-1 r, d=3, n={n} (BASELINE.json configs[3])", "n": n, "N": N,
+            "config": {"workload": f"cfg4 FD apply P^-1 r, d=3, n={'x'.join(map(str, ns))} (BASELINE.json configs[3]"
+                                   + (", weak-scaling family SURVEY.md §8(d))" if ws > 1 else ")"),
+                       "n": n, "shape": list(ns), "N": N,
                        "factors": "U ~ N(0,1), lam ~ U(1,100), W = U^-1 (device LU), x ~ N(0,1)",
-                       "l2": "inputs > L2: 134 MB vector + 3 x 134 MB work buffers vs 126 MB L2" if n >= 256
+                       "l2": "inputs > L2: 134 MB vector + 3 x 134 MB work buffers per GPU vs 126 MB L2" if n >= 256
                        else "vector fits in L2 (no flush)",
-                       "parallelism": "replicas" if ws > 1 else "single GPU"},
+                       "parallelism": f"slab-sharded over {ws} GPUs (NCCL all-to-all in the mode-d pass)" if ws > 1
+                       else "single GPU"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "dmma_gemm_kernel (6 launches per apply: 3 forward + 3 backward mode products)",
+                         "kernel": "dmma_gemm_kernel (6 launches per apply: 3 forward + 3 backward mode products)"
+                                   + (", per GPU" if ws > 1 else ""),
                          "flops_per_apply": flops,
                          "peak_source": "own DMMA.8x8x4 register loop, sustained 3 s (profiles/r01_peaks_fp64.jsonl); "
                                         "MEASURED_PEAKS.json has no FP64 entry"},
-            "e2e": {"value": N / (e2e_ms * 1e-3) / 1e9 * ws, "unit": "GDOF/s", "ms_per_step": e2e_ms,
+            "e2e": {"value": N / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
                     "path": "fd_apply_host (pinned host buffers, H2D + apply + D2H inside the call)"},
             "gpu_launches": launches,
