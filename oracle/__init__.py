@@ -15,7 +15,8 @@ Modules
             sum-factorised matvec, explicit single rows
   fastdiag  FD setup (generalized eig) and FD apply (loops, mode products), the
             dense Kronecker preconditioner P
-  krylov    right-preconditioned restarted GMRES(m) with MGS (Saad 1986)
+  krylov    right-preconditioned restarted GMRES(m) with MGS (Saad 1986) and
+            right-preconditioned BiCGStab with half-iteration accounting
 
 Parity pins: every function is pinned by tests in tests/test_oracle_*.py against
 values the paper or the mathematics fix (SPEC examples, closed forms, invariants,
