@@ -242,9 +242,18 @@ def gmres_section(ctx, fd, steps, ws=1, rank=0, sharded=False):
             rep = fd.gmres_solve(ctx, A, P, b, x)
             times.append(gmax(rep["t_total_ms"]))
             iters.append(rep["iters"])
+        # the paper's own solver on the same system: BiCGStab + FD, half-iteration counts
+        brep = fd.bicgstab_solve(ctx, A, P, b, x)  # warm-up (captures the chunk graph)
+        btimes = []
+        for _ in range(max(3, min(steps, 10))):
+            brep = fd.bicgstab_solve(ctx, A, P, b, x)
+            btimes.append(gmax(brep["t_total_ms"]))
+        bicg = {"time_to_tol_ms": float(np.median(btimes)), "iters": brep["iters"],
+                "rel_res_true": brep["rel_res_true"]}
         entry = {"time_to_tol_ms": float(np.median(times)), "iters": int(np.median(iters)),
                  "rel_res_true": rep["rel_res_true"], "n": A.n[0], "N": A.N_global, "fd_setup_ms": t_setup * 1e3,
-                 "ms_per_iter": float(np.median(times)) / max(1, int(np.median(iters))), "ranks": ws}
+                 "ms_per_iter": float(np.median(times)) / max(1, int(np.median(iters))), "ranks": ws,
+                 "bicgstab": bicg}
         if cfg == 5:
             # stored-operator matvec roofline (HBM): bytes = 8 nnz + 16 N (this rank's rows)
             stream = torch.cuda.current_stream()

@@ -206,6 +206,32 @@ typedef struct {
 int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const double* b, double* x,
                 const gmres_opts* opts, gmres_report* report);
 
+/* ----------------------------------------------------------------- BiCGStab ---- */
+
+typedef struct {
+  double rtol;    /* stop when the recursive residual <= rtol ||b|| (default 1e-8) */
+  int max_iters;  /* full iterations (default 1000) */
+  int use_x0;     /* 1: x holds the initial guess; 0: x0 = 0 */
+} bicgstab_opts;
+
+typedef struct {
+  double iters;            /* half-iteration count: k - 0.5 when the BiCG half of iteration k converged */
+  int converged;
+  int breakdown;           /* rho, r^.v or t.t vanished (or a non-finite value) before convergence */
+  int half;                /* 1 when convergence happened at a BiCG half step */
+  double rel_res_true;     /* ||b - A x|| / ||b|| at return */
+  double rel_res_recursive;/* the recursive residual that met the test */
+  double t_total_ms;
+  double* history;         /* optional (caller-owned, length history_cap): recursive rel. residual per half step */
+  int history_cap;
+} bicgstab_report;
+
+/* Right-preconditioned BiCGStab (van der Vorst 1992), the paper's solver: every iteration is
+ * a BiCG step then one GMRES(1) step, each with one P^{-1} apply and one matvec; shadow residual r^ = r_0.
+ * b, x: device, local slab.  Returns NOT_CONVERGED / BREAKDOWN with the report filled.  Synchronises. */
+int bicgstab_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const double* b, double* x,
+                   const bicgstab_opts* opts, bicgstab_report* report);
+
 /* ------------------------------------------------------------ instrumentation ---- */
 /* Number of kernels this library launched since the context was created (all entry points). */
 int64_t fdiga_kernel_launches(const fdiga_ctx* ctx);

@@ -25,6 +25,16 @@ class GmresReport(C.Structure):
                 ("history", c_double_p), ("history_cap", C.c_int)]
 
 
+class BicgstabOpts(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("max_iters", C.c_int), ("use_x0", C.c_int)]
+
+
+class BicgstabReport(C.Structure):
+    _fields_ = [("iters", C.c_double), ("converged", C.c_int), ("breakdown", C.c_int), ("half", C.c_int),
+                ("rel_res_true", C.c_double), ("rel_res_recursive", C.c_double), ("t_total_ms", C.c_double),
+                ("history", c_double_p), ("history_cap", C.c_int)]
+
+
 # name -> (restype, argtypes); every symbol include/fdiga.h declares
 SIGNATURES = {
     "fdiga_ctx_create": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
@@ -67,6 +77,8 @@ SIGNATURES = {
     "colloc_1d_factors": (C.c_int, [C.c_int, C.c_int64, c_double_p, c_double_p]),
     "gmres_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(GmresOpts),
                               C.POINTER(GmresReport)]),
+    "bicgstab_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.POINTER(BicgstabOpts), C.POINTER(BicgstabReport)]),
     "fdiga_kernel_launches": (C.c_int64, [C.c_void_p]),
 }
 

@@ -8,7 +8,7 @@ import ctypes as C
 
 import numpy as np
 
-from ._lib import (FdSetupOpts, GmresOpts, GmresReport, c_double_p, c_int32_p, c_int64_p, check, load)
+from ._lib import (BicgstabOpts, BicgstabReport, FdSetupOpts, GmresOpts, GmresReport, c_double_p, c_int32_p, c_int64_p, check, load)
 
 ORTH_CGS_DGKS = 0
 ORTH_CGS2 = 1
@@ -342,4 +342,27 @@ def gmres_solve(ctx, A, P, b, x, m=30, rtol=1e-8, max_iters=1000, orth=ORTH_CGS_
                status=st)
     if hist is not None:
         out["history"] = hist[:rep.iters].copy()
+    return out
+
+
+def bicgstab_solve(ctx, A, P, b, x, rtol=1e-8, max_iters=1000, use_x0=False, history=False,
+                   raise_on_failure=True):
+    """Right-preconditioned BiCGStab (the paper's solver); returns the report as a dict (iters is a
+    half-iteration count)."""
+    opts = BicgstabOpts(float(rtol), int(max_iters), int(use_x0))
+    rep = BicgstabReport()
+    hist = None
+    if history:
+        hist = np.zeros(2 * max_iters)
+        rep.history = _dptr(hist)
+        rep.history_cap = 2 * max_iters
+    st = ctx._lib.bicgstab_solve(ctx.handle, A.handle, P.handle if P is not None else None, _devptr(b, A.N),
+                                 _devptr(x, A.N), C.byref(opts), C.byref(rep))
+    if st != 0 and (raise_on_failure or st not in (-8, -9)):
+        check(st, "bicgstab_solve")
+    out = dict(iters=rep.iters, converged=bool(rep.converged), breakdown=bool(rep.breakdown), half=bool(rep.half),
+               rel_res_true=rep.rel_res_true, rel_res_recursive=rep.rel_res_recursive, t_total_ms=rep.t_total_ms,
+               status=st)
+    if hist is not None:
+        out["history"] = hist[:int(round(2 * rep.iters))].copy()
     return out

@@ -82,6 +82,7 @@ struct fdiga_ctx {
   size_t pinned_cap = 0;
   fdiga::DevBuf ws[4];        // GMRES workspace: basis V, z/w vectors, reduction partials, device state
   void* gmres_graph = nullptr; // cached captured GMRES cycle (krylov.cu)
+  void* bicg_graph = nullptr;  // cached captured BiCGStab iterations (bicgstab.cu)
 };
 
 namespace fdiga {
@@ -107,5 +108,6 @@ int loopback_attach(fdiga_ctx* ctx, fdiga_loopback* hub);
 int64_t stencil_local_rows(const fdiga_stencil* S);
 int64_t fd_plan_local_size(const fd_plan* P);
 // Drop the cached GMRES graph (it captures pointers of A, P and the workspace).
-void destroy_gmres_graph(fdiga_ctx* ctx);
+void destroy_gmres_graph(fdiga_ctx* ctx);  // also drops the BiCGStab graph
+void destroy_bicgstab_graph(fdiga_ctx* ctx);
 }  // namespace fdiga

@@ -346,3 +346,60 @@ def test_kernel_launch_counter(ctx):
     before = ctx.kernel_launches()
     fd.fd_apply(plan, r, r)
     assert ctx.kernel_launches() - before == 6
+
+
+# ----------------------------------------------------------------------------- BiCGStab
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 5])
+def test_bicgstab_iterations_match_oracle(ctx, cfg):
+    c = get_config(cfg)
+    A = fd.colloc_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params)
+    _, M, K, _ = splines.colloc_1d(c.ne, c.p)
+    P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
+    b = gpu(rhs(cfg, A.N))
+    x = torch.empty_like(b)
+    for _ in range(2):  # the second solve replays the captured chunk graph
+        rep = fd.bicgstab_solve(ctx, A, P, b, x)
+        ref = GOLD["configs"][str(cfg)]
+        assert rep["converged"] and not rep["breakdown"]
+        assert abs(rep["iters"] - ref["bicgstab_iters"]) <= 1.0, (rep, ref)
+        assert rep["iters"] % 1 == (0.5 if rep["half"] else 0.0)
+        assert rep["rel_res_true"] <= 2e-8
+    if cfg == 1:
+        assert rep["iters"] == 0.5  # FD is exact on the identity map
+    disc = assembly.Discretisation(c.d, c.p, c.ne, c.geometry, c.geo_params)
+    bh = host(b)
+    assert np.linalg.norm(bh - disc.matvec(host(x))) / np.linalg.norm(bh) <= 2e-8
+
+
+def test_bicgstab_small_matches_oracle_history(ctx):
+    c = get_config(2)
+    ne = 16
+    A = fd.colloc_assemble(ctx, 2, 3, ne, c.geometry, c.geo_params)
+    disc = assembly.Discretisation(2, 3, ne, c.geometry, c.geo_params)
+    f = fastdiag.setup([disc.M] * 2, [disc.K] * 2)
+    P = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
+    bh = rhs(2, disc.N, rep=5)
+    x = torch.empty(disc.N, dtype=torch.float64, device=DEV)
+    rep = fd.bicgstab_solve(ctx, A, P, gpu(bh), x, rtol=1e-11, history=True)
+    xo, repo = krylov.bicgstab(disc.matvec, bh, precond=lambda v: fastdiag.apply(f, v), rtol=1e-11)
+    assert abs(rep["iters"] - repo["iters"]) <= 1.0
+    assert rel(host(x), xo) <= 1e-9
+    k = min(len(rep["history"]), len(repo["history"])) - 2
+    np.testing.assert_allclose(rep["history"][:k], repo["history"][:k], rtol=1e-5)
+
+
+def test_bicgstab_unpreconditioned_and_status(ctx):
+    A = fd.colloc_assemble(ctx, 2, 2, 8, 0)
+    disc = assembly.Discretisation(2, 2, 8, 0)
+    bh = rhs(1, disc.N)
+    x = torch.empty(disc.N, dtype=torch.float64, device=DEV)
+    rep = fd.bicgstab_solve(ctx, A, None, gpu(bh), x, rtol=1e-10, max_iters=500)
+    xo, repo = krylov.bicgstab(disc.matvec, bh, rtol=1e-10, max_iters=500)
+    assert rep["converged"] and abs(rep["iters"] - repo["iters"]) <= 2
+    assert rel(host(x), xo) <= 1e-6
+    A2 = fd.colloc_assemble(ctx, 2, 3, 32, 1, (1.0, 2.0))
+    b2 = gpu(rhs(2, A2.N))
+    x2 = torch.empty_like(b2)
+    rep = fd.bicgstab_solve(ctx, A2, None, b2, x2, max_iters=3, raise_on_failure=False)
+    assert rep["status"] == -8 and not rep["converged"] and rep["iters"] == 3.0

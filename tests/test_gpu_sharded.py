@@ -221,3 +221,46 @@ def test_nccl_one_rank_gmres_captured(nccl_ctx):
         assert rep["rel_res_true"] <= 1e-8
     P.close()
     A.close()
+
+
+@pytest.mark.parametrize("cfg,nranks", [(3, 3), (5, 4)])
+def test_sharded_bicgstab_matches_oracle_counts(cfg, nranks):
+    c = get_config(cfg)
+    _, M, K, _ = splines.colloc_1d(c.ne, c.p)
+    n = M.shape[0]
+    b = rhs(cfg, n ** 3)
+
+    def work(ctx, rank):
+        A = fd.colloc_assemble(ctx, 3, c.p, c.ne, c.geometry, c.geo_params)
+        P = fd.fd_setup(ctx, [M] * 3, [K] * 3)
+        lo, hi = slab_rows(n, nranks, rank, n * n)
+        bt = torch.from_numpy(b[lo:hi].copy()).to(DEV)
+        x = torch.empty_like(bt)
+        rep = fd.bicgstab_solve(ctx, A, P, bt, x)
+        torch.cuda.current_stream().synchronize()
+        out = (rep, x.cpu().numpy())
+        P.close()
+        A.close()
+        return out
+
+    res = run_ranks(nranks, work)
+    reps = [r[0] for r in res]
+    assert all(r["iters"] == reps[0]["iters"] and r["rel_res_true"] == reps[0]["rel_res_true"] for r in reps)
+    assert reps[0]["converged"]
+    assert abs(reps[0]["iters"] - GOLD["configs"][str(cfg)]["bicgstab_iters"]) <= 1.0
+    x = np.concatenate([r[1] for r in res])
+    disc = assembly.Discretisation(3, c.p, c.ne, c.geometry, c.geo_params)
+    assert np.linalg.norm(b - disc.matvec(x)) / np.linalg.norm(b) <= 2e-8
+
+
+def test_nccl_one_rank_bicgstab_captured(nccl_ctx):
+    c = get_config(3)
+    _, M, K, _ = splines.colloc_1d(c.ne, c.p)
+    A = fd.colloc_assemble(nccl_ctx, 3, c.p, c.ne, c.geometry, c.geo_params)
+    P = fd.fd_setup(nccl_ctx, [M] * 3, [K] * 3)
+    b = torch.from_numpy(rhs(3, A.N)).to(DEV)
+    x = torch.empty_like(b)
+    rep = fd.bicgstab_solve(nccl_ctx, A, P, b, x)
+    assert rep["converged"] and abs(rep["iters"] - GOLD["configs"]["3"]["bicgstab_iters"]) <= 1.0
+    P.close()
+    A.close()
