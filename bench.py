@@ -254,6 +254,31 @@ def gmres_section(ctx, fd, steps, ws=1, rank=0, sharded=False):
                  "rel_res_true": rep["rel_res_true"], "n": A.n[0], "N": A.N_global, "fd_setup_ms": t_setup * 1e3,
                  "ms_per_iter": float(np.median(times)) / max(1, int(np.median(iters))), "ranks": ws,
                  "bicgstab": bicg}
+        if c.d == 3:
+            # the same solves with the matrix-free sum-factorised operator (NEXT-1, no stored values)
+            Amf = fd.colloc_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params, matrix_free=True)
+            fd.gmres_solve(ctx, Amf, P, b, x)
+            mt, mi = [], []
+            for _ in range(max(3, min(steps, 10))):
+                r2 = fd.gmres_solve(ctx, Amf, P, b, x)
+                mt.append(gmax(r2["t_total_ms"]))
+                mi.append(r2["iters"])
+            fd.bicgstab_solve(ctx, Amf, P, b, x)
+            bt2 = []
+            for _ in range(max(3, min(steps, 10))):
+                b2 = fd.bicgstab_solve(ctx, Amf, P, b, x)
+                bt2.append(gmax(b2["t_total_ms"]))
+            entry["matrix_free"] = {"gmres_time_to_tol_ms": float(np.median(mt)), "gmres_iters": int(np.median(mi)),
+                                    "gmres_rel_res_true": r2["rel_res_true"],
+                                    "bicgstab_time_to_tol_ms": float(np.median(bt2)), "bicgstab_iters": b2["iters"]}
+            if cfg == 5:
+                stream = torch.cuda.current_stream()
+                xv = torch.randn(A.N, dtype=torch.float64, device=dev)
+                yv = torch.empty_like(xv)
+                sync = (lambda: dist.barrier()) if ws > 1 else None
+                entry["matrix_free"]["matvec_ms"] = gmax(timed(lambda: fd.stencil_matvec(Amf, xv, yv), stream, 20, 3,
+                                                               sync))
+            Amf.close()
         if cfg == 5:
             # stored-operator matvec roofline (HBM): bytes = 8 nnz + 16 N (this rank's rows)
             stream = torch.cuda.current_stream()

@@ -162,6 +162,14 @@ int stencil_create(fdiga_ctx* ctx, int d, const int64_t* n, const int32_t* const
  * with parameters geo_params (see FDIGA_GEOM_*).  Row i holds (L (B_j o F^{-1}))(F(tau_i)). */
 int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
                     fdiga_stencil** out);
+/* The same operator applied MATRIX-FREE (the paper's future work):
+ * no values are stored; stencil_matvec evaluates sum_t c_t(tau_i) (D_3^{t_3} (x) D_2^{t_2} (x) D_1^{t_1}) x
+ * by sum factorisation over the 1D windows with the geometry coefficients c_t computed on the fly from
+ * the analytic map (8 + 8 bytes of HBM traffic per row instead of 8 nnz/row + 16).  3D only; usable
+ * wherever a stencil is (matvec, gmres_solve, bicgstab_solve, sharded).  stencil_get_values reports
+ * NOT_SUPPORTED; stencil_info's nnz is the structural count of the equivalent stored operator. */
+int colloc_matrix_free(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
+                       fdiga_stencil** out);
 /* y = A x.  x, y: device, length N (no aliasing).  Asynchronous on the ctx stream. */
 int stencil_matvec(fdiga_stencil* A, const double* x, double* y);
 /* Number of stored values and the 1D window tables (host copies; any pointer may be NULL). */

@@ -279,13 +279,16 @@ def fd_apply_host(plan, r_host, s_host):
     return s_host
 
 
-def colloc_assemble(ctx, d, p, ne, geometry, geo_params=()):
+def colloc_assemble(ctx, d, p, ne, geometry, geo_params=(), matrix_free=False):
+    """The collocation operator A_C: stored tensor-window values (colloc_assemble) or, with
+    matrix_free=True, the sum-factorised on-the-fly operator (colloc_matrix_free, 3D)."""
     nes = [ne] * d if np.isscalar(ne) else list(ne)
     n = (C.c_int64 * d)(*nes)
     prm = np.ascontiguousarray(np.asarray(list(geo_params) + [0.0] * 4, dtype=np.float64))
     h = C.c_void_p()
-    check(ctx._lib.colloc_assemble(ctx.handle, d, int(p), n, int(geometry), _dptr(prm), C.byref(h)),
-          "colloc_assemble")
+    fn = ctx._lib.colloc_matrix_free if matrix_free else ctx._lib.colloc_assemble
+    check(fn(ctx.handle, d, int(p), n, int(geometry), _dptr(prm), C.byref(h)),
+          "colloc_matrix_free" if matrix_free else "colloc_assemble")
     return Stencil(ctx, h)
 
 

@@ -20,6 +20,8 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "geometry.cuh"
+#include "matfree.cuh"
 
 using namespace fdiga;
 
@@ -49,6 +51,14 @@ struct fdiga_stencil {
   double* halo = nullptr;         // (o - lo + hi - e) planes: lower halo, then upper halo
   std::vector<fdiga::P2PMsg> hsend, hrecv;  // halo messages (x pointers patched per call)
   std::vector<int64_t> hsend_plane;         // first plane (global) of each send
+  // matrix-free operator (NEXT-1, matfree.cu): no stored values; 1D tables and the map on the device
+  bool mf = false;
+  int mf_W = 0, mf_B[3] = {0, 0, 0};
+  double* mf_tau[3] = {nullptr, nullptr, nullptr};
+  double* mf_tab[3] = {nullptr, nullptr, nullptr};
+  double* mf_trig[3] = {nullptr, nullptr, nullptr};  // (sin, cos)(theta tau) per direction
+  int32_t* mf_box[3] = {nullptr, nullptr, nullptr};  // per tile: (first column, extent) of its x box
+  fdiga::Geo mf_geo{};
 };
 
 namespace {
@@ -160,92 +170,6 @@ void build_table(int p, int64_t ne, Table1D& T) {
   }
 }
 
-// ------------------------------------------------------------------ device geometry
-struct Geo {
-  int id;
-  double prm[4];
-};
-
-struct JH {
-  double J[3][3];     // J[c][a] = dF_c / dxi_a
-  double H[3][3][3];  // H[c][a][b] = d^2 F_c / dxi_a dxi_b
-};
-
-// Closed-form Jacobian and Hessians of the analytic maps (FDIGA_GEOM_*); unused entries are zero.
-__device__ __forceinline__ JH geometry_jh(const Geo g, const double x0, const double x1, const double x2) {
-  JH r;
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      r.J[c][a] = (c == a) ? 1.0 : 0.0;
-#pragma unroll
-      for (int b = 0; b < 3; ++b) r.H[c][a][b] = 0.0;
-    }
-  const double PI = 3.141592653589793;
-  if (g.id == FDIGA_GEOM_ANNULUS || g.id == FDIGA_GEOM_THICK_RING) {
-    const double r0 = g.prm[0], r1 = g.prm[1];
-    const double dr = r1 - r0, w = 0.5 * PI;
-    const double rad = r0 + dr * x0;
-    const double sn = sin(w * x1), cs = cos(w * x1);
-    r.J[0][0] = dr * cs;
-    r.J[0][1] = -rad * w * sn;
-    r.J[1][0] = dr * sn;
-    r.J[1][1] = rad * w * cs;
-    r.H[0][0][1] = -dr * w * sn;
-    r.H[0][1][0] = -dr * w * sn;
-    r.H[0][1][1] = -rad * w * w * cs;
-    r.H[1][0][1] = dr * w * cs;
-    r.H[1][1][0] = dr * w * cs;
-    r.H[1][1][1] = -rad * w * w * sn;
-    if (g.id == FDIGA_GEOM_THICK_RING) r.J[2][2] = g.prm[2];
-  } else if (g.id == FDIGA_GEOM_DEFORMED_CUBE) {
-    const double amp = g.prm[0];
-    const double s0 = sin(PI * x0), c0 = cos(PI * x0);
-    const double s1 = sin(PI * x1), c1 = cos(PI * x1);
-    const double s2 = sin(PI * x2), c2 = cos(PI * x2);
-    const double gr[3] = {PI * c0 * s1 * s2, PI * s0 * c1 * s2, PI * s0 * s1 * c2};
-    const double P2 = PI * PI;
-    const double hd = -P2 * s0 * s1 * s2, h01 = P2 * c0 * c1 * s2, h02 = P2 * c0 * s1 * c2, h12 = P2 * s0 * c1 * c2;
-    const double hg[3][3] = {{hd, h01, h02}, {h01, hd, h12}, {h02, h12, hd}};
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        r.J[c][a] += amp * gr[a];
-#pragma unroll
-        for (int b = 0; b < 3; ++b) r.H[c][a][b] = amp * hg[a][b];
-      }
-  }
-  return r;
-}
-
-// Inverse of the leading D x D block by cofactors.
-template <int D>
-__device__ __forceinline__ void inv_small(const double A[3][3], double B[3][3]) {
-  if (D == 2) {
-    const double det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
-    B[0][0] = A[1][1] / det;
-    B[0][1] = -A[0][1] / det;
-    B[1][0] = -A[1][0] / det;
-    B[1][1] = A[0][0] / det;
-    return;
-  }
-  const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
-  const double c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2];
-  const double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
-  const double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
-  B[0][0] = c00 / det;
-  B[1][0] = c01 / det;
-  B[2][0] = c02 / det;
-  B[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) / det;
-  B[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) / det;
-  B[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) / det;
-  B[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) / det;
-  B[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) / det;
-  B[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) / det;
-}
-
 struct AsmArgs {
   int wmax;
   int64_t n1, n2, n3, S1, S2;
@@ -269,32 +193,8 @@ __global__ void assemble_kernel(AsmArgs A) {
   const int64_t row = A.row0 + lrow;
   const int64_t i1 = row % A.n1, i2 = (row / A.n1) % A.n2, i3 = row / (A.n1 * A.n2);
   const double x0 = A.tau1[i1], x1 = A.tau2[i2], x2 = (D == 3) ? A.tau3[i3] : 0.0;
-  const JH g = geometry_jh(A.geo, x0, x1, x2);
-  double JtJ[3][3], G[3][3], Ji[3][3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      double s = 0;
-#pragma unroll
-      for (int c = 0; c < D; ++c) s += g.J[c][a] * g.J[c][b];
-      JtJ[a][b] = s;
-      G[a][b] = 0;
-      Ji[a][b] = 0;
-    }
-  inv_small<D>(JtJ, G);
-  inv_small<D>(g.J, Ji);
-  double beta[3] = {0, 0, 0};
-#pragma unroll
-  for (int c = 0; c < D; ++c) {
-    double tr = 0;  // tr(G H_c)
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) tr += G[a][b] * g.H[c][b][a];
-#pragma unroll
-    for (int a = 0; a < D; ++a) beta[a] += Ji[a][c] * tr;
-  }
+  double G[3][3], beta[3];
+  colloc_coeffs<D>(geometry_jh(A.geo, x0, x1, x2), G, beta);
   const int W = A.wmax;
   const int w1 = A.w1[i1];
   const int w2 = A.w2[i2];
@@ -617,6 +517,12 @@ int stencil_destroy(fdiga_stencil* S) {
   cudaFree(S->vals);
   cudaFree(S->voff1);
   cudaFree(S->halo);
+  for (int l = 0; l < 3; ++l) {
+    cudaFree(S->mf_tau[l]);
+    cudaFree(S->mf_tab[l]);
+    cudaFree(S->mf_trig[l]);
+    cudaFree(S->mf_box[l]);
+  }
   delete S;
   return FDIGA_OK;
 }
@@ -657,12 +563,13 @@ int stencil_create(fdiga_ctx* ctx, int d, const int64_t* n, const int32_t* const
   return FDIGA_OK;
 }
 
-int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
-                    fdiga_stencil** out) {
+static int colloc_build(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
+                        int matrix_free, fdiga_stencil** out) {
   FDIGA_CHECK(ctx && ne && out, FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_CHECK(d == 2 || d == 3, FDIGA_ERR_INVALID_ARG, "d must be 2 or 3");
   FDIGA_CHECK(p >= 1 && p <= 8, FDIGA_ERR_INVALID_ARG, "degree p = %d out of range", p);
   FDIGA_CHECK(!ctx->sharded || d == 3, FDIGA_ERR_NOT_SUPPORTED, "2D operators are not sharded (replicas only)");
+  FDIGA_CHECK(!matrix_free || d == 3, FDIGA_ERR_NOT_SUPPORTED, "the matrix-free operator is 3D only");
   const bool ok_geo = geometry_id == FDIGA_GEOM_IDENTITY || (geometry_id == FDIGA_GEOM_ANNULUS && d == 2) ||
                       ((geometry_id == FDIGA_GEOM_DEFORMED_CUBE || geometry_id == FDIGA_GEOM_THICK_RING) && d == 3);
   FDIGA_CHECK(ok_geo, FDIGA_ERR_INVALID_ARG, "geometry %d not available in %dD", geometry_id, d);
@@ -728,7 +635,51 @@ int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometr
     A.voff1 = S->voff1;
     A.wm1 = S->wm1;
   }
-  if (s == FDIGA_OK) {
+  if (s == FDIGA_OK && matrix_free) {
+    // keep the 1D tables and the map; the 8^3 tiles' x boxes bound the shared memory of the kernel
+    S->mf = true;
+    S->mf_W = p + 1;
+    S->mf_geo = A.geo;
+    for (int l = 0; l < 3; ++l) {
+      S->mf_tau[l] = const_cast<double*>(l == 0 ? A.tau1 : l == 1 ? A.tau2 : A.tau3);
+      S->mf_tab[l] = const_cast<double*>(l == 0 ? A.tab1 : l == 1 ? A.tab2 : A.tab3);
+      tmp.erase(std::remove(tmp.begin(), tmp.end(), (void*)S->mf_tau[l]), tmp.end());
+      tmp.erase(std::remove(tmp.begin(), tmp.end(), (void*)S->mf_tab[l]), tmp.end());
+      const int64_t first = (l == 2) ? S->o : 0, last = (l == 2) ? S->e : n[l];
+      int bmax = 1;
+      std::vector<int32_t> box;
+      for (int64_t a0 = first; a0 < last; a0 += MF_T) {
+        int hi0 = 0;
+        for (int64_t i = a0; i < std::min<int64_t>(a0 + MF_T, last); ++i) {
+          hi0 = std::max(hi0, S->hstart[l][i] + S->hwidth[l][i]);
+          if (i > a0 && S->hstart[l][i] < S->hstart[l][i - 1]) s = FDIGA_ERR_NOT_SUPPORTED;
+        }
+        bmax = std::max(bmax, hi0 - S->hstart[l][a0]);
+        box.push_back(S->hstart[l][a0]);
+        box.push_back(hi0 - S->hstart[l][a0]);
+      }
+      S->mf_B[l] = bmax;
+      if (box.empty()) box.assign(2, 0);
+      if (cudaMalloc(&S->mf_box[l], box.size() * 4) != cudaSuccess ||
+          cudaMemcpy(S->mf_box[l], box.data(), box.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+        s = FDIGA_ERR_CUDA;
+      // trigonometric factors of the map at the Greville points (setup, host libm)
+      std::vector<double> trig(2 * n[l]);
+      const double th = geo_theta(geometry_id);
+      for (int64_t i = 0; i < n[l]; ++i) {
+        trig[2 * i] = std::sin(th * T[l].tau[i]);
+        trig[2 * i + 1] = std::cos(th * T[l].tau[i]);
+      }
+      if (cudaMalloc(&S->mf_trig[l], trig.size() * 8) != cudaSuccess ||
+          cudaMemcpy(S->mf_trig[l], trig.data(), trig.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+        s = FDIGA_ERR_CUDA;
+    }
+    if (s == FDIGA_OK && matfree_smem_bytes(S->mf_B[0], S->mf_B[1], S->mf_B[2]) > 200 * 1024) {
+      set_error("matrix-free operator: tile box %dx%dx%d exceeds shared memory", S->mf_B[0], S->mf_B[1], S->mf_B[2]);
+      s = FDIGA_ERR_NOT_SUPPORTED;
+    }
+  }
+  if (s == FDIGA_OK && !matrix_free) {
     cudaError_t e = cudaMalloc(&S->vals, (S->nnz + 2) * sizeof(double));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e == cudaSuccess) e = cudaMemsetAsync(S->vals, 0, (S->nnz + 2) * sizeof(double), ctx->stream);
@@ -760,6 +711,16 @@ int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometr
   return FDIGA_OK;
 }
 
+int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
+                    fdiga_stencil** out) {
+  return colloc_build(ctx, d, p, ne, geometry_id, geo_params, 0, out);
+}
+
+int colloc_matrix_free(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
+                       fdiga_stencil** out) {
+  return colloc_build(ctx, d, p, ne, geometry_id, geo_params, 1, out);
+}
+
 int stencil_matvec(fdiga_stencil* S, const double* x, double* y) { return fdiga::stencil_matvec_ex(S, x, y, nullptr); }
 
 }  // extern "C"
@@ -778,6 +739,51 @@ int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* s
     FDIGA_TRY(comm_exchange(ctx, snd, S->hrecv));
   }
   if (S->Nloc == 0) return FDIGA_OK;
+  if (S->mf) {  // matrix-free sum-factorised operator (matfree.cu)
+    MfArgs M{};
+    M.n1 = S->n[0];
+    M.n2 = S->n[1];
+    M.n3 = S->n[2];
+    M.o = S->o;
+    M.e = S->e;
+    M.lo = S->lo;
+    M.t1 = (S->n[0] + MF_T - 1) / MF_T;
+    M.t2 = (S->n[1] + MF_T - 1) / MF_T;
+    M.t3 = (S->e - S->o + MF_T - 1) / MF_T;
+    M.x = x;
+    const int64_t plane = S->n[0] * S->n[1];
+    M.halo_lo = S->halo;
+    M.halo_hi = S->halo ? S->halo + (S->o - S->lo) * plane : nullptr;
+    M.y = y;
+    M.st1 = S->start[0];
+    M.st2 = S->start[1];
+    M.st3 = S->start[2];
+    M.w1 = S->width[0];
+    M.w2 = S->width[1];
+    M.w3 = S->width[2];
+    M.tab1 = S->mf_tab[0];
+    M.tab2 = S->mf_tab[1];
+    M.tab3 = S->mf_tab[2];
+    M.tau1 = S->mf_tau[0];
+    M.tau2 = S->mf_tau[1];
+    M.tau3 = S->mf_tau[2];
+    M.trig1 = S->mf_trig[0];
+    M.trig2 = S->mf_trig[1];
+    M.trig3 = S->mf_trig[2];
+    M.box1 = S->mf_box[0];
+    M.box2 = S->mf_box[1];
+    M.box3 = S->mf_box[2];
+    M.W = S->mf_W;
+    M.B1 = S->mf_B[0];
+    M.B2 = S->mf_B[1];
+    M.B3 = S->mf_B[2];
+    M.geo = S->mf_geo;
+    M.skip = skip;
+    M.sharded = sh ? 1 : 0;
+    FDIGA_TRY(matfree_launch(M, ctx->stream));
+    count_launch(ctx);
+    return FDIGA_OK;
+  }
   MvArgs A = make_mv_args(S, x, y);
   A.skip = skip;
   const unsigned grid = (unsigned)((S->Nloc + 255) / 256);
@@ -843,6 +849,7 @@ int stencil_info(const fdiga_stencil* S, int64_t* nnz, int64_t* n_out, int32_t* 
 
 int stencil_get_values(const fdiga_stencil* S, double* values_host) {
   FDIGA_CHECK(S && values_host, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_CHECK(!S->mf, FDIGA_ERR_NOT_SUPPORTED, "a matrix-free operator stores no values");
   FDIGA_TRY(bind(S->ctx));
   double* canon = nullptr;
   FDIGA_CUDA(cudaMalloc(&canon, S->nnz * sizeof(double)));

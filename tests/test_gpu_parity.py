@@ -403,3 +403,45 @@ def test_bicgstab_unpreconditioned_and_status(ctx):
     x2 = torch.empty_like(b2)
     rep = fd.bicgstab_solve(ctx, A2, None, b2, x2, max_iters=3, raise_on_failure=False)
     assert rep["status"] == -8 and not rep["converged"] and rep["iters"] == 3.0
+
+
+# ----------------------------------------------------------------------------- matrix-free operator (NEXT-1)
+
+@pytest.mark.parametrize("cfg,ne", [(3, None), (5, None), (3, 1), (3, 3), (5, 2), (5, 7), (5, 13), (3, 17)])
+def test_matrix_free_matvec_matches_oracle(ctx, cfg, ne):
+    c, disc = _disc(cfg, ne)
+    A = fd.colloc_assemble(ctx, c.d, c.p, ne or c.ne, c.geometry, c.geo_params, matrix_free=True)
+    assert A.N == disc.N
+    x = np.random.default_rng(cfg * 11 + (ne or 0)).standard_normal(disc.N)
+    y = torch.empty(disc.N, dtype=torch.float64, device=DEV)
+    fd.stencil_matvec(A, gpu(x), y)
+    assert rel(host(y), disc.matvec(x)) <= 1e-12
+    with pytest.raises(fd.FdigaError):
+        A.values()
+
+
+def test_matrix_free_identity_map_is_kronecker(ctx):
+    # identity map: A_C = K (x) M (x) M + M (x) K (x) M + M (x) M (x) K (eq:colloc3D)
+    _, M, K, _ = splines.colloc_1d(9, 4)
+    n = M.shape[0]
+    A = fd.colloc_assemble(ctx, 3, 4, 9, 0, matrix_free=True)
+    P = assembly.kron_preconditioner_sparse([M] * 3, [K] * 3)
+    x = np.random.default_rng(4).standard_normal(n ** 3)
+    y = torch.empty(n ** 3, dtype=torch.float64, device=DEV)
+    fd.stencil_matvec(A, gpu(x), y)
+    assert rel(host(y), P @ x) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_matrix_free_gmres_and_bicgstab(ctx, cfg):
+    c = get_config(cfg)
+    A = fd.colloc_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params, matrix_free=True)
+    _, M, K, _ = splines.colloc_1d(c.ne, c.p)
+    P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
+    b = gpu(rhs(cfg, A.N))
+    x = torch.empty_like(b)
+    ref = GOLD["configs"][str(cfg)]
+    rep = fd.gmres_solve(ctx, A, P, b, x)
+    assert rep["converged"] and abs(rep["iters"] - ref["iters"]) <= 1 and rep["rel_res_true"] <= 1e-8
+    rep = fd.bicgstab_solve(ctx, A, P, b, x)
+    assert rep["converged"] and abs(rep["iters"] - ref["bicgstab_iters"]) <= 1.0

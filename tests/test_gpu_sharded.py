@@ -264,3 +264,24 @@ def test_nccl_one_rank_bicgstab_captured(nccl_ctx):
     assert rep["converged"] and abs(rep["iters"] - GOLD["configs"]["3"]["bicgstab_iters"]) <= 1.0
     P.close()
     A.close()
+
+
+@pytest.mark.parametrize("cfg,ne,nranks", [(5, 7, 5), (3, 20, 3), (5, 16, 4)])
+def test_sharded_matrix_free_matvec(cfg, ne, nranks):
+    c = get_config(cfg)
+    disc = assembly.Discretisation(c.d, c.p, ne, c.geometry, c.geo_params)
+    x = np.random.default_rng(ne + 7 * nranks).standard_normal(disc.N)
+    n = disc.n
+
+    def work(ctx, rank):
+        A = fd.colloc_assemble(ctx, 3, c.p, ne, c.geometry, c.geo_params, matrix_free=True)
+        lo, hi = slab_rows(n, nranks, rank, n * n)
+        y = torch.empty(hi - lo, dtype=torch.float64, device=DEV)
+        fd.stencil_matvec(A, torch.from_numpy(x[lo:hi].copy()).to(DEV), y)
+        torch.cuda.current_stream().synchronize()
+        out = y.cpu().numpy()
+        A.close()
+        return out
+
+    y = np.concatenate(run_ranks(nranks, work))
+    assert rel(y, disc.matvec(x)) <= 1e-12
