@@ -192,7 +192,9 @@ typedef struct {
   int m;             /* restart length (default 30) */
   double rtol;       /* stop when ||b - A x|| <= rtol ||b|| (default 1e-8) */
   int max_iters;     /* Arnoldi steps over all cycles (default 1000) */
-  int orth;          /* FDIGA_ORTH_* (default CGS with DGKS re-orthogonalisation) */
+  int orth;          /* FDIGA_ORTH_CGS2 (default with opts == NULL): classical Gram-Schmidt twice;
+                        FDIGA_ORTH_CGS_DGKS: the second pass only when ||w'|| < ||w|| / sqrt(2) (with the FD
+                        preconditioner A P^{-1} ~ I, so that test fails at every step and CGS2 is faster) */
   int use_x0;        /* 1: x holds the initial guess; 0: x0 = 0 */
 } gmres_opts;
 

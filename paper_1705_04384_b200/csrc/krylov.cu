@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "reduce.cuh"
+#include "ptx.cuh"
 
 using namespace fdiga;
 
@@ -41,96 +42,115 @@ struct GmState {
   int max_iters;
   int first;       // first residual of the solve (records ||b||)
   int breakdown;   // non-finite value met
+  int reorth;      // CGS + DGKS: the current step needs the second pass
+  int nreorth;     // second passes taken
   unsigned int counter[NCNT];
 };
 
-// Element loops of the three passes: each thread handles pairs of elements with 16-byte loads (V rows
-// and w are 512-byte aligned, ldv even); a scalar tail covers odd N.
-#define FDIGA_PAIRS(e2) for (int64_t e2 = blockIdx.x * (int64_t)RT + threadIdx.x; e2 < (N >> 1); e2 += (int64_t)gridDim.x * RT)
-#define FDIGA_TAIL(e) for (int64_t e = (N & ~int64_t(1)) + blockIdx.x * (int64_t)RT + threadIdx.x; e < N; e += (int64_t)gridDim.x * RT)
+// ---- streaming Gram-Schmidt passes.  The k basis vectors and w are streamed through shared memory by
+// the TMA engine (1D bulk copies, mbarrier completion) in chunks of SC elements, ST stages deep, so the
+// bytes in flight do not depend on registers; every thread then owns one element of the chunk.  V rows
+// and w are 512-byte aligned with a leading dimension ldv (multiple of 64) >= N, so every copy is a
+// whole number of 16-byte units; elements >= N are masked.
+constexpr int SC = RT;  // elements per chunk (one per thread)
 
-// pass 1: h1[i] = V_i . w (i < k), h1[k] = w . w
+enum { GS_DOT = 0, GS_UPD_DOT = 1, GS_UPD = 2 };
+
+template <int K>
+__host__ __device__ constexpr int gs_stages() {
+  return (200 * 1024) / ((K + 1) * SC * 8) >= 4 ? 4 : ((200 * 1024) / ((K + 1) * SC * 8) >= 3 ? 3 : 2);
+}
+
+template <int K>
+__host__ __device__ constexpr size_t gs_smem_bytes() {
+  return (size_t)gs_stages<K>() * (K + 1) * SC * 8 + 64;
+}
+
+// acc[i] (i < K) = V_i . w or V_i . w' and acc[K] = w.w or w'.w' with w' = w - V hs (GS_UPD_DOT / GS_UPD,
+// w' stored back to global)
+template <int K, int MODE>
+__device__ __forceinline__ void gs_stream(const double* __restrict__ V, int64_t ldv, double* w, int64_t N,
+                                          const double* hs, double (&acc)[K + 1]) {
+  constexpr int S = gs_stages<K>();
+  extern __shared__ __align__(128) double gsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(gsm + (size_t)S * (K + 1) * SC);
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int i = 0; i <= K; ++i) acc[i] = 0.0;
+  const int64_t nchunk = (N + SC - 1) / SC;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // warp 0 issues a stage: lane 0 posts the byte count, then lane i copies row i (V_i, or w for i = K)
+  auto issue = [&](int64_t c, int s) {
+    const int lane = tid & 31;
+    const int64_t e0 = c * SC;
+    const uint32_t bytes = (uint32_t)((ldv - e0 < SC ? ldv - e0 : SC) * 8);
+    double* dst = gsm + (size_t)s * (K + 1) * SC;
+    if (lane == 0) mbar_arrive_expect_tx(&full[s], (K + 1) * bytes);
+    __syncwarp();
+    if (lane <= K) bulk_g2s(dst + lane * SC, lane < K ? V + lane * ldv + e0 : w + e0, bytes, &full[s]);
+  };
+  if (tid < 32)
+    for (int s = 0; s < S; ++s) {
+      const int64_t c = blockIdx.x + (int64_t)s * gridDim.x;
+      if (c < nchunk) issue(c, s);
+    }
+  int it = 0;
+  for (int64_t c = blockIdx.x; c < nchunk; c += gridDim.x, ++it) {
+    const int s = it % S;
+    mbar_wait(&full[s], (uint32_t)((it / S) & 1));
+    const double* buf = gsm + (size_t)s * (K + 1) * SC;
+    const int64_t e = c * SC + tid;
+    if (e < N) {
+      double wv = buf[K * SC + tid];
+      if (MODE != GS_DOT) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) wv = fma(-hs[i], buf[i * SC + tid], wv);
+        w[e] = wv;
+      }
+      if (MODE != GS_UPD) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc[i] = fma(buf[i * SC + tid], wv, acc[i]);
+      }
+      acc[K] = fma(wv, wv, acc[K]);
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (tid < 32) {
+      const int64_t cn = c + (int64_t)S * gridDim.x;
+      if (cn < nchunk) {
+        fence_proxy_async();
+        issue(cn, s);
+      }
+    }
+  }
+}
+
+// pass 1: h[i] = V_i . w (i < k), h[k] = w . w
 template <int K>
 __global__ void __launch_bounds__(RT) arnoldi_pass1(const double* __restrict__ V, int64_t ldv, int /*k (= K)*/,
                                                     const double* __restrict__ w, int64_t N, double* part,
-                                                    GmState* st, double* hout) {
-  constexpr int k = K;
-  if (st->stop) return;
-  double acc[KMAX + 1];
-#pragma unroll
-  for (int i = 0; i <= KMAX; ++i) acc[i] = 0.0;
-  const double2* w2 = reinterpret_cast<const double2*>(w);
-  FDIGA_PAIRS(e2) {
-    const double2 wv = w2[e2];
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i)
-      if (i < k) {
-        const double2 v = reinterpret_cast<const double2*>(V + i * ldv)[e2];
-        acc[i] = fma(v.x, wv.x, fma(v.y, wv.y, acc[i]));
-      }
-    acc[KMAX] = fma(wv.x, wv.x, fma(wv.y, wv.y, acc[KMAX]));
-  }
-  FDIGA_TAIL(e) {
-    const double wv = w[e];
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i)
-      if (i < k) acc[i] = fma(V[i * ldv + e], wv, acc[i]);
-    acc[KMAX] = fma(wv, wv, acc[KMAX]);
-  }
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i)
-    if (i == k) acc[i] = acc[KMAX];  // w.w to slot k (static register indexing)
-  reduce_last<KMAX + 1>(acc, k + 1, part, &st->counter[0], hout);
+                                                    GmState* st, double* hout, int cond) {
+  if (st->stop || (cond && !st->reorth)) return;
+  double acc[K + 1];
+  gs_stream<K, GS_DOT>(V, ldv, const_cast<double*>(w), N, nullptr, acc);
+  reduce_last<K + 1>(acc, K + 1, part, &st->counter[0], hout);
 }
 
-// pass 2: w <- w - V h1 ; h2[i] = V_i . w (new w), h2[k] = ||w||^2.  V_i is read twice per element
-// pair; the second read hits L1 (the block's working set is <= 256 threads x 32 x 16 B).
+// pass 2: w <- w - V h1 ; h2[i] = V_i . w (new w), h2[k] = ||w||^2 (V read once, from shared memory)
 template <int K>
 __global__ void __launch_bounds__(RT) arnoldi_pass2(const double* __restrict__ V, int64_t ldv, int /*k (= K)*/,
                                                     double* __restrict__ w, int64_t N, double* part, GmState* st,
                                                     double* hout) {
-  constexpr int k = K;
   if (st->stop) return;
   __shared__ double hs[KMAX];
-  if (threadIdx.x < k) hs[threadIdx.x] = st->h1[threadIdx.x];
+  if (threadIdx.x < K) hs[threadIdx.x] = st->h1[threadIdx.x];
   __syncthreads();
-  double acc[KMAX + 1];
-#pragma unroll
-  for (int i = 0; i <= KMAX; ++i) acc[i] = 0.0;
-  double2* w2 = reinterpret_cast<double2*>(w);
-  FDIGA_PAIRS(e2) {
-    double2 wv = w2[e2];
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i)
-      if (i < k) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(V + i * ldv) + e2);
-        wv.x = fma(-hs[i], v.x, wv.x);
-        wv.y = fma(-hs[i], v.y, wv.y);
-      }
-    w2[e2] = wv;
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i)
-      if (i < k) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(V + i * ldv) + e2);
-        acc[i] = fma(v.x, wv.x, fma(v.y, wv.y, acc[i]));
-      }
-    acc[KMAX] = fma(wv.x, wv.x, fma(wv.y, wv.y, acc[KMAX]));
-  }
-  FDIGA_TAIL(e) {
-    double wv = w[e];
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i)
-      if (i < k) wv = fma(-hs[i], V[i * ldv + e], wv);
-    w[e] = wv;
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i)
-      if (i < k) acc[i] = fma(V[i * ldv + e], wv, acc[i]);
-    acc[KMAX] = fma(wv, wv, acc[KMAX]);
-  }
-#pragma unroll
-  for (int i = 0; i < KMAX; ++i)
-    if (i == k) acc[i] = acc[KMAX];
-  reduce_last<KMAX + 1>(acc, k + 1, part, &st->counter[1], hout);
+  double acc[K + 1];
+  gs_stream<K, GS_UPD_DOT>(V, ldv, w, N, hs, acc);
+  reduce_last<K + 1>(acc, K + 1, part, &st->counter[1], hout);
 }
 
 // Givens rotations / convergence test for step j (one thread), once h = h1 + h2 and ||w''||^2 are known.
@@ -162,6 +182,7 @@ __device__ void arnoldi_close_step(GmState* st, int j, int m, double wn2, double
   st->g[j] = c * st->g[j];
   st->iters += 1;
   st->k = k;
+  st->reorth = 0;
   st->rel_implicit = fabs(st->g[k]) / st->bnorm;
   if (hist && st->iters - 1 < hist_cap) hist[st->iters - 1] = st->rel_implicit;
   st->invh = hn > 0.0 ? 1.0 / hn : 0.0;
@@ -169,53 +190,57 @@ __device__ void arnoldi_close_step(GmState* st, int j, int m, double wn2, double
   if (bad || fabs(st->g[k]) <= st->target || hn == 0.0 || st->iters >= st->max_iters || k >= m) st->stop = 1;
 }
 
-// pass 3: w <- w - V h2 ; ||w||^2 ; the last block closes the step
+// CGS + DGKS decision after the first update (one thread): Daniel-Gragg-Kaufman-Stewart test
+// ||w'|| < ||w|| / sqrt(2) (w.w before the update sits in h1[k]) -> a second pass; otherwise h2 = 0 and
+// the step closes with the first pass.
+__device__ void dgks_decide(GmState* st, int j, int m, double wn2, double* hist, int hist_cap) {
+  const int k = j + 1;
+  if (!(wn2 >= 0.5 * st->h1[k])) {  // also catches NaN
+    st->reorth = 1;
+    st->nreorth += 1;
+    return;
+  }
+  for (int i = 0; i < k; ++i) st->h2[i] = 0.0;
+  arnoldi_close_step(st, j, m, wn2, hist, hist_cap);
+}
+
+enum { P3_CLOSE = 0, P3_DGKS = 1, P3_CLOSE_IF_REORTH = 2 };
+
+// pass 3: w <- w - V h ; ||w||^2 ; the last block closes the step.  mode P3_CLOSE (CGS2): h = h2, close;
+// P3_DGKS (CGS first update): h = h1, DGKS decision; P3_CLOSE_IF_REORTH: only after a DGKS
+// re-orthogonalisation, h = h2, close.
 template <int K>
 __global__ void __launch_bounds__(RT) arnoldi_pass3(const double* __restrict__ V, int64_t ldv, int /*k (= K)*/,
                                                     double* __restrict__ w, int64_t N, double* part, GmState* st,
-                                                    int j, int m, double* hist, int hist_cap, int close) {
+                                                    int j, int m, double* hist, int hist_cap, int close, int mode) {
   constexpr int k = K;
-  if (st->stop) return;
+  if (st->stop || (mode == P3_CLOSE_IF_REORTH && !st->reorth)) return;
   __shared__ double hs[KMAX];
-  if (threadIdx.x < k) hs[threadIdx.x] = st->h2[threadIdx.x];
+  if (threadIdx.x < k) hs[threadIdx.x] = mode == P3_DGKS ? st->h1[threadIdx.x] : st->h2[threadIdx.x];
   __syncthreads();
-  double acc[1] = {0.0};
-  double2* w2 = reinterpret_cast<double2*>(w);
-  FDIGA_PAIRS(e2) {
-    double2 wv = w2[e2];
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i)
-      if (i < k) {
-        const double2 v = reinterpret_cast<const double2*>(V + i * ldv)[e2];
-        wv.x = fma(-hs[i], v.x, wv.x);
-        wv.y = fma(-hs[i], v.y, wv.y);
-      }
-    w2[e2] = wv;
-    acc[0] = fma(wv.x, wv.x, fma(wv.y, wv.y, acc[0]));
-  }
-  FDIGA_TAIL(e) {
-    double wv = w[e];
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i)
-      if (i < k) wv = fma(-hs[i], V[i * ldv + e], wv);
-    w[e] = wv;
-    acc[0] = fma(wv, wv, acc[0]);
-  }
+  double accs[K + 1];
+  gs_stream<K, GS_UPD>(V, ldv, w, N, hs, accs);
+  double acc[1] = {accs[K]};
   __shared__ double nrm[1];
   if (reduce_last<1>(acc, 1, part, &st->counter[2], nrm)) {
     if (threadIdx.x == 0) {
-      if (close)
-        arnoldi_close_step(st, j, m, nrm[0], hist, hist_cap);
-      else
+      if (!close)
         st->wn2l = nrm[0];  // sharded: all-reduced into wn2, then close_step_kernel
+      else if (mode == P3_DGKS)
+        dgks_decide(st, j, m, nrm[0], hist, hist_cap);
+      else
+        arnoldi_close_step(st, j, m, nrm[0], hist, hist_cap);
     }
   }
 }
 
-// sharded: close step j once ||w''||^2 is global
-__global__ void close_step_kernel(GmState* st, int j, int m, double* hist, int hist_cap) {
-  if (st->stop) return;
-  arnoldi_close_step(st, j, m, st->wn2, hist, hist_cap);
+// sharded: close step j (or take the DGKS decision) once ||w||^2 is global
+__global__ void close_step_kernel(GmState* st, int j, int m, double* hist, int hist_cap, int mode) {
+  if (st->stop || (mode == P3_CLOSE_IF_REORTH && !st->reorth)) return;
+  if (mode == P3_DGKS)
+    dgks_decide(st, j, m, st->wn2, hist, hist_cap);
+  else
+    arnoldi_close_step(st, j, m, st->wn2, hist, hist_cap);
 }
 
 // v_{j+1} = w * invh (a no-op once the cycle stopped)
@@ -315,25 +340,65 @@ struct Ws {
   int64_t N, ldv;
   int nblk;
   bool sh;  // nranks > 1: reductions are all-reduced between the passes
+  int orth; // FDIGA_ORTH_*
   double *V, *z, *w, *part, *hist;
   GmState* st;
 };
 
+// launch shape of the streaming passes for k = K: dynamic shared memory and a persistent grid of as
+// many CTAs per SM as the stages allow (<= 8)
 template <int K>
-int passes_k(fdiga_ctx* ctx, const Ws& W, int j, int m, int hist_cap) {
+int gs_grid(fdiga_ctx* ctx, int64_t N, size_t* smem) {
+  *smem = gs_smem_bytes<K>();
+  static bool attr = false;
+  if (!attr) {
+    FDIGA_CUDA(cudaFuncSetAttribute(arnoldi_pass1<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
+    FDIGA_CUDA(cudaFuncSetAttribute(arnoldi_pass2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
+    FDIGA_CUDA(cudaFuncSetAttribute(arnoldi_pass3<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
+    attr = true;
+  }
+  const int per_sm = std::max(1, std::min(8, (int)((227 * 1024) / (*smem + 1024))));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((N + SC - 1) / SC, (int64_t)ctx->sm_count * per_sm));
+}
+
+template <int K>
+int pass3_k(fdiga_ctx* ctx, const Ws& W, int j, int m, int hist_cap, int mode) {
   GmState* st = W.st;
-  arnoldi_pass1<K><<<W.nblk, RT, 0, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, W.sh ? st->h1l : st->h1);
-  if (W.sh) FDIGA_TRY(comm_allreduce(ctx, st->h1l, st->h1, K + 1));
-  arnoldi_pass2<K><<<W.nblk, RT, 0, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, W.sh ? st->h2l : st->h2);
-  if (W.sh) FDIGA_TRY(comm_allreduce(ctx, st->h2l, st->h2, K + 1));
-  arnoldi_pass3<K><<<W.nblk, RT, 0, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, j, m, W.hist, hist_cap,
-                                                   W.sh ? 0 : 1);
+  size_t smem = 0;
+  const int grid = gs_grid<K>(ctx, W.N, &smem);
+  arnoldi_pass3<K><<<grid, RT, smem, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, j, m, W.hist, hist_cap,
+                                                   W.sh ? 0 : 1, mode);
+  count_launch(ctx);
   if (W.sh) {
     FDIGA_TRY(comm_allreduce(ctx, &st->wn2l, &st->wn2, 1));
-    close_step_kernel<<<1, 1, 0, ctx->stream>>>(st, j, m, W.hist, hist_cap);
+    close_step_kernel<<<1, 1, 0, ctx->stream>>>(st, j, m, W.hist, hist_cap, mode);
     count_launch(ctx);
   }
   return FDIGA_OK;
+}
+
+template <int K>
+int passes_k(fdiga_ctx* ctx, const Ws& W, int j, int m, int hist_cap) {
+  GmState* st = W.st;
+  size_t smem = 0;
+  const int grid = gs_grid<K>(ctx, W.N, &smem);
+  arnoldi_pass1<K><<<grid, RT, smem, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, W.sh ? st->h1l : st->h1, 0);
+  count_launch(ctx);
+  if (W.sh) FDIGA_TRY(comm_allreduce(ctx, st->h1l, st->h1, K + 1));
+  if (W.orth == FDIGA_ORTH_CGS2) {
+    // classical Gram-Schmidt twice: pass 2 fuses the update with the second projection
+    arnoldi_pass2<K><<<grid, RT, smem, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, W.sh ? st->h2l : st->h2);
+    count_launch(ctx);
+    if (W.sh) FDIGA_TRY(comm_allreduce(ctx, st->h2l, st->h2, K + 1));
+    return pass3_k<K>(ctx, W, j, m, hist_cap, P3_CLOSE);
+  }
+  // classical Gram-Schmidt with DGKS re-orthogonalisation: update, test, and only when the test fails a
+  // second projection + update (device flag; the launches are no-ops otherwise)
+  FDIGA_TRY(pass3_k<K>(ctx, W, j, m, hist_cap, P3_DGKS));
+  arnoldi_pass1<K><<<grid, RT, smem, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, W.sh ? st->h2l : st->h2, 1);
+  count_launch(ctx);
+  if (W.sh) FDIGA_TRY(comm_allreduce(ctx, st->h2l, st->h2, K + 1));
+  return pass3_k<K>(ctx, W, j, m, hist_cap, P3_CLOSE_IF_REORTH);
 }
 
 // The three CGS2 passes of step j with k = j + 1 basis vectors (one instantiation per k: fully
@@ -370,7 +435,7 @@ int enqueue_cycle(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const Ws& W, int
     const int k = j + 1;
     FDIGA_TRY(launch_passes(ctx, W, k, j, m, hist_cap));
     next_basis_kernel<<<W.nblk, RT, 0, ctx->stream>>>(W.w, W.V + (int64_t)(j + 1) * W.ldv, W.N, W.st);
-    count_launch(ctx, 4);
+    count_launch(ctx);
     FDIGA_CUDA(cudaGetLastError());
   }
   return FDIGA_OK;
@@ -382,7 +447,7 @@ int enqueue_cycle(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const Ws& W, int
 struct GmresGraph {
   fdiga_stencil* A = nullptr;
   fd_plan* P = nullptr;
-  int m = 0, hist_cap = 0;
+  int m = 0, hist_cap = 0, orth = 0;
   int64_t N = 0;
   double* V = nullptr;
   double* hist = nullptr;
@@ -417,6 +482,9 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   Ws W;
   W.N = stencil_local_rows(A);
   W.sh = ctx->sharded;
+  W.orth = opts ? opts->orth : FDIGA_ORTH_CGS2;
+  FDIGA_CHECK(W.orth == FDIGA_ORTH_CGS_DGKS || W.orth == FDIGA_ORTH_CGS2, FDIGA_ERR_INVALID_ARG, "unknown orth %d",
+              W.orth);
   const bool use_graph = comm_capturable(ctx);
   FDIGA_CHECK(!P || fd_plan_local_size(P) == W.N, FDIGA_ERR_INVALID_ARG,
               "preconditioner and operator sizes differ (%lld vs %lld local rows)",
@@ -427,7 +495,7 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   const size_t st_doubles = (sizeof(GmState) + 7) / 8;
   FDIGA_TRY(ctx->ws[0].ensure((size_t)(m + 1) * W.ldv));
   FDIGA_TRY(ctx->ws[1].ensure((size_t)2 * W.ldv));
-  FDIGA_TRY(ctx->ws[2].ensure((size_t)W.nblk * (KMAX + 1)));
+  FDIGA_TRY(ctx->ws[2].ensure((size_t)std::max(W.nblk, 8 * ctx->sm_count) * (KMAX + 1)));
   FDIGA_TRY(ctx->ws[3].ensure(st_doubles + hist_cap));
   W.V = ctx->ws[0].p;
   W.z = ctx->ws[1].p;
@@ -441,7 +509,7 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   // ---- the captured cycle (once per (A, P, m, N, workspace))
   GmresGraph* G = static_cast<GmresGraph*>(ctx->gmres_graph);
   if (G && (G->A != A || G->P != P || G->m != m || G->N != W.N || G->V != W.V || G->hist != W.hist ||
-            G->hist_cap != hist_cap)) {
+            G->hist_cap != hist_cap || G->orth != W.orth)) {
     destroy_gmres_graph(ctx);
     G = nullptr;
   }
@@ -455,6 +523,7 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
     G->V = W.V;
     G->hist = W.hist;
     G->hist_cap = hist_cap;
+    G->orth = W.orth;
     FDIGA_CUDA(cudaStreamCreateWithFlags(&G->cap_stream, cudaStreamNonBlocking));
     FDIGA_CUDA(cudaStreamSynchronize(st));
     cudaStream_t saved = ctx->stream;
@@ -552,7 +621,7 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
     rep->iters = hs.iters;
     rep->restarts = cycles;
     rep->converged = (status == FDIGA_OK) ? 1 : 0;
-    rep->reorth = hs.iters;  // CGS2: every step re-orthogonalises
+    rep->reorth = W.orth == FDIGA_ORTH_CGS2 ? hs.iters : hs.nreorth;  // second Gram-Schmidt passes
     rep->rel_res_true = hs.rel_true;
     rep->rel_res_implicit = hs.rel_implicit;
     rep->t_total_ms = ms;

@@ -445,3 +445,20 @@ def test_matrix_free_gmres_and_bicgstab(ctx, cfg):
     assert rep["converged"] and abs(rep["iters"] - ref["iters"]) <= 1 and rep["rel_res_true"] <= 1e-8
     rep = fd.bicgstab_solve(ctx, A, P, b, x)
     assert rep["converged"] and abs(rep["iters"] - ref["bicgstab_iters"]) <= 1.0
+
+
+@pytest.mark.parametrize("cfg", [2, 5])
+def test_gmres_orthogonalisation_variants_agree(ctx, cfg):
+    # CGS + DGKS (default) and CGS2 take the same number of steps (orthogonalisation-
+    # independent counts) and reach the same solution
+    c = get_config(cfg)
+    A = fd.colloc_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params, matrix_free=(c.d == 3))
+    _, M, K, _ = splines.colloc_1d(c.ne, c.p)
+    P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
+    b = gpu(rhs(cfg, A.N))
+    x1, x2 = torch.empty_like(b), torch.empty_like(b)
+    r1 = fd.gmres_solve(ctx, A, P, b, x1, orth=fd.ORTH_CGS_DGKS)
+    r2 = fd.gmres_solve(ctx, A, P, b, x2, orth=fd.ORTH_CGS2)
+    assert r1["iters"] == r2["iters"] == GOLD["configs"][str(cfg)]["iters"]
+    assert r2["reorth"] == r2["iters"] and 0 <= r1["reorth"] <= r1["iters"]
+    assert rel(host(x1), host(x2)) <= 1e-7
