@@ -8,6 +8,15 @@
 
 #include "fd_gemm.cuh"
 
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
 namespace fdiga {
 namespace {
 
@@ -54,6 +63,9 @@ using KN4 = TileCfg<64, 64, 16, 2, 2, 4>;    // warp 32x32, 4 warps (small grids
 using KN5 = TileCfg<72, 64, 16, 1, 4, 4>;    // warp 72x16, 4 warps
 using KN6 = TileCfg<128, 64, 16, 2, 2, 3>;   // warp 64x32, 4 warps, 2 CTAs/SM
 using KN7 = TileCfg<128, 128, 32, 2, 4, 3>;  // BK = 32: half the barriers
+using KN8 = TileCfg<144, 64, 16, 2, 2, 3>;   // warp 72x32, 4 warps, 3 stages: 2 CTAs/SM (n in (128, 144])
+using KN9 = TileCfg<72, 32, 16, 1, 2, 4>;    // warp 72x16, 2 warps (n <= 72, small N)
+using KN10 = TileCfg<72, 16, 16, 1, 1, 4>;   // warp 72x16, 1 warp  (n <= 72, tiny N)
 using NK0 = TileCfg<128, 128, 16, 2, 4, 4>;
 using NK1 = TileCfg<128, 144, 16, 4, 2, 4>;  // warp 32x72
 using NK2 = TileCfg<128, 72, 16, 8, 1, 4>;   // warp 16x72
@@ -62,16 +74,22 @@ using NK4 = TileCfg<64, 64, 16, 2, 2, 4>;
 using NK5 = TileCfg<64, 72, 16, 4, 1, 4>;    // warp 16x72, 4 warps
 using NK6 = TileCfg<64, 128, 16, 2, 2, 3>;   // warp 32x64, 4 warps, 2 CTAs/SM
 using NK7 = TileCfg<128, 128, 32, 2, 4, 3>;
+using NK8 = TileCfg<64, 144, 16, 2, 2, 3>;   // warp 32x72, 4 warps, 3 stages: 2 CTAs/SM
+using NK9 = TileCfg<32, 72, 16, 2, 1, 4>;    // warp 16x72, 2 warps
+using NK10 = TileCfg<16, 72, 16, 1, 1, 4>;   // warp 16x72, 1 warp
 
-const char* kKnNames[] = {"128x128", "144x128", "72x128", "88x128", "64x64", "72x64", "128x64", "128x128k32"};
-const char* kNkNames[] = {"128x128", "128x144", "128x72", "128x88", "64x64", "64x72", "64x128", "128x128k32"};
+const char* kKnNames[] = {"128x128", "144x128", "72x128", "88x128", "64x64", "72x64",
+                          "128x64", "128x128k32", "144x64", "72x32", "72x16"};
+const char* kNkNames[] = {"128x128", "128x144", "128x72", "128x88", "64x64", "64x72",
+                          "64x128", "128x128k32", "64x144", "32x72", "16x72"};
+constexpr int kNumCfg = 11;
 
 }  // namespace
 
-int gemm_num_configs(BLayout) { return 8; }
+int gemm_num_configs(BLayout) { return kNumCfg; }
 
 const char* gemm_config_name(BLayout L, int cfg) {
-  if (cfg < 0 || cfg >= 8) return "?";
+  if (cfg < 0 || cfg >= kNumCfg) return "?";
   return L == BLayout::KN ? kKnNames[cfg] : kNkNames[cfg];
 }
 
@@ -86,6 +104,9 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 5: return launch_cfg<KN5, BLayout::KN>(ctx, stream, p);
       case 6: return launch_cfg<KN6, BLayout::KN>(ctx, stream, p);
       case 7: return launch_cfg<KN7, BLayout::KN>(ctx, stream, p);
+      case 8: return launch_cfg<KN8, BLayout::KN>(ctx, stream, p);
+      case 9: return launch_cfg<KN9, BLayout::KN>(ctx, stream, p);
+      case 10: return launch_cfg<KN10, BLayout::KN>(ctx, stream, p);
     }
   } else {
     switch (cfg) {
@@ -97,13 +118,74 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 5: return launch_cfg<NK5, BLayout::NK>(ctx, stream, p);
       case 6: return launch_cfg<NK6, BLayout::NK>(ctx, stream, p);
       case 7: return launch_cfg<NK7, BLayout::NK>(ctx, stream, p);
+      case 8: return launch_cfg<NK8, BLayout::NK>(ctx, stream, p);
+      case 9: return launch_cfg<NK9, BLayout::NK>(ctx, stream, p);
+      case 10: return launch_cfg<NK10, BLayout::NK>(ctx, stream, p);
     }
   }
   set_error("bad GEMM configuration %d", cfg);
   return FDIGA_ERR_INVALID_ARG;
 }
 
+// ---- tuning table: the tile configuration per problem shape, measured once on a B200 and shipped with the
+// library (paper_1705_04384_b200/gemm_table.txt, next to lib/), so a plan picks the same kernels in every
+// run -- including runs under a profiler, where event timing is meaningless.  Shapes missing from the
+// table are autotuned at setup; FDIGA_GEMM_TABLE_OUT=<file> appends those results ("L M N K inner cfg").
+namespace {
+struct TuneKey {
+  int L, M, N, K;
+  int64_t inner;
+  bool operator==(const TuneKey& o) const {
+    return L == o.L && M == o.M && N == o.N && K == o.K && inner == o.inner;
+  }
+};
+std::vector<std::pair<TuneKey, int>> g_table;
+std::mutex g_table_mu;
+bool g_table_loaded = false;
+
+std::string table_path() {
+  if (const char* e = getenv("FDIGA_GEMM_TABLE")) return e;
+  Dl_info info;
+  if (dladdr(reinterpret_cast<void*>(&gemm_num_configs), &info) && info.dli_fname) {
+    std::string so = info.dli_fname;  // .../paper_1705_04384_b200/lib/libfdiga.so
+    const size_t cut = so.rfind("/lib/");
+    if (cut != std::string::npos) return so.substr(0, cut) + "/gemm_table.txt";
+  }
+  return "";
+}
+
+void load_table() {
+  if (g_table_loaded) return;
+  g_table_loaded = true;
+  const std::string path = table_path();
+  if (path.empty() || getenv("FDIGA_GEMM_TUNE_ALWAYS")) return;
+  FILE* f = fopen(path.c_str(), "r");
+  if (!f) return;
+  char line[256];
+  while (fgets(line, sizeof line, f)) {
+    char lay[8];
+    int M, N, K, cfg;
+    long long inner;
+    if (line[0] == '#' || sscanf(line, "%7s %d %d %d %lld %d", lay, &M, &N, &K, &inner, &cfg) != 6) continue;
+    if (cfg < 0 || cfg >= kNumCfg) continue;
+    g_table.push_back({{lay[0] == 'K' ? 0 : 1, M, N, K, (int64_t)inner}, cfg});
+  }
+  fclose(f);
+}
+}  // namespace
+
 int gemm_autotune(fdiga_ctx* ctx, BLayout L, const GemmParams& p, int* best_cfg, float* best_ms) {
+  const TuneKey key{L == BLayout::KN ? 0 : 1, p.M, p.N, p.K, L == BLayout::KN ? p.inner : 0};
+  {
+    std::lock_guard<std::mutex> lk(g_table_mu);
+    load_table();
+    for (const auto& e : g_table)
+      if (e.first == key) {
+        *best_cfg = e.second;
+        if (best_ms) *best_ms = 0.0f;
+        return FDIGA_OK;
+      }
+  }
   cudaStream_t s = ctx->stream;
   cudaEvent_t e0, e1;
   FDIGA_CUDA(cudaEventCreate(&e0));
@@ -137,6 +219,17 @@ int gemm_autotune(fdiga_ctx* ctx, BLayout L, const GemmParams& p, int* best_cfg,
   FDIGA_CUDA(cudaGetLastError());
   *best_cfg = best;
   if (best_ms) *best_ms = best_t;
+  {
+    std::lock_guard<std::mutex> lk(g_table_mu);
+    g_table.push_back({key, best});
+    if (const char* out = getenv("FDIGA_GEMM_TABLE_OUT")) {
+      if (FILE* f = fopen(out, "a")) {
+        fprintf(f, "%s %d %d %d %lld %d  # %s %.2f us\n", L == BLayout::KN ? "KN" : "NK", p.M, p.N, p.K,
+                (long long)key.inner, best, gemm_config_name(L, best), 1e3 * best_t);
+        fclose(f);
+      }
+    }
+  }
   return FDIGA_OK;
 }
 
