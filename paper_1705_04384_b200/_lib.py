@@ -3,7 +3,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libfdiga.so")
+LIB_PATH = os.environ.get("FDIGA_LIB") or os.path.join(_PKG, "lib", "libfdiga.so")  # override: experiments
 
 c_int64_p = C.POINTER(C.c_int64)
 c_double_p = C.POINTER(C.c_double)
