@@ -364,11 +364,13 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        torch.cuda.profiler.start()  # ncu --profile-from-start off captures exactly the timed steps
         e0.record(stream)
         for _ in range(args.steps):
             fd.fd_apply(plan, x, s)
         e1.record(stream)
         e1.synchronize()
+        torch.cuda.profiler.stop()
     torch.cuda.synchronize()
     sync_all()
     launches = ctx.kernel_launches() - launches0
