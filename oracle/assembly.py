@@ -12,6 +12,9 @@ D^{(0)} = M^C, D^{(1)} = B', D^{(2)} = B'' = -K^C, the operator is
     A_C = sum_{a,b} diag(-G_ab) (x)_l D_l^{(e_a+e_b)_l}  +  sum_a diag(beta_a) (x)_l D_l^{(e_a)_l}
 with (x)_l ordered D_d (x) ... (x) D_1 (i_1 fastest).
 For the identity map G = I, beta = 0 and this is exactly eq:colloc2D / eq:colloc3D.
+
+Convection-diffusion (NEXT-4; eq:convection P:345, L_w = -Lap + w . grad): grad_x u = J^{-T} grad_xi u^, so
+w . grad_x u = (J^{-1} w) . grad_xi u^ and the first-order coefficient becomes beta_a + (J^{-1} w(F(tau)))_a.
 """
 import numpy as np
 import scipy.sparse as sp
@@ -23,8 +26,9 @@ from .splines import colloc_1d
 class Discretisation:
     """1D factors + pointwise geometry coefficients for one (d, p, ne, geometry)."""
 
-    def __init__(self, d, p, ne, geometry, params=()):
+    def __init__(self, d, p, ne, geometry, params=(), wind=0, wind_params=()):
         self.d, self.p, self.ne, self.geometry, self.params = d, p, ne, geometry, tuple(params)
+        self.wind, self.wind_params = wind, tuple(wind_params)
         tau, M, K, D1 = colloc_1d(ne, p)
         self.tau, self.M, self.K, self.D1 = tau, M, K, D1
         self.n = len(tau)
@@ -44,11 +48,13 @@ class Discretisation:
         """G (N, d, d) and beta (N, d) at every collocation point F(tau_i)."""
         if self._coeffs is None:
             xi = self.points()
-            _, J, H = geo.evaluate(self.geometry, xi, self.params)
+            F, J, H = geo.evaluate(self.geometry, xi, self.params)
             Jinv = np.linalg.inv(J)
             G = np.linalg.inv(np.einsum("pca,pcb->pab", J, J))            # (J^T J)^{-1}
             trGH = np.einsum("pab,pcba->pc", G, H)                         # tr(G H_c) for each c
             beta = np.einsum("pac,pc->pa", Jinv, trGH)
+            if self.wind:
+                beta = beta + np.einsum("pac,pc->pa", Jinv, geo.wind(self.wind, F, self.wind_params))
             self._coeffs = (G, beta)
         return self._coeffs
 

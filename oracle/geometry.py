@@ -101,6 +101,26 @@ def thick_ring_inverse(x, r0=1.0, r1=2.0, height=1.0):
     return np.concatenate([annulus_inverse(x[:, :2], r0, r1), x[:, 2:3] / height], axis=1)
 
 
+WIND_NONE, WIND_CONSTANT, WIND_ROTATING = 0, 1, 2
+
+
+def wind(kind: int, x: np.ndarray, params=()):
+    """Physical wind w(x) of the convection-diffusion operator L_w = -Lap + w . grad (eq:convection).
+    WIND_CONSTANT: w = (w_1..w_d) = params; WIND_ROTATING: w = omega (-x_2, x_1, 0..) (rigid rotation about the
+    x_3 axis), omega = params[0].  Returns (P, d)."""
+    P, d = x.shape
+    if kind == WIND_NONE:
+        return np.zeros((P, d))
+    if kind == WIND_CONSTANT:
+        return np.broadcast_to(np.asarray(params[:d], dtype=np.float64), (P, d)).copy()
+    if kind == WIND_ROTATING:
+        w = np.zeros((P, d))
+        w[:, 0] = -params[0] * x[:, 1]
+        w[:, 1] = params[0] * x[:, 0]
+        return w
+    raise ValueError(f"unknown wind {kind}")
+
+
 def evaluate(geometry: int, xi: np.ndarray, params=()):
     if geometry == IDENTITY:
         return identity(xi)

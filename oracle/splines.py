@@ -112,6 +112,15 @@ def colloc_1d(ne: int, p: int):
     return tau, M, K, D1
 
 
+def colloc_1d_convection(ne: int, p: int, wt):
+    """1D convection factor of the collocation analogue of eq:convec_prec_2:
+    H[i, j] = w~(tau_i) B'_j(tau_i) at the interior Greville points (wt: scalar or the n values w~(tau_i)).
+    The collocation counterpart of the paper's Galerkin H_l = int w~ B_i B'_j (reading 17)."""
+    tau, M, K, D1 = colloc_1d(ne, p)
+    wt = np.broadcast_to(np.asarray(wt, dtype=np.float64), tau.shape)
+    return wt[:, None] * D1
+
+
 def flatten_index(mi, n: int) -> int:
     """1-based multi-index (i_1..i_d) -> scalar i = 1 + sum_l n^{l-1}(i_l - 1)."""
     return 1 + sum((n ** l) * (il - 1) for l, il in enumerate(mi))

@@ -24,6 +24,8 @@ class Config:
     geometry: int
     geo_params: Tuple[float, ...] = field(default_factory=tuple)
     note: str = ""
+    wind: int = 0            # NEXT-4 only: 0 none, 1 constant, 2 rigid rotation about x_3 (omega = wind_params[0])
+    wind_params: Tuple[float, ...] = field(default_factory=tuple)
 
     @property
     def n(self) -> int:
@@ -42,12 +44,25 @@ CONFIGS = {
     5: Config(5, 3, 5, 128, GEOM_THICK_RING, (1.0, 2.0, 1.0), "3D p=5 128^3 thick quarter ring"),
 }
 
+# NEXT-4 workloads (not BASELINE.json configs): convection-diffusion L_w = -Lap + w . grad
+# (eq:convection) on the cfg5 geometry with the rotating wind w = omega (-y, x, 0), for which
+# J^{-1} w = (0, 2 omega / pi, 0) exactly, so the univariate wind of eq:convec_prec_2 is w~_2 = 2 omega / pi.
+#   6: strongly convective (omega = 3000, ne = 32): the preconditioner's pencil (K_2 + H_2, M_2) has complex
+#      pairs; without the wind (eq:convec_prec_1) GMRES(30) does not converge in 300 steps.
+#   7: mildly convective (omega = 10) at the full cfg5 size: real spectrum.
+NEXT4_CONFIGS = {
+    6: Config(6, 3, 5, 32, GEOM_THICK_RING, (1.0, 2.0, 1.0), "NEXT-4: cfg5 geometry, rotating wind omega=3000",
+              2, (3000.0,)),
+    7: Config(7, 3, 5, 128, GEOM_THICK_RING, (1.0, 2.0, 1.0), "NEXT-4: cfg5 geometry, rotating wind omega=10",
+              2, (10.0,)),
+}
+
 # cfg4 is the isolated FD-apply sweep: d=3, n in {128, 256, 512}, random factors.
 FD_SWEEP_N = (128, 256, 512)
 
 
 def get_config(cfg: int) -> Config:
-    return CONFIGS[cfg]
+    return CONFIGS[cfg] if cfg in CONFIGS else NEXT4_CONFIGS[cfg]
 
 
 def n_dofs(ne: int, p: int) -> int:

@@ -135,3 +135,80 @@ def test_chain_rule_coefficients_identity():
     G, beta = disc.coefficients()
     np.testing.assert_allclose(G, np.broadcast_to(np.eye(2), G.shape), atol=0)
     np.testing.assert_allclose(beta, 0, atol=0)
+
+
+# ---- convection-diffusion (NEXT-4; eq:convection P:345, L_w = -Lap + w . grad)
+
+def test_convection_identity_map_constant_wind_is_kronecker():
+    # identity map, constant wind: A = sum_k (x)_l (K_k + H_k if l = k else M_l) with the collocation
+    # factor H_k = w_k B'_j(tau_i) (the collocation analogue of eq:convec_prec_2)
+    d, p, ne, w = 3, 3, 4, (2.0, -3.0, 0.5)
+    disc = assembly.Discretisation(d, p, ne, GEOM_IDENTITY, (), wind=geo.WIND_CONSTANT, wind_params=w)
+    A = disc.assemble_csr().toarray()
+    Ks = [disc.K + splines.colloc_1d_convection(ne, p, w[l]) for l in range(d)]
+    P = assembly.kron_preconditioner_dense([disc.M] * d, Ks)
+    np.testing.assert_allclose(A, P, atol=1e-12 * np.abs(P).max())
+
+
+def test_convection_factor_pins():
+    # full-basis derivative rows sum to 0 (partition of unity); Greville reproduction x = sum tau*_j B_j
+    # differentiates to sum_j tau*_j B'_j = 1, so on interior rows far from the boundary H reproduces w~
+    ne, p = 8, 3
+    knots = splines.open_uniform_knots(ne, p)
+    tau_full = splines.greville_full(knots, p)
+    tau, M, K, D1 = splines.colloc_1d(ne, p)
+    H = splines.colloc_1d_convection(ne, p, 5.0)
+    np.testing.assert_allclose(H, 5.0 * D1, atol=0)
+    i = len(tau) // 2
+    row_full = np.array([splines.basis_all(knots, p, tau[i], 1)[k] for k in range(len(tau_full))])
+    np.testing.assert_allclose(row_full.sum(), 0.0, atol=1e-12)
+    np.testing.assert_allclose(row_full @ tau_full, 1.0, atol=1e-12)
+
+
+def _fd_convection_entry(disc, i_flat, j_flat, h=1e-4):
+    """(-Lap + w . grad)(B^_j o F^{-1}) at F(tau_i) by central differences in physical space."""
+    d, n = disc.d, disc.n
+    kv = splines.open_uniform_knots(disc.ne, disc.p)
+    ii = [(i_flat // n ** l) % n for l in range(d)]
+    jj = [(j_flat // n ** l) % n for l in range(d)]
+    xi0 = np.array([[disc.tau[ii[l]] for l in range(d)]])
+    x0, _, _ = geo.evaluate(disc.geometry, xi0, disc.params)
+
+    def u(x):
+        xi = geo.inverse(disc.geometry, x[None, :], disc.params)[0]
+        v = 1.0
+        for l in range(d):
+            v *= splines.basis_all(kv, disc.p, float(np.clip(xi[l], 0, 1)), 0)[jj[l] + 1]
+        return v
+
+    c = u(x0[0])
+    w = geo.wind(disc.wind, x0, disc.wind_params)[0]
+    val = 0.0
+    for k in range(d):
+        e = np.zeros(d)
+        e[k] = h
+        up, um = u(x0[0] + e), u(x0[0] - e)
+        val += -(up - 2 * c + um) / h ** 2 + w[k] * (up - um) / (2 * h)
+    return val
+
+
+@pytest.mark.parametrize("d,geom,params,wind,wp", [(2, GEOM_ANNULUS, (1.0, 2.0), geo.WIND_ROTATING, (7.0,)),
+                                                   (3, GEOM_THICK_RING, (1.0, 2.0, 1.0), geo.WIND_ROTATING, (3.0,)),
+                                                   (3, GEOM_DEFORMED_CUBE, (0.1,), geo.WIND_CONSTANT,
+                                                    (1.0, -2.0, 4.0))])
+def test_convection_entries_equal_physical_operator(d, geom, params, wind, wp):
+    disc = assembly.Discretisation(d, 5, 5, geom, params, wind=wind, wind_params=wp)
+    rng = np.random.default_rng(11)
+    for i in rng.choice(disc.N, 3, replace=False):
+        row = disc.row(int(i))
+        for j in list(row)[:6]:
+            ref = _fd_convection_entry(disc, int(i), int(j))
+            assert abs(row[j] - ref) <= 2e-5 * max(1.0, abs(ref)), (i, j, row[j], ref)
+
+
+def test_rotating_wind_is_angular_on_the_ring():
+    # w = omega (-y, x, 0) on the thick ring: J^{-1} w = (0, 2 omega / pi, 0) exactly (synth NEXT-4 configs)
+    xi = np.random.default_rng(2).uniform(0, 1, (20, 3))
+    F, J, _ = geo.thick_ring(xi)
+    v = np.linalg.solve(J, geo.wind(geo.WIND_ROTATING, F, (3.0,))[..., None])[..., 0]
+    np.testing.assert_allclose(v, np.tile([0.0, 6.0 / np.pi, 0.0], (20, 1)), atol=1e-12)

@@ -31,6 +31,28 @@ def main():
                                         bicgstab_rel_res_true=repb["rel_res_true"],
                                         seconds=round(time.time() - t0, 2))
         print(cfg, out["configs"][str(cfg)], flush=True)
+    # NEXT-4 convection-diffusion workloads: GMRES(30) with the wind-aware FD preconditioner (collocation
+    # analogue of eq:convec_prec_2: K_2 + H_2 in the angular direction, complex pairs allowed) and without
+    # the wind (eq:convec_prec_1), max 300 steps
+    import numpy as np
+    from oracle import splines
+    out["next4"] = {}
+    for cfg in (6, 7):
+        c = get_config(cfg)
+        t0 = time.time()
+        disc = assembly.Discretisation(c.d, c.p, c.ne, c.geometry, c.geo_params, c.wind, c.wind_params)
+        H2 = splines.colloc_1d_convection(c.ne, c.p, 2 * c.wind_params[0] / np.pi)
+        fw = fastdiag.setup([disc.M] * 3, [disc.K, disc.K + H2, disc.K], allow_complex=True, cond_max=1e30)
+        f0 = fastdiag.setup([disc.M] * 3, [disc.K] * 3)
+        b = rhs(cfg, disc.N)
+        _, rw = krylov.gmres(disc.matvec, b, precond=lambda v: fastdiag.apply(fw, v), max_iters=300)
+        _, r0 = krylov.gmres(disc.matvec, b, precond=lambda v: fastdiag.apply(f0, v), max_iters=300)
+        out["next4"][str(cfg)] = dict(ne=c.ne, p=c.p, n=disc.n, N=disc.N, omega=c.wind_params[0],
+                                      iters_wind_fd=rw["iters"], converged_wind_fd=rw["converged"],
+                                      rel_res_true_wind_fd=rw["rel_res_true"], has_complex_pairs=bool(fw.has_pairs),
+                                      iters_plain_fd=r0["iters"], converged_plain_fd=r0["converged"],
+                                      seconds=round(time.time() - t0, 2))
+        print(cfg, out["next4"][str(cfg)], flush=True)
     with open(os.path.join(ROOT, "tests", "golden", "oracle_gmres.json"), "w") as fh:
         json.dump(out, fh, indent=1)
 
