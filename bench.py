@@ -296,6 +296,39 @@ def gmres_section(ctx, fd, steps, ws=1, rank=0, sharded=False):
         out[f"cfg{cfg}"] = entry
         P.close()
         A.close()
+    # NEXT-4: convection-diffusion on the cfg5 geometry (synth configs 6, 7), matrix-free operator, GMRES(30)
+    # with the wind-aware FD (collocation analogue of eq:convec_prec_2; complex pairs at cfg 6) and, for
+    # comparison, the plain Laplacian FD (eq:convec_prec_1)
+    for cfg in (6, 7):
+        c = get_config(cfg)
+        A = fd.colloc_assemble(ctx, 3, c.p, c.ne, c.geometry, c.geo_params, matrix_free=True, wind=c.wind,
+                               wind_params=c.wind_params)
+        M, K = fd.colloc_1d_factors(c.p, c.ne)
+        H2 = fd.colloc_1d_convection(c.p, c.ne, 2 * c.wind_params[0] / np.pi)
+        try:
+            Pw = fd.fd_setup(ctx, [M] * 3, [K, K + H2, K], allow_complex_pairs=True, cond_max=1e30)
+        except fd.FdigaError as e:  # complex-pair FD is single-rank
+            out[f"cfg{cfg}_convection"] = {"skipped": str(e)[:120]}
+            A.close()
+            continue
+        P0 = fd.fd_setup(ctx, [M] * 3, [K] * 3)
+        lo = A.slab[0] * A.n[0] * A.n[1]
+        b = torch.from_numpy(rhs(cfg, A.N_global)[lo:lo + A.N].copy()).to(dev)
+        x = torch.empty_like(b)
+        fd.gmres_solve(ctx, A, Pw, b, x, max_iters=300)
+        tw = []
+        for _ in range(3):
+            rw = fd.gmres_solve(ctx, A, Pw, b, x, max_iters=300)
+            tw.append(gmax(rw["t_total_ms"]))
+        r0 = fd.gmres_solve(ctx, A, P0, b, x, max_iters=300, raise_on_nonconvergence=False)
+        out[f"cfg{cfg}_convection"] = {
+            "omega": c.wind_params[0], "ne": c.ne, "N": A.N_global,
+            "wind_fd": {"time_to_tol_ms": float(np.median(tw)), "iters": rw["iters"], "converged": rw["converged"],
+                        "complex_pairs": bool(np.any(Pw.factors(1)[3] != 0))},
+            "plain_fd": {"time_ms": gmax(r0["t_total_ms"]), "iters": r0["iters"], "converged": r0["converged"]}}
+        Pw.close()
+        P0.close()
+        A.close()
     return out
 
 

@@ -53,6 +53,13 @@ enum {
   FDIGA_GEOM_THICK_RING = 3     /* 3D quarter annulus x [0,h], geo_params = {r0, r1, h} */
 };
 
+/* Wind ids for colloc_assemble_cd (convection-diffusion, NEXT-4; eq:convection P:345). */
+enum {
+  FDIGA_WIND_NONE = 0,
+  FDIGA_WIND_CONSTANT = 1, /* w = (wind_params[0], wind_params[1], wind_params[2]) */
+  FDIGA_WIND_ROTATING = 2  /* w = omega (-x_2, x_1, 0), omega = wind_params[0] */
+};
+
 typedef struct fdiga_ctx fdiga_ctx;
 typedef struct fd_plan fd_plan;
 typedef struct fdiga_stencil fdiga_stencil;
@@ -170,6 +177,12 @@ int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometr
  * NOT_SUPPORTED; stencil_info's nnz is the structural count of the equivalent stored operator. */
 int colloc_matrix_free(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
                        fdiga_stencil** out);
+/* Convection-diffusion operator L_w = -Lap + w . grad (eq:convection; NEXT-4), collocated like
+ * colloc_assemble: row i holds (L_w (B_j o F^{-1}))(F(tau_i)), i.e. the first-order coefficient becomes
+ * beta_a + (J^{-1} w(F(tau_i)))_a.  wind_id: FDIGA_WIND_*, wind_params: d constants or {omega}.
+ * matrix_free = 1 builds the on-the-fly operator (3D only), else stored values. */
+int colloc_assemble_cd(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
+                       int wind_id, const double* wind_params, int matrix_free, fdiga_stencil** out);
 /* y = A x.  x, y: device, length N (no aliasing).  Asynchronous on the ctx stream. */
 int stencil_matvec(fdiga_stencil* A, const double* x, double* y);
 /* Number of stored values and the 1D window tables (host copies; any pointer may be NULL). */
@@ -183,6 +196,9 @@ int colloc_1d_factors(int p, int64_t ne, double* M, double* K);
 /* The 1D column windows of the stored operator (host only): row i of direction l couples to columns
  * [start[i], start[i] + width[i]) (length n = ne + p - 2). */
 int colloc_1d_windows(int p, int64_t ne, int32_t* start, int32_t* width);
+/* The 1D convection factor of the collocation analogue of eq:convec_prec_2 (reading 17),
+ * host only: H[i][j] = wt[i] B'_j(tau_i), wt = the univariate wind w~_l at the n Greville points (host). */
+int colloc_1d_convection(int p, int64_t ne, const double* wt, double* H);
 
 /* -------------------------------------------------------------------- GMRES ---- */
 

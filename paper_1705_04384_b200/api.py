@@ -279,13 +279,19 @@ def fd_apply_host(plan, r_host, s_host):
     return s_host
 
 
-def colloc_assemble(ctx, d, p, ne, geometry, geo_params=(), matrix_free=False):
+def colloc_assemble(ctx, d, p, ne, geometry, geo_params=(), matrix_free=False, wind=0, wind_params=()):
     """The collocation operator A_C: stored tensor-window values (colloc_assemble) or, with
-    matrix_free=True, the sum-factorised on-the-fly operator (colloc_matrix_free, 3D)."""
+    matrix_free=True, the sum-factorised on-the-fly operator (colloc_matrix_free, 3D).  wind != 0: the
+    convection-diffusion operator -Lap + w . grad (colloc_assemble_cd, NEXT-4)."""
     nes = [ne] * d if np.isscalar(ne) else list(ne)
     n = (C.c_int64 * d)(*nes)
     prm = np.ascontiguousarray(np.asarray(list(geo_params) + [0.0] * 4, dtype=np.float64))
     h = C.c_void_p()
+    if wind:
+        wp = np.ascontiguousarray(np.asarray(list(wind_params) + [0.0] * 3, dtype=np.float64))
+        check(ctx._lib.colloc_assemble_cd(ctx.handle, d, int(p), n, int(geometry), _dptr(prm), int(wind), _dptr(wp),
+                                          int(bool(matrix_free)), C.byref(h)), "colloc_assemble_cd")
+        return Stencil(ctx, h)
     fn = ctx._lib.colloc_matrix_free if matrix_free else ctx._lib.colloc_assemble
     check(fn(ctx.handle, d, int(p), n, int(geometry), _dptr(prm), C.byref(h)),
           "colloc_matrix_free" if matrix_free else "colloc_assemble")
@@ -317,6 +323,15 @@ def stencil_create(ctx, n, start, width, values):
 def stencil_matvec(A, x, y):
     check(A.ctx._lib.stencil_matvec(A.handle, _devptr(x, A.N), _devptr(y, A.N)), "stencil_matvec")
     return y
+
+
+def colloc_1d_convection(p, ne, wt):
+    """H[i][j] = wt[i] B'_j(tau_i) (host), wt scalar or the n values of the univariate wind."""
+    n = ne + p - 2
+    w = np.ascontiguousarray(np.broadcast_to(np.asarray(wt, dtype=np.float64), (n,)))
+    H = np.empty((n, n))
+    check(load().colloc_1d_convection(int(p), int(ne), _dptr(w), _dptr(H)), "colloc_1d_convection")
+    return H
 
 
 def colloc_1d_factors(p, ne):

@@ -8,6 +8,8 @@ namespace fdiga {
 struct Geo {
   int id;
   double prm[4];
+  int wind;      // FDIGA_WIND_*: convection-diffusion L_w = -Lap + w . grad (eq:convection); 0 = Poisson
+  double wprm[3];
 };
 
 struct JH {
@@ -68,6 +70,38 @@ __device__ __forceinline__ JH geometry_jh(const Geo g, const double x0, const do
   return r;
 }
 
+// The map F(xi) itself (same trigonometric factors as geometry_jh).
+__device__ __forceinline__ void geometry_F(const Geo g, const double x0, const double x1, const double x2,
+                                           const double sn[3], const double cs[3], double F[3]) {
+  F[0] = x0;
+  F[1] = x1;
+  F[2] = x2;
+  if (g.id == FDIGA_GEOM_ANNULUS || g.id == FDIGA_GEOM_THICK_RING) {
+    const double rad = g.prm[0] + (g.prm[1] - g.prm[0]) * x0;
+    F[0] = rad * cs[1];
+    F[1] = rad * sn[1];
+    F[2] = g.id == FDIGA_GEOM_THICK_RING ? g.prm[2] * x2 : 0.0;
+  } else if (g.id == FDIGA_GEOM_DEFORMED_CUBE) {
+    const double bump = g.prm[0] * sn[0] * sn[1] * sn[2];
+    F[0] += bump;
+    F[1] += bump;
+    F[2] += bump;
+  }
+}
+
+// Physical wind w(x) (FDIGA_WIND_*): constant (wprm), or the rigid rotation omega (-x_2, x_1, 0).
+__device__ __forceinline__ void wind_at(const Geo g, const double F[3], double w[3]) {
+  w[0] = w[1] = w[2] = 0.0;
+  if (g.wind == FDIGA_WIND_CONSTANT) {
+    w[0] = g.wprm[0];
+    w[1] = g.wprm[1];
+    w[2] = g.wprm[2];
+  } else if (g.wind == FDIGA_WIND_ROTATING) {
+    w[0] = -g.wprm[0] * F[1];
+    w[1] = g.wprm[0] * F[0];
+  }
+}
+
 // Same, evaluating the trigonometric factors here.
 __device__ __forceinline__ JH geometry_jh(const Geo g, const double x0, const double x1, const double x2) {
   const double th = geo_theta(g.id);
@@ -107,8 +141,11 @@ __device__ __forceinline__ void inv_small(const double A[3][3], double B[3][3]) 
 // Collocation coefficients at one point (eq:collocation, chain rule):
 //   -Lap_x u = - sum_ab G_ab d_a d_b u^ + sum_a beta_a d_a u^,  G = (J^T J)^{-1},
 //   beta_a = sum_c (J^{-1})_{ac} tr(G H_c).
+// wphys (may be nullptr): the physical wind at the point; adds (J^{-1} w)_a to beta_a (w . grad_x u =
+// (J^{-1} w) . grad_xi u^, NEXT-4).
 template <int D>
-__device__ __forceinline__ void colloc_coeffs(const JH& jh, double G[3][3], double beta[3]) {
+__device__ __forceinline__ void colloc_coeffs(const JH& jh, double G[3][3], double beta[3],
+                                              const double* wphys = nullptr) {
   double Ji[3][3];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
@@ -136,6 +173,12 @@ __device__ __forceinline__ void colloc_coeffs(const JH& jh, double G[3][3], doub
       for (int b = 0; b < D; ++b) tr += G[a][b] * jh.H[c][b][a];
 #pragma unroll
     for (int a = 0; a < D; ++a) beta[a] += Ji[a][c] * tr;
+  }
+  if (wphys) {
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int c = 0; c < D; ++c) beta[a] += Ji[a][c] * wphys[c];
   }
 }
 

@@ -199,10 +199,13 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
       // the ring maps do not depend on xi_3: one coefficient set per (i1, i2)
       const bool dep3 = A.geo.id == FDIGA_GEOM_DEFORMED_CUBE;
       double G[3][3], beta[3];
-      if (!dep3) {
+      double Fp[3], wv[3];
+      if (!dep3) {  // the ring maps and the winds used with them do not depend on xi_3
         sn[2] = 0.0;
         cs[2] = 1.0;
-        colloc_coeffs<3>(geometry_jh(A.geo, xi1, sn, cs), G, beta);
+        geometry_F(A.geo, xi1, __ldg(A.tau2 + g2), 0.0, sn, cs, Fp);
+        wind_at(A.geo, Fp, wv);
+        colloc_coeffs<3>(geometry_jh(A.geo, xi1, sn, cs), G, beta, A.geo.wind ? wv : nullptr);
       }
       for (int i3 = tid / (T * T); i3 < m3; i3 += NT / (T * T)) {
         const int64_t g3 = a3 + i3;
@@ -237,7 +240,9 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
         if (dep3) {
           sn[2] = __ldg(A.trig3 + 2 * g3);
           cs[2] = __ldg(A.trig3 + 2 * g3 + 1);
-          colloc_coeffs<3>(geometry_jh(A.geo, xi1, sn, cs), G, beta);
+          geometry_F(A.geo, xi1, __ldg(A.tau2 + g2), __ldg(A.tau3 + g3), sn, cs, Fp);
+          wind_at(A.geo, Fp, wv);
+          colloc_coeffs<3>(geometry_jh(A.geo, xi1, sn, cs), G, beta, A.geo.wind ? wv : nullptr);
         }
         double yv = beta[2] * z[0] - G[2][2] * z[1] + beta[1] * z[2] - 2.0 * G[1][2] * z[3] - G[1][1] * z[4] +
                     beta[0] * z[5] - 2.0 * G[0][2] * z[6] - 2.0 * G[0][1] * z[7] - G[0][0] * z[8];

@@ -194,7 +194,17 @@ __global__ void assemble_kernel(AsmArgs A) {
   const int64_t i1 = row % A.n1, i2 = (row / A.n1) % A.n2, i3 = row / (A.n1 * A.n2);
   const double x0 = A.tau1[i1], x1 = A.tau2[i2], x2 = (D == 3) ? A.tau3[i3] : 0.0;
   double G[3][3], beta[3];
-  colloc_coeffs<D>(geometry_jh(A.geo, x0, x1, x2), G, beta);
+  {
+    const double th = geo_theta(A.geo.id);
+    double sn[3], cs[3];
+    sincos(th * x0, &sn[0], &cs[0]);
+    sincos(th * x1, &sn[1], &cs[1]);
+    sincos(th * x2, &sn[2], &cs[2]);
+    double F[3], w[3];
+    geometry_F(A.geo, x0, x1, x2, sn, cs, F);
+    wind_at(A.geo, F, w);
+    colloc_coeffs<D>(geometry_jh(A.geo, x0, sn, cs), G, beta, A.geo.wind ? w : nullptr);
+  }
   const int W = A.wmax;
   const int w1 = A.w1[i1];
   const int w2 = A.w2[i2];
@@ -564,7 +574,7 @@ int stencil_create(fdiga_ctx* ctx, int d, const int64_t* n, const int32_t* const
 }
 
 static int colloc_build(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
-                        int matrix_free, fdiga_stencil** out) {
+                        int wind_id, const double* wind_params, int matrix_free, fdiga_stencil** out) {
   FDIGA_CHECK(ctx && ne && out, FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_CHECK(d == 2 || d == 3, FDIGA_ERR_INVALID_ARG, "d must be 2 or 3");
   FDIGA_CHECK(p >= 1 && p <= 8, FDIGA_ERR_INVALID_ARG, "degree p = %d out of range", p);
@@ -609,6 +619,13 @@ static int colloc_build(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geo
                                                          : geometry_id == FDIGA_GEOM_THICK_RING  ? 3 : 0;
     FDIGA_CHECK(np == 0 || geo_params, FDIGA_ERR_INVALID_ARG, "geometry %d needs %d parameters", geometry_id, np);
     for (int k = 0; k < np; ++k) A.geo.prm[k] = geo_params[k];
+    A.geo.wind = wind_id;
+    for (int k = 0; k < 3; ++k) A.geo.wprm[k] = 0.0;
+    FDIGA_CHECK(wind_id >= FDIGA_WIND_NONE && wind_id <= FDIGA_WIND_ROTATING, FDIGA_ERR_INVALID_ARG, "wind id %d",
+                wind_id);
+    const int nw = wind_id == FDIGA_WIND_CONSTANT ? d : wind_id == FDIGA_WIND_ROTATING ? 1 : 0;
+    FDIGA_CHECK(nw == 0 || wind_params, FDIGA_ERR_INVALID_ARG, "wind %d needs %d parameters", wind_id, nw);
+    for (int k = 0; k < nw; ++k) A.geo.wprm[k] = wind_params[k];
     const double* taus[3] = {nullptr, nullptr, nullptr};
     const double* tabs[3] = {nullptr, nullptr, nullptr};
     for (int l = 0; l < d && s == FDIGA_OK; ++l) {
@@ -713,12 +730,29 @@ static int colloc_build(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geo
 
 int colloc_assemble(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
                     fdiga_stencil** out) {
-  return colloc_build(ctx, d, p, ne, geometry_id, geo_params, 0, out);
+  return colloc_build(ctx, d, p, ne, geometry_id, geo_params, FDIGA_WIND_NONE, nullptr, 0, out);
 }
 
 int colloc_matrix_free(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
                        fdiga_stencil** out) {
-  return colloc_build(ctx, d, p, ne, geometry_id, geo_params, 1, out);
+  return colloc_build(ctx, d, p, ne, geometry_id, geo_params, FDIGA_WIND_NONE, nullptr, 1, out);
+}
+
+int colloc_assemble_cd(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
+                       int wind_id, const double* wind_params, int matrix_free, fdiga_stencil** out) {
+  return colloc_build(ctx, d, p, ne, geometry_id, geo_params, wind_id, wind_params, matrix_free ? 1 : 0, out);
+}
+
+int colloc_1d_convection(int p, int64_t ne, const double* wt, double* H) {
+  FDIGA_CHECK(H && wt && p >= 1 && ne >= 1 && ne + p - 2 >= 1, FDIGA_ERR_INVALID_ARG,
+              "bad colloc_1d_convection arguments");
+  Table1D T;
+  build_table(p, ne, T);
+  const int64_t n = T.n;
+  std::memset(H, 0, n * n * sizeof(double));
+  for (int64_t i = 0; i < n; ++i)
+    for (int c = 0; c < T.width[i]; ++c) H[i * n + T.start[i] + c] = wt[i] * T.val[1][i * T.wmax + c];
+  return FDIGA_OK;
 }
 
 int stencil_matvec(fdiga_stencil* S, const double* x, double* y) { return fdiga::stencil_matvec_ex(S, x, y, nullptr); }

@@ -462,3 +462,50 @@ def test_gmres_orthogonalisation_variants_agree(ctx, cfg):
     assert r1["iters"] == r2["iters"] == GOLD["configs"][str(cfg)]["iters"]
     assert r2["reorth"] == r2["iters"] and 0 <= r1["reorth"] <= r1["iters"]
     assert rel(host(x1), host(x2)) <= 1e-7
+
+
+# ----------------------------------------------------------------------------- NEXT-4: convection-diffusion
+
+@pytest.mark.parametrize("d,geom,params,wind,wp,ne,mf", [
+    (3, 3, (1.0, 2.0, 1.0), 2, (3000.0,), 7, False), (3, 3, (1.0, 2.0, 1.0), 2, (3000.0,), 7, True),
+    (3, 2, (0.1,), 1, (1.0, -2.0, 4.0), 6, False), (3, 2, (0.1,), 1, (1.0, -2.0, 4.0), 9, True),
+    (3, 0, (), 2, (5.0,), 5, True), (2, 1, (1.0, 2.0), 2, (7.0,), 9, False),
+    (3, 3, (1.0, 2.0, 1.0), 2, (10.0,), None, True)])
+def test_convection_operator_matches_oracle(ctx, d, geom, params, wind, wp, ne, mf):
+    p = 5 if d == 3 else 3
+    ne = ne or 128
+    disc = assembly.Discretisation(d, p, ne, geom, params, wind=wind, wind_params=wp)
+    A = fd.colloc_assemble(ctx, d, p, ne, geom, params, matrix_free=mf, wind=wind, wind_params=wp)
+    x = np.random.default_rng(ne + wind).standard_normal(disc.N)
+    y = torch.empty(disc.N, dtype=torch.float64, device=DEV)
+    fd.stencil_matvec(A, gpu(x), y)
+    assert rel(host(y), disc.matvec(x)) <= 1e-12
+
+
+def test_convection_factor_matches_oracle():
+    wt = np.linspace(-3.0, 5.0, 11)
+    np.testing.assert_allclose(fd.colloc_1d_convection(3, 10, wt), splines.colloc_1d_convection(10, 3, wt),
+                               rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("cfg", [6, 7])
+def test_convection_gmres_wind_aware_fd(ctx, cfg):
+    # eq:convec_prec_2 (collocation analogue): K_2 + H_2 with w~_2 = 2 omega / pi; complex pairs at cfg 6
+    c = get_config(cfg)
+    ref = GOLD["next4"][str(cfg)]
+    A = fd.colloc_assemble(ctx, 3, c.p, c.ne, c.geometry, c.geo_params, matrix_free=True, wind=c.wind,
+                           wind_params=c.wind_params)
+    M, K = fd.colloc_1d_factors(c.p, c.ne)
+    H2 = fd.colloc_1d_convection(c.p, c.ne, 2 * c.wind_params[0] / np.pi)
+    Pw = fd.fd_setup(ctx, [M] * 3, [K, K + H2, K], allow_complex_pairs=True, cond_max=1e30)
+    assert np.any(Pw.factors(1)[3] != 0) == ref["has_complex_pairs"]
+    b = gpu(rhs(cfg, A.N))
+    x = torch.empty_like(b)
+    rep = fd.gmres_solve(ctx, A, Pw, b, x, max_iters=300)
+    assert rep["converged"] and abs(rep["iters"] - ref["iters_wind_fd"]) <= 1, (rep, ref)
+    P0 = fd.fd_setup(ctx, [M] * 3, [K] * 3)
+    rep0 = fd.gmres_solve(ctx, A, P0, b, x, max_iters=300, raise_on_nonconvergence=False)
+    if ref["converged_plain_fd"]:
+        assert abs(rep0["iters"] - ref["iters_plain_fd"]) <= 1
+    else:
+        assert rep0["status"] == -8 and rep0["iters"] == 300
