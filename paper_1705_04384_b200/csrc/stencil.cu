@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "ptx.cuh"
 #include "geometry.cuh"
+#include "bspline.h"
 #include "matfree.cuh"
 
 using namespace fdiga;
@@ -62,60 +63,6 @@ struct fdiga_stencil {
 };
 
 namespace {
-
-// ------------------------------------------------------------------ host B-spline tables
-// Piegl & Tiller "DersBasisFuns": nonzero basis functions of degree p on the knot span `span`
-// and their derivatives up to order nd, ders[k][r] for functions span-p+r, r = 0..p.
-void ders_basis_funs(int span, double u, int p, int nd, const std::vector<double>& U,
-                     std::vector<std::vector<double>>& ders) {
-  std::vector<std::vector<double>> ndu(p + 1, std::vector<double>(p + 1));
-  std::vector<double> left(p + 1), right(p + 1);
-  ndu[0][0] = 1.0;
-  for (int j = 1; j <= p; ++j) {
-    left[j] = u - U[span + 1 - j];
-    right[j] = U[span + j] - u;
-    double saved = 0.0;
-    for (int r = 0; r < j; ++r) {
-      ndu[j][r] = right[r + 1] + left[j - r];
-      double temp = ndu[r][j - 1] / ndu[j][r];
-      ndu[r][j] = saved + right[r + 1] * temp;
-      saved = left[j - r] * temp;
-    }
-    ndu[j][j] = saved;
-  }
-  ders.assign(nd + 1, std::vector<double>(p + 1, 0.0));
-  for (int j = 0; j <= p; ++j) ders[0][j] = ndu[j][p];
-  std::vector<std::vector<double>> a(2, std::vector<double>(p + 1));
-  for (int r = 0; r <= p; ++r) {
-    int s1 = 0, s2 = 1;
-    a[0][0] = 1.0;
-    for (int k = 1; k <= nd; ++k) {
-      double dd = 0.0;
-      int rk = r - k, pk = p - k;
-      if (r >= k) {
-        a[s2][0] = a[s1][0] / ndu[pk + 1][rk];
-        dd = a[s2][0] * ndu[rk][pk];
-      }
-      int j1 = (rk >= -1) ? 1 : -rk;
-      int j2 = (r - 1 <= pk) ? k - 1 : p - r;
-      for (int j = j1; j <= j2; ++j) {
-        a[s2][j] = (a[s1][j] - a[s1][j - 1]) / ndu[pk + 1][rk + j];
-        dd += a[s2][j] * ndu[rk + j][pk];
-      }
-      if (r <= pk) {
-        a[s2][k] = -a[s1][k - 1] / ndu[pk + 1][r];
-        dd += a[s2][k] * ndu[r][pk];
-      }
-      ders[k][r] = dd;
-      std::swap(s1, s2);
-    }
-  }
-  int r = p;
-  for (int k = 1; k <= nd; ++k) {
-    for (int j = 0; j <= p; ++j) ders[k][j] *= r;
-    r *= (p - k);
-  }
-}
 
 // 1D tables for one direction: Greville points, windows, and B^{(r)}_j(tau_i) on the window.
 struct Table1D {
