@@ -296,6 +296,27 @@ def gmres_section(ctx, fd, steps, ws=1, rank=0, sharded=False):
         out[f"cfg{cfg}"] = entry
         P.close()
         A.close()
+    # NEXT-3: weighted-quadrature Galerkin systems (synth configs 8, 9), symmetric FD of the Galerkin pencils
+    for cfg in ((9,) if sharded else (8, 9)):
+        c = get_config(cfg)
+        A = fd.wq_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params)
+        M, K = fd.galerkin_1d_factors(c.p, c.ne)
+        P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
+        lo = A.slab[0] * A.n[0] * A.n[1]
+        b = torch.from_numpy(rhs(cfg, A.N_global)[lo:lo + A.N].copy()).to(dev)
+        x = torch.empty_like(b)
+        fd.gmres_solve(ctx, A, P, b, x)
+        tg, tb = [], []
+        for _ in range(3):
+            rg = fd.gmres_solve(ctx, A, P, b, x)
+            tg.append(gmax(rg["t_total_ms"]))
+            rb = fd.bicgstab_solve(ctx, A, P, b, x)
+            tb.append(gmax(rb["t_total_ms"]))
+        out[f"cfg{cfg}_wq"] = {"N": A.N_global, "p": c.p, "ne": c.ne, "nnz_stored": A.nnz,
+                               "gmres": {"time_to_tol_ms": float(np.median(tg)), "iters": rg["iters"]},
+                               "bicgstab": {"time_to_tol_ms": float(np.median(tb)), "iters": rb["iters"]}}
+        P.close()
+        A.close()
     # NEXT-4: convection-diffusion on the cfg5 geometry (synth configs 6, 7), matrix-free operator, GMRES(30)
     # with the wind-aware FD (collocation analogue of eq:convec_prec_2; complex pairs at cfg 6) and, for
     # comparison, the plain Laplacian FD (eq:convec_prec_1)

@@ -183,6 +183,16 @@ int colloc_matrix_free(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geom
  * matrix_free = 1 builds the on-the-fly operator (3D only), else stored values. */
 int colloc_assemble_cd(fdiga_ctx* ctx, int d, int p, const int64_t* ne, int geometry_id, const double* geo_params,
                        int wind_id, const double* wind_params, int matrix_free, fdiga_stencil** out);
+/* Weighted-quadrature Galerkin operator A_wq (eq:WQapprox P:195-199, eq:Q P:192) on
+ * the same analytic maps, stored in the tensor-window layout (windows |i_l - j_l| <= p): degree p <= 5,
+ * ne elements per direction (same in every direction).  The 1D rule (reading 18) is built on
+ * the host, Q = det(J) J^{-1} J^{-T} on the device point grid, the rows by sum factorisation on the
+ * device.  Sharded contexts assemble their slab's rows (3D).  Setup only; synchronises. */
+int wq_assemble(fdiga_ctx* ctx, int d, int p, int64_t ne, int geometry_id, const double* geo_params,
+                fdiga_stencil** out);
+/* Univariate Galerkin factors (eq:univariateWQ P:209; host out, row-major n x n):
+ * M[i][j] = int B_i B_j, K[i][j] = int B'_i B'_j -- the symmetric pencils of the WQ preconditioner. */
+int galerkin_1d_factors(int p, int64_t ne, double* M, double* K);
 /* y = A x.  x, y: device, length N (no aliasing).  Asynchronous on the ctx stream. */
 int stencil_matvec(fdiga_stencil* A, const double* x, double* y);
 /* Number of stored values and the 1D window tables (host copies; any pointer may be NULL). */

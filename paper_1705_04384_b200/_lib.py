@@ -75,6 +75,8 @@ SIGNATURES = {
     "colloc_assemble_cd": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_int64_p, C.c_int, c_double_p, C.c_int,
                                      c_double_p, C.c_int, C.POINTER(C.c_void_p)]),
     "colloc_1d_convection": (C.c_int, [C.c_int, C.c_int64, c_double_p, c_double_p]),
+    "wq_assemble": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int, c_double_p, C.POINTER(C.c_void_p)]),
+    "galerkin_1d_factors": (C.c_int, [C.c_int, C.c_int64, c_double_p, c_double_p]),
     "stencil_matvec": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "stencil_info": (C.c_int, [C.c_void_p, c_int64_p, c_int64_p, c_int32_p, c_int32_p]),
     "stencil_get_values": (C.c_int, [C.c_void_p, c_double_p]),

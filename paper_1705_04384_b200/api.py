@@ -334,6 +334,23 @@ def colloc_1d_convection(p, ne, wt):
     return H
 
 
+def wq_assemble(ctx, d, p, ne, geometry, geo_params=()):
+    """The weighted-quadrature Galerkin operator A_wq (NEXT-3) in the tensor-window layout."""
+    prm = np.ascontiguousarray(np.asarray(list(geo_params) + [0.0] * 4, dtype=np.float64))
+    h = C.c_void_p()
+    check(ctx._lib.wq_assemble(ctx.handle, int(d), int(p), int(ne), int(geometry), _dptr(prm), C.byref(h)),
+          "wq_assemble")
+    return Stencil(ctx, h)
+
+
+def galerkin_1d_factors(p, ne):
+    """Univariate Galerkin factors M = int B_i B_j, K = int B'_i B'_j (host)."""
+    n = ne + p - 2
+    M, K = np.empty((n, n)), np.empty((n, n))
+    check(load().galerkin_1d_factors(int(p), int(ne), _dptr(M), _dptr(K)), "galerkin_1d_factors")
+    return M, K
+
+
 def colloc_1d_factors(p, ne):
     n = ne + p - 2
     M, K = np.empty((n, n)), np.empty((n, n))

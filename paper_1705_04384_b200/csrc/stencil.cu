@@ -426,7 +426,7 @@ int finish_stencil(fdiga_stencil* S) {
   const int64_t n1 = S->n[0];
   int wm1 = 0;
   for (int64_t i = 0; i < n1; ++i) wm1 = std::max<int>(wm1, S->hwidth[0][i]);
-  FDIGA_CHECK(wm1 <= 9, FDIGA_ERR_NOT_SUPPORTED, "direction-1 window width %d > 9", wm1);
+  FDIGA_CHECK(wm1 <= 11, FDIGA_ERR_NOT_SUPPORTED, "direction-1 window width %d > 11", wm1);
   S->wm1 = wm1;
   S->hvoff1.assign(n1 * wm1, 0);
   int64_t colpre = 0;
@@ -802,6 +802,8 @@ int stencil_matvec_ex(fdiga_stencil* S, const double* x, double* y, const int* s
     FDIGA_MV_CASE(7)
     FDIGA_MV_CASE(8)
     FDIGA_MV_CASE(9)
+    FDIGA_MV_CASE(10)
+    FDIGA_MV_CASE(11)
 #undef FDIGA_MV_CASE
 #undef FDIGA_MV_LAUNCH
     default:

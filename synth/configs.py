@@ -57,12 +57,24 @@ NEXT4_CONFIGS = {
               2, (10.0,)),
 }
 
+# NEXT-3 workloads: the weighted-quadrature Galerkin system A_wq u = f (eq:WQsystem)
+# with the symmetric FD of the exact 1D Galerkin pencils (eq:univariateWQ) as preconditioner.
+#   8: the quarter annulus of cfg2 (Table 3's domain), p = 3, 256 x 256 elements
+#   9: the thick quarter ring of cfg5, p = 3, 32^3 elements
+WQ_CONFIGS = {
+    8: Config(8, 2, 3, 256, GEOM_ANNULUS, (1.0, 2.0), "NEXT-3: WQ-Galerkin, quarter annulus p=3 256x256"),
+    9: Config(9, 3, 3, 32, GEOM_THICK_RING, (1.0, 2.0, 1.0), "NEXT-3: WQ-Galerkin, thick ring p=3 32^3"),
+}
+
 # cfg4 is the isolated FD-apply sweep: d=3, n in {128, 256, 512}, random factors.
 FD_SWEEP_N = (128, 256, 512)
 
 
 def get_config(cfg: int) -> Config:
-    return CONFIGS[cfg] if cfg in CONFIGS else NEXT4_CONFIGS[cfg]
+    for table in (CONFIGS, NEXT4_CONFIGS, WQ_CONFIGS):
+        if cfg in table:
+            return table[cfg]
+    raise KeyError(cfg)
 
 
 def n_dofs(ne: int, p: int) -> int:

@@ -509,3 +509,41 @@ def test_convection_gmres_wind_aware_fd(ctx, cfg):
         assert abs(rep0["iters"] - ref["iters_plain_fd"]) <= 1
     else:
         assert rep0["status"] == -8 and rep0["iters"] == 300
+
+
+# ----------------------------------------------------------------------------- NEXT-3: weighted quadrature
+
+@pytest.mark.parametrize("d,p,ne,geom,params", [(2, 2, 7, 1, (1.0, 2.0)), (2, 3, 9, 1, (1.0, 2.0)),
+                                                (2, 4, 8, 1, (1.0, 2.0)), (2, 5, 11, 1, (1.0, 2.0)),
+                                                (3, 2, 5, 3, (1.0, 2.0, 1.0)), (3, 3, 6, 2, (0.1,)),
+                                                (3, 4, 5, 0, ()), (2, 3, 1, 1, (1.0, 2.0))])
+def test_wq_operator_matches_oracle(ctx, d, p, ne, geom, params):
+    from oracle import quadrature
+    if ne + p - 2 < 1:
+        pytest.skip("empty space")
+    disc = quadrature.WQDiscretisation(d, p, ne, geom, params)
+    Ao = disc.assemble_wq()
+    A = fd.wq_assemble(ctx, d, p, ne, geom, params)
+    assert A.nnz >= Ao.nnz
+    x = np.random.default_rng(d * 10 + p + ne).standard_normal(disc.N)
+    y = torch.empty(disc.N, dtype=torch.float64, device=DEV)
+    fd.stencil_matvec(A, gpu(x), y)
+    assert rel(host(y), Ao @ x) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg", [8, 9])
+def test_wq_solvers_match_oracle_counts(ctx, cfg):
+    c = get_config(cfg)
+    ref = GOLD["wq"][str(cfg)]
+    A = fd.wq_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params)
+    M, K = fd.galerkin_1d_factors(c.p, c.ne)
+    P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
+    for l in range(c.d):   # symmetric positive definite pencil: real, positive spectrum (V = U)
+        U, W, lam, lam_im = P.factors(l)
+        assert np.all(lam_im == 0) and np.all(lam > 0)
+    b = gpu(rhs(cfg, A.N))
+    x = torch.empty_like(b)
+    rep = fd.gmres_solve(ctx, A, P, b, x)
+    assert rep["converged"] and abs(rep["iters"] - ref["iters"]) <= 1
+    rb = fd.bicgstab_solve(ctx, A, P, b, x)
+    assert rb["converged"] and abs(rb["iters"] - ref["bicgstab_iters"]) <= 1.0

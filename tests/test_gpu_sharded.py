@@ -285,3 +285,24 @@ def test_sharded_matrix_free_matvec(cfg, ne, nranks):
 
     y = np.concatenate(run_ranks(nranks, work))
     assert rel(y, disc.matvec(x)) <= 1e-12
+
+
+def test_sharded_wq_matvec():
+    from oracle import quadrature
+    disc = quadrature.WQDiscretisation(3, 3, 7, 3, (1.0, 2.0, 1.0))
+    Ao = disc.assemble_wq()
+    x = np.random.default_rng(3).standard_normal(disc.N)
+    n = disc.n
+
+    def work(ctx, rank):
+        A = fd.wq_assemble(ctx, 3, 3, 7, 3, (1.0, 2.0, 1.0))
+        lo, hi = slab_rows(n, 3, rank, n * n)
+        y = torch.empty(hi - lo, dtype=torch.float64, device=DEV)
+        fd.stencil_matvec(A, torch.from_numpy(x[lo:hi].copy()).to(DEV), y)
+        torch.cuda.current_stream().synchronize()
+        out = y.cpu().numpy()
+        A.close()
+        return out
+
+    y = np.concatenate(run_ranks(3, work))
+    assert rel(y, Ao @ x) <= 1e-12

@@ -87,3 +87,23 @@ def test_wq_3d_thick_ring_close_to_galerkin():
     A = disc.assemble_wq().toarray()
     G = disc.assemble_galerkin().toarray()
     assert np.linalg.norm(A - G) / np.linalg.norm(G) < 0.05
+
+
+@pytest.mark.slow
+def test_wq_bicgstab_counts_match_paper_table3():
+    # Table 3: BiCGStab + FD on the WQ quarter ring needs 16.0 iterations for every h and p; with the
+    # readings of Table 2's pin (radii 1, 2, tol 1e-6, x0 = 0) and a random b the counts are within 2 and
+    # independent of p (the preconditioner is the symmetric FD of the exact Galerkin pencils)
+    from oracle import fastdiag, krylov
+    from synth import rhs
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_table3_wq_bicgstab.json")))
+    counts = []
+    for j, p in enumerate(gold["p"]):
+        disc = qd.WQDiscretisation(2, p, 128, GEOM_ANNULUS, (1.0, 2.0))
+        A = disc.assemble_wq()
+        M, K, _ = splines.galerkin_1d(128, p, 0.0)
+        f = fastdiag.setup([M] * 2, [K] * 2)
+        _, rep = krylov.bicgstab(lambda v: A @ v, rhs(8, disc.N), precond=lambda v: fastdiag.apply(f, v), rtol=1e-6)
+        assert rep["converged"] and abs(rep["iters"] - gold["iterations"]["128"][j]) <= 2.0
+        counts.append(rep["iters"])
+    assert max(counts) - min(counts) <= 1.0

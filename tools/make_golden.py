@@ -53,6 +53,24 @@ def main():
                                       iters_plain_fd=r0["iters"], converged_plain_fd=r0["converged"],
                                       seconds=round(time.time() - t0, 2))
         print(cfg, out["next4"][str(cfg)], flush=True)
+    # NEXT-3 weighted-quadrature Galerkin workloads: GMRES(30) and BiCGStab with the symmetric FD of the
+    # exact 1D Galerkin pencils
+    from oracle import quadrature
+    out["wq"] = {}
+    for cfg in (8, 9):
+        c = get_config(cfg)
+        t0 = time.time()
+        disc = quadrature.WQDiscretisation(c.d, c.p, c.ne, c.geometry, c.geo_params)
+        A = disc.assemble_wq()
+        M, K, _ = splines.galerkin_1d(c.ne, c.p, 0.0)
+        f = fastdiag.setup([M] * c.d, [K] * c.d)
+        b = rhs(cfg, disc.N)
+        _, rg = krylov.gmres(lambda v: A @ v, b, precond=lambda v: fastdiag.apply(f, v))
+        _, rb = krylov.bicgstab(lambda v: A @ v, b, precond=lambda v: fastdiag.apply(f, v))
+        out["wq"][str(cfg)] = dict(d=c.d, p=c.p, ne=c.ne, n=disc.n, N=disc.N, nnz=int(A.nnz), iters=rg["iters"],
+                                   rel_res_true=rg["rel_res_true"], bicgstab_iters=rb["iters"],
+                                   seconds=round(time.time() - t0, 2))
+        print(cfg, out["wq"][str(cfg)], flush=True)
     with open(os.path.join(ROOT, "tests", "golden", "oracle_gmres.json"), "w") as fh:
         json.dump(out, fh, indent=1)
 
