@@ -53,15 +53,23 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int KV_ = 0>
 struct TileCfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  // KV = 1 (BK = 16): k-permuted fragments.  MMA step kk of a k-tile contracts the k indices
+  // {kk, kk + 4, kk + 8, kk + 12}, thread lc taking k = 4 lc + kk, so a thread's four A (and NK-B)
+  // fragments of the tile are 4 consecutive doubles: two 16-byte shared loads instead of four 8-byte
+  // ones.  The same permutation on both operands leaves the product unchanged (summation order only).
+  static constexpr int KV = KV_;
+  static_assert(KV == 0 || BK == 16, "k-permuted fragments need BK = 16");
   static constexpr int THREADS = WM * WN * 32;
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int MI = WTM / 8, NJ = WTN / 8;
-  static constexpr int SA = BK + 4;    // A row stride (doubles): == 4 (mod 16) for BK % 16 == 0
+  // A row stride (doubles): == 4 (mod 16) -> conflict-free 8-byte fragment loads; KV: == 2 (mod 16) ->
+  // conflict-free 16-byte loads (a quarter-warp covers two rows x four 4-word groups)
+  static constexpr int SA = BK + (KV ? 2 : 4);
   static constexpr int SBkn = BN + 4;  // B [k][n] row stride (BN % 16 == 0 -> == 4 mod 16; else 8-way split phases)
-  static constexpr int SBnk = BK + 4;  // B [n][k] row stride
+  static constexpr int SBnk = BK + (KV ? 2 : 4);  // B [n][k] row stride
   static_assert(WTM % 8 == 0 && WTN % 8 == 0 && BK % 4 == 0, "tile shape");
   static constexpr int A_ELEMS = BM * SA;
   static constexpr int B_ELEMS_KN = BK * SBkn;
@@ -195,22 +203,58 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
     const int st = kt % T::STAGES;
     const double* a_s = sA + st * T::A_ELEMS + (warp_m * T::WTM + lr) * T::SA + lc;
     const double* b_s = sB + st * BE;
+    if (T::KV) {
+      // k-permuted fragments: thread lc holds k = 4 lc + kk for the four steps kk of the tile
+      const double* a_v = a_s - lc + 4 * lc;
+      double af[T::MI][4], bf[T::NJ][4];
 #pragma unroll
-    for (int kk = 0; kk < T::BK / 4; ++kk) {
-      double af[T::MI], bf[T::NJ];
-#pragma unroll
-      for (int i = 0; i < T::MI; ++i) af[i] = a_s[i * 8 * T::SA + kk * 4];
-#pragma unroll
-      for (int j = 0; j < T::NJ; ++j) {
-        if (BL == BLayout::KN)
-          bf[j] = b_s[(kk * 4 + lc) * T::SBkn + warp_n * T::WTN + j * 8 + lr];
-        else
-          bf[j] = b_s[(warp_n * T::WTN + j * 8 + lr) * T::SBnk + kk * 4 + lc];
+      for (int i = 0; i < T::MI; ++i) {
+        const double2 x0 = *reinterpret_cast<const double2*>(a_v + i * 8 * T::SA);
+        const double2 x1 = *reinterpret_cast<const double2*>(a_v + i * 8 * T::SA + 2);
+        af[i][0] = x0.x;
+        af[i][1] = x0.y;
+        af[i][2] = x1.x;
+        af[i][3] = x1.y;
       }
 #pragma unroll
-      for (int i = 0; i < T::MI; ++i)
+      for (int j = 0; j < T::NJ; ++j) {
+        if (BL == BLayout::KN) {
 #pragma unroll
-        for (int j = 0; j < T::NJ; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+          for (int kk = 0; kk < 4; ++kk) bf[j][kk] = b_s[(4 * lc + kk) * T::SBkn + warp_n * T::WTN + j * 8 + lr];
+        } else {
+          const double* bp = b_s + (warp_n * T::WTN + j * 8 + lr) * T::SBnk + 4 * lc;
+          const double2 y0 = *reinterpret_cast<const double2*>(bp);
+          const double2 y1 = *reinterpret_cast<const double2*>(bp + 2);
+          bf[j][0] = y0.x;
+          bf[j][1] = y0.y;
+          bf[j][2] = y1.x;
+          bf[j][3] = y1.y;
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < T::NJ; ++j) dmma_8x8x4(acc[i][j], af[i][kk], bf[j][kk]);
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < T::BK / 4; ++kk) {
+        double af[T::MI], bf[T::NJ];
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i) af[i] = a_s[i * 8 * T::SA + kk * 4];
+#pragma unroll
+        for (int j = 0; j < T::NJ; ++j) {
+          if (BL == BLayout::KN)
+            bf[j] = b_s[(kk * 4 + lc) * T::SBkn + warp_n * T::WTN + j * 8 + lr];
+          else
+            bf[j] = b_s[(warp_n * T::WTN + j * 8 + lr) * T::SBnk + kk * 4 + lc];
+        }
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < T::NJ; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+      }
     }
   }
   cp_async_wait<0>();

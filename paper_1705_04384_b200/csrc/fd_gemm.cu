@@ -66,6 +66,8 @@ using KN7 = TileCfg<128, 128, 32, 2, 4, 3>;  // BK = 32: half the barriers
 using KN8 = TileCfg<144, 64, 16, 2, 2, 3>;   // warp 72x32, 4 warps, 3 stages: 2 CTAs/SM (n in (128, 144])
 using KN9 = TileCfg<72, 32, 16, 1, 2, 4>;    // warp 72x16, 2 warps (n <= 72, small N)
 using KN10 = TileCfg<72, 16, 16, 1, 1, 4>;   // warp 72x16, 1 warp  (n <= 72, tiny N)
+using KN11 = TileCfg<64, 64, 16, 2, 2, 4, 1>;   // KN4 with k-permuted 16-byte fragment loads
+using KN12 = TileCfg<64, 128, 16, 2, 2, 3, 1>;  // warp 32x64, 4 warps, 3 stages, k-permuted fragments
 using NK0 = TileCfg<128, 128, 16, 2, 4, 4>;
 using NK1 = TileCfg<128, 144, 16, 4, 2, 4>;  // warp 32x72
 using NK2 = TileCfg<128, 72, 16, 8, 1, 4>;   // warp 16x72
@@ -77,12 +79,14 @@ using NK7 = TileCfg<128, 128, 32, 2, 4, 3>;
 using NK8 = TileCfg<64, 144, 16, 2, 2, 3>;   // warp 32x72, 4 warps, 3 stages: 2 CTAs/SM
 using NK9 = TileCfg<32, 72, 16, 2, 1, 4>;    // warp 16x72, 2 warps
 using NK10 = TileCfg<16, 72, 16, 1, 1, 4>;   // warp 16x72, 1 warp
+using NK11 = TileCfg<64, 64, 16, 2, 2, 4, 1>;   // NK4 with k-permuted 16-byte fragment loads
+using NK12 = TileCfg<64, 128, 16, 2, 2, 3, 1>;  // NK6 with k-permuted 16-byte fragment loads
 
 const char* kKnNames[] = {"128x128", "144x128", "72x128", "88x128", "64x64", "72x64",
-                          "128x64", "128x128k32", "144x64", "72x32", "72x16"};
+                          "128x64", "128x128k32", "144x64", "72x32", "72x16", "64x64kv", "64x128kv"};
 const char* kNkNames[] = {"128x128", "128x144", "128x72", "128x88", "64x64", "64x72",
-                          "64x128", "128x128k32", "64x144", "32x72", "16x72"};
-constexpr int kNumCfg = 11;
+                          "64x128", "128x128k32", "64x144", "32x72", "16x72", "64x64kv", "64x128kv"};
+constexpr int kNumCfg = 13;
 
 }  // namespace
 
@@ -107,6 +111,8 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 8: return launch_cfg<KN8, BLayout::KN>(ctx, stream, p);
       case 9: return launch_cfg<KN9, BLayout::KN>(ctx, stream, p);
       case 10: return launch_cfg<KN10, BLayout::KN>(ctx, stream, p);
+      case 11: return launch_cfg<KN11, BLayout::KN>(ctx, stream, p);
+      case 12: return launch_cfg<KN12, BLayout::KN>(ctx, stream, p);
     }
   } else {
     switch (cfg) {
@@ -121,6 +127,8 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 8: return launch_cfg<NK8, BLayout::NK>(ctx, stream, p);
       case 9: return launch_cfg<NK9, BLayout::NK>(ctx, stream, p);
       case 10: return launch_cfg<NK10, BLayout::NK>(ctx, stream, p);
+      case 11: return launch_cfg<NK11, BLayout::NK>(ctx, stream, p);
+      case 12: return launch_cfg<NK12, BLayout::NK>(ctx, stream, p);
     }
   }
   set_error("bad GEMM configuration %d", cfg);
@@ -175,6 +183,14 @@ void load_table() {
 }  // namespace
 
 int gemm_autotune(fdiga_ctx* ctx, BLayout L, const GemmParams& p, int* best_cfg, float* best_ms) {
+  // experiments / tests: force one configuration per layout
+  if (const char* f = getenv(L == BLayout::KN ? "FDIGA_GEMM_FORCE_KN" : "FDIGA_GEMM_FORCE_NK")) {
+    const int c = atoi(f);
+    FDIGA_CHECK(c >= 0 && c < kNumCfg, FDIGA_ERR_INVALID_ARG, "bad forced GEMM configuration %d", c);
+    *best_cfg = c;
+    if (best_ms) *best_ms = 0.0f;
+    return FDIGA_OK;
+  }
   const TuneKey key{L == BLayout::KN ? 0 : 1, p.M, p.N, p.K, L == BLayout::KN ? p.inner : 0};
   {
     std::lock_guard<std::mutex> lk(g_table_mu);
