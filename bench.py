@@ -145,13 +145,13 @@ def cpu_fd_sample(n, budget_s=12.0, max_reps=20):
 
 def run_reference(args):
     """The reference arm: the CPU oracle (numpy mode products) on this box's host cores, on the same
-    workload as our arm at this N (weak-scaling shape), rank 0 only.  Steps are capped so that the run
+    workload as our arm (the n^3 apply at every N), rank 0 only.  Steps are capped so that the run
     stays within ~1 minute of CPU work (a bounded sample; the JSON says how many applies were timed)."""
     ws, rank, _ = dist_init()
     if rank != 0:
         return
     n = args.n
-    ns = weak_shape(n, ws)
+    ns = (n, n, n)
     N = int(np.prod(ns))
     from oracle import fastdiag
     from synth import fd_sweep_factors, fd_sweep_vector
@@ -178,7 +178,7 @@ def run_reference(args):
     shape = "x".join(map(str, ns))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": "GDOF/s", "n_gpus": ws, "steps": steps,
-        "warmup": warm + 1, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": warm + 1, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"cfg4 FD apply P^-1 r, d=3, n={shape} (oracle on the host CPU)", "n": n,
                    "shape": list(ns), "N": N},
@@ -362,6 +362,8 @@ def main():
     ap.add_argument("--impl", default="fdiga", choices=["fdiga", "reference"])
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-weak", action="store_true")
+    ap.add_argument("--weak", action="store_true", help="also run the weak-scaling section at N = 1 (tests)")
     ap.add_argument("--sharded", action="store_true",
                     help="at --gpus 1: run the slab-sharded path over a one-rank NCCL communicator (tests the N>1 code)")
     args = ap.parse_args()
@@ -396,7 +398,9 @@ def main():
     stream = torch.cuda.current_stream()
     ctx = fd.Context(local, stream=stream.cuda_stream, nranks=ws, rank=rank, nccl_unique_id=uid)
     n = args.n
-    ns = weak_shape(n, ws)
+    # every N applies the same n^3 FD (strong scaling; the driver computes the efficiency from the values);
+    # the weak-scaling family of SURVEY.md §8(d) is reported beside it (flop-rate efficiency)
+    ns = (n, n, n)
     N = int(np.prod(ns))
     # setup (not timed): W_l = U_l^{-1} on the device (fd_setup_from_eig, M = I), BASELINE.json configs[3]
     rng, U, lam = fd_sweep_factors(ns)
@@ -455,6 +459,37 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    weak = None
+    if (ws > 1 or args.weak) and not args.no_weak:
+        # weak-scaling family: N / P fixed at n^3, directions doubled from the last one.
+        # Flop-rate efficiency against this GPU's own single-rank n^3 apply (FD work per DOF grows with the
+        # factor sizes, so GDOF/s is not comparable across the family)
+        wns = weak_shape(n, ws)
+        rngw, Uw, lamw = fd_sweep_factors(wns)
+        plan_w = fd.fd_setup_from_eig(ctx, Uw, lamw)
+        gw = torch.Generator(device=dev)
+        gw.manual_seed(5000 + rank)
+        xw = torch.randn(plan_w.N, dtype=torch.float64, device=dev, generator=gw)
+        sw = torch.empty_like(xw)
+        ms_w = timed(lambda: fd.fd_apply(plan_w, xw, sw), stream, max(3, min(args.steps, 10)), 2, sync_all)
+        if ws > 1:
+            t = torch.tensor([ms_w], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_w = float(t.item())
+        ctx1 = fd.Context(local, stream=stream.cuda_stream)  # single-rank reference on this GPU
+        plan_1 = fd.fd_setup_from_eig(ctx1, U, lam)
+        x1 = torch.randn(N, dtype=torch.float64, device=dev, generator=gw)
+        s1 = torch.empty_like(x1)
+        ms_1 = timed(lambda: fd.fd_apply(plan_1, x1, s1), stream, max(3, min(args.steps, 10)), 2)
+        tf_1 = plan_1.flops() / ms_1 / 1e9
+        tf_w = plan_w.flops() / ws / ms_w / 1e9
+        weak = {"shape": list(wns), "N": int(np.prod(wns)), "ms_per_apply": ms_w,
+                "GDOF_per_s": float(np.prod(wns)) / ms_w / 1e6, "tflops_per_gpu": tf_w,
+                "single_gpu_tflops_n3": tf_1, "flop_rate_efficiency": tf_w / tf_1}
+        plan_1.close()
+        ctx1.close()
+        plan_w.close()
+        del x1, s1, xw, sw
     traffic = None
     if os.path.exists(NCU_SUMMARY):
         try:
@@ -472,10 +507,10 @@ def main():
     if rank == 0:
         rec = {
             "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"cfg4 FD apply P^-1 r, d=3, n={'x'.join(map(str, ns))} (BASELINE.json configs[3]"
-                                   + (", weak-scaling family SURVEY.md §8(d))" if ws > 1 else ")"),
+                                   + (f", slab-sharded over {ws} GPUs)" if ws > 1 else ")"),
                        "n": n, "shape": list(ns), "N": N,
                        "factors": "U ~ N(0,1), lam ~ U(1,100), W = U^-1 (device LU), x ~ N(0,1)",
                        "l2": "inputs > L2: 134 MB vector + 3 x 134 MB work buffers per GPU vs 126 MB L2" if n >= 256
@@ -496,6 +531,7 @@ def main():
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "gmres": gm,
+            "weak_scaling": weak,
         }
         print(json.dumps(rec), flush=True)
     for h in (plan,):
