@@ -85,6 +85,9 @@ struct TileCfg {
 // VA / VB: doubles per cp.async chunk for A / B (2 needs 16-byte aligned rows, else 1).
 template <class T, BLayout BL, int VA, int VB>
 __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) {
+  // programmatic dependent launch: this grid may start while the previous kernel of the stream drains;
+  // nothing it produced (the B/A operand, the skip flag) is read before its completion is awaited here
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (p.skip && *p.skip) return;
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;
@@ -258,6 +261,8 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
     }
   }
   cp_async_wait<0>();
+  // the next mode product may begin launching its CTAs (they wait for this grid's completion)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
   // ---- epilogue: optional eigenvalue-sum divide (eq:FD3D diagonal term), store
   const bool c_vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((p.ldc & 1) == 0) &&

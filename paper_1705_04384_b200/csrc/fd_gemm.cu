@@ -22,6 +22,12 @@ namespace {
 
 inline bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
+// programmatic dependent launch of the mode products (FDIGA_PDL=0 disables it, for A/B measurements)
+const bool g_pdl = [] {
+  const char* e = getenv("FDIGA_PDL");
+  return !(e && e[0] == '0');
+}();
+
 template <class T, BLayout BL, int VA, int VB>
 int launch_variant(fdiga_ctx* ctx, cudaStream_t stream, GemmParams p) {
   auto kern = dmma_gemm_kernel<T, BL, VA, VB>;
@@ -35,7 +41,20 @@ int launch_variant(fdiga_ctx* ctx, cudaStream_t stream, GemmParams p) {
   p.tiles_n = (p.N + T::BN - 1) / T::BN;
   const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n;
   FDIGA_CHECK(tiles >= 1 && tiles < (int64_t(1) << 31), FDIGA_ERR_NOT_SUPPORTED, "GEMM grid too large");
-  kern<<<(unsigned)tiles, T::THREADS, smem, stream>>>(p);
+  // programmatic dependent launch (Blackwell/Hopper): overlaps this launch and its CTAs' setup with the
+  // tail of the previous kernel on the stream (the kernel waits with griddepcontrol.wait before reading)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)tiles);
+  cfg.blockDim = dim3(T::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  // only for grids of at least a full wave: tiny grids (n = 65) measured slower with it
+  attr[0].val.programmaticStreamSerializationAllowed = (g_pdl && tiles >= ctx->sm_count) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FDIGA_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());
   return FDIGA_OK;
