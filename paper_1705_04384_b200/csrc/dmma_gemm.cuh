@@ -53,9 +53,15 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int KV_ = 0>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int KV_ = 0, int NP_ = 0>
 struct TileCfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  // NP = 1 (KN layout, with KV, warp tiles 64 wide): n-permuted fragments.  Within a warp tile the
+  // logical column (MMA j, lane row r) is the physical column r NJ + j, so a thread's NJ B fragments of
+  // one k are NJ consecutive doubles (16-byte loads) and its accumulators map to two runs of NJ
+  // consecutive output columns.  The shared B tile is unpadded with its 16-byte chunks XOR-swizzled by
+  // (k / 4) mod 4, which makes those 16-byte loads bank-conflict free.
+  static constexpr int NP = NP_;
   // KV = 1 (BK = 16): k-permuted fragments.  MMA step kk of a k-tile contracts the k indices
   // {kk, kk + 4, kk + 8, kk + 12}, thread lc taking k = 4 lc + kk, so a thread's four A (and NK-B)
   // fragments of the tile are 4 consecutive doubles: two 16-byte shared loads instead of four 8-byte
@@ -68,9 +74,10 @@ struct TileCfg {
   // A row stride (doubles): == 4 (mod 16) -> conflict-free 8-byte fragment loads; KV: == 2 (mod 16) ->
   // conflict-free 16-byte loads (a quarter-warp covers two rows x four 4-word groups)
   static constexpr int SA = BK + (KV ? 2 : 4);
-  static constexpr int SBkn = BN + 4;  // B [k][n] row stride (BN % 16 == 0 -> == 4 mod 16; else 8-way split phases)
+  static constexpr int SBkn = NP ? BN : BN + 4;  // B [k][n] row stride (padded: == 4 mod 16 for BN % 16 == 0)
   static constexpr int SBnk = BK + (KV ? 2 : 4);  // B [n][k] row stride
   static_assert(WTM % 8 == 0 && WTN % 8 == 0 && BK % 4 == 0, "tile shape");
+  static_assert(NP == 0 || (KV == 1 && WTN == 64), "n-permuted fragments need KV and 64-wide warp tiles");
   static constexpr int A_ELEMS = BM * SA;
   static constexpr int B_ELEMS_KN = BK * SBkn;
   static constexpr int B_ELEMS_NK = BN * SBnk;
@@ -154,7 +161,9 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
       for (int c = tid; c < CH; c += T::THREADS) {
         const int r = c / CPR_B_KN;
         const int gk = k0 + r;
-        const uint32_t d = smem_u32(dstB + r * T::SBkn + cc * VB);
+        int pc = cc * VB;  // physical column of the chunk (NP: 16-byte chunks XOR-swizzled by (k / 4) mod 4)
+        if (T::NP) pc = ((((cc * VB) >> 1) ^ ((r >> 2) & 3)) << 1) | ((cc * VB) & 1);
+        const uint32_t d = smem_u32(dstB + r * T::SBkn + pc);
         int bytes = 0;
         const double* src = B;
         if (gk < K && b_col_bytes) {
@@ -221,7 +230,17 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
       }
 #pragma unroll
       for (int j = 0; j < T::NJ; ++j) {
-        if (BL == BLayout::KN) {
+        if (BL == BLayout::KN && T::NP) {
+          if (j % 2 == 0) {  // physical columns warp_n WTN + lr NJ + j, j + 1: one 16-byte chunk
+            const int c16 = ((warp_n * T::WTN + lr * T::NJ + j) >> 1) ^ lc;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const double2 y = *reinterpret_cast<const double2*>(b_s + (4 * lc + kk) * T::SBkn + 2 * c16);
+              bf[j][kk] = y.x;
+              bf[j + 1][kk] = y.y;
+            }
+          }
+        } else if (BL == BLayout::KN) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) bf[j][kk] = b_s[(4 * lc + kk) * T::SBkn + warp_n * T::WTN + j * 8 + lr];
         } else {
@@ -267,6 +286,45 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
   // ---- epilogue: optional eigenvalue-sum divide (eq:FD3D diagonal term), store
   const bool c_vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((p.ldc & 1) == 0) &&
                      (BL == BLayout::NK || ((p.inner & 1) == 0 && (p.bstride & 1) == 0));
+  if (T::NP) {
+    // accumulator (i, j, h) is physical column warp_n WTN + (2 lc + h) NJ + j: pairs (j, j + 1) adjacent
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < T::NJ; j += 2) {
+        const int col = n0 + warp_n * T::WTN + (2 * lc + h) * T::NJ + j;
+        if (col >= N) continue;
+        const bool two = col + 1 < N;
+        const int64_t sl = col / p.inner, lidx = col - sl * p.inner;
+        const int64_t coff = sl * p.bstride + lidx;
+        int64_t coff1 = coff + 1, lidx1 = lidx + 1;
+        if (two && lidx1 >= p.inner) {
+          lidx1 = 0;
+          coff1 = (sl + 1) * p.bstride;
+        }
+        const double ln0 = p.lam_m ? p.lam_n[lidx] : 0.0;
+        const double ln1 = (p.lam_m && two) ? p.lam_n[lidx1] : 0.0;
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i) {
+          const int row = m0 + warp_m * T::WTM + i * 8 + lr;
+          if (row >= M) continue;
+          double v0 = acc[i][j][h], v1 = acc[i][j + 1][h];
+          if (p.lam_m) {
+            const double lm = p.lam_m[row];
+            v0 = v0 / (lm + ln0);
+            v1 = v1 / (lm + ln1);
+          }
+          double* dst = C + (int64_t)row * p.ldc;
+          if (c_vec && two && coff1 == coff + 1) {
+            *reinterpret_cast<double2*>(dst + coff) = make_double2(v0, v1);
+          } else {
+            dst[coff] = v0;
+            if (two) dst[coff1] = v1;
+          }
+        }
+      }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < T::NJ; ++j) {
     const int col = n0 + warp_n * T::WTN + j * 8 + 2 * lc;

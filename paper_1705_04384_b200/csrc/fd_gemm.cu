@@ -87,6 +87,9 @@ using KN9 = TileCfg<72, 32, 16, 1, 2, 4>;    // warp 72x16, 2 warps (n <= 72, sm
 using KN10 = TileCfg<72, 16, 16, 1, 1, 4>;   // warp 72x16, 1 warp  (n <= 72, tiny N)
 using KN11 = TileCfg<64, 64, 16, 2, 2, 4, 1>;   // KN4 with k-permuted 16-byte fragment loads
 using KN12 = TileCfg<64, 128, 16, 2, 2, 3, 1>;  // warp 32x64, 4 warps, 3 stages, k-permuted fragments
+using KN13 = TileCfg<64, 128, 16, 2, 2, 3, 1, 1>;   // warp 32x64, k- and n-permuted fragments, 3 stages
+using KN14 = TileCfg<64, 128, 16, 2, 2, 4, 1, 1>;   // same, 4 stages
+using KN15 = TileCfg<128, 128, 16, 4, 2, 4, 1, 1>;  // 8 warps of 32x64, k- and n-permuted
 using NK0 = TileCfg<128, 128, 16, 2, 4, 4>;
 using NK1 = TileCfg<128, 144, 16, 4, 2, 4>;  // warp 32x72
 using NK2 = TileCfg<128, 72, 16, 8, 1, 4>;   // warp 16x72
@@ -100,12 +103,15 @@ using NK9 = TileCfg<32, 72, 16, 2, 1, 4>;    // warp 16x72, 2 warps
 using NK10 = TileCfg<16, 72, 16, 1, 1, 4>;   // warp 16x72, 1 warp
 using NK11 = TileCfg<64, 64, 16, 2, 2, 4, 1>;   // NK4 with k-permuted 16-byte fragment loads
 using NK12 = TileCfg<64, 128, 16, 2, 2, 3, 1>;  // NK6 with k-permuted 16-byte fragment loads
+using NK13 = TileCfg<64, 128, 16, 2, 2, 4, 1>;  // 4 stages
+using NK14 = TileCfg<128, 64, 16, 2, 2, 4, 1>;  // warp 64x32
+using NK15 = TileCfg<128, 128, 16, 2, 4, 4, 1>; // NK0 with k-permuted fragments
 
 const char* kKnNames[] = {"128x128", "144x128", "72x128", "88x128", "64x64", "72x64",
-                          "128x64", "128x128k32", "144x64", "72x32", "72x16", "64x64kv", "64x128kv"};
+                          "128x64", "128x128k32", "144x64", "72x32", "72x16", "64x64kv", "64x128kv", "64x128np", "64x128np4", "128x128np"};
 const char* kNkNames[] = {"128x128", "128x144", "128x72", "128x88", "64x64", "64x72",
-                          "64x128", "128x128k32", "64x144", "32x72", "16x72", "64x64kv", "64x128kv"};
-constexpr int kNumCfg = 13;
+                          "64x128", "128x128k32", "64x144", "32x72", "16x72", "64x64kv", "64x128kv", "64x128kv4", "128x64kv", "128x128kv"};
+constexpr int kNumCfg = 16;
 
 }  // namespace
 
@@ -132,6 +138,9 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 10: return launch_cfg<KN10, BLayout::KN>(ctx, stream, p);
       case 11: return launch_cfg<KN11, BLayout::KN>(ctx, stream, p);
       case 12: return launch_cfg<KN12, BLayout::KN>(ctx, stream, p);
+      case 13: return launch_cfg<KN13, BLayout::KN>(ctx, stream, p);
+      case 14: return launch_cfg<KN14, BLayout::KN>(ctx, stream, p);
+      case 15: return launch_cfg<KN15, BLayout::KN>(ctx, stream, p);
     }
   } else {
     switch (cfg) {
@@ -148,6 +157,9 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 10: return launch_cfg<NK10, BLayout::NK>(ctx, stream, p);
       case 11: return launch_cfg<NK11, BLayout::NK>(ctx, stream, p);
       case 12: return launch_cfg<NK12, BLayout::NK>(ctx, stream, p);
+      case 13: return launch_cfg<NK13, BLayout::NK>(ctx, stream, p);
+      case 14: return launch_cfg<NK14, BLayout::NK>(ctx, stream, p);
+      case 15: return launch_cfg<NK15, BLayout::NK>(ctx, stream, p);
     }
   }
   set_error("bad GEMM configuration %d", cfg);
@@ -244,6 +256,9 @@ int gemm_autotune(fdiga_ctx* ctx, BLayout L, const GemmParams& p, int* best_cfg,
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     ms /= reps;
+    if (getenv("FDIGA_VERBOSE") && atoi(getenv("FDIGA_VERBOSE")) >= 2)
+      fprintf(stderr, "[fdiga] autotune %s M=%d N=%d K=%d inner=%lld: %-10s %8.2f us\n", L == BLayout::KN ? "KN" : "NK",
+              p.M, p.N, p.K, (long long)p.inner, gemm_config_name(L, c), 1e3 * ms);
     if (ms < best_t * 0.98f) {  // prefer the earlier (larger-tile) config on near ties
       best_t = ms;
       best = c;
