@@ -149,6 +149,14 @@ int fd_get_factors(const fd_plan* plan, int l, double* U, double* W, double* lam
 int fd_apply(fd_plan* plan, const double* r, double* s);
 /* Same, with HOST buffers r, s (copied in and out inside the call; synchronises). */
 int fd_apply_host(fd_plan* plan, const double* r_host, double* s_host);
+/* Streaming variant: enqueue H2D of r_host, the apply and D2H into s_host and return at once.  Consecutive
+ * calls alternate between two device staging buffers on dedicated copy streams, so the H2D of one call,
+ * the apply of the previous one and the D2H of the one before overlap (both PCIe directions and the
+ * SMs busy at once).  r_host / s_host must stay valid (and pinned, for real overlap) until fd_host_sync;
+ * a later call may reuse them only after the earlier results were consumed. */
+int fd_apply_host_async(fd_plan* plan, const double* r_host, double* s_host);
+/* Wait for every fd_apply_host_async of this plan. */
+int fd_host_sync(fd_plan* plan);
 /* Algorithmic flops of one apply: 4 N sum_l n_l (= 12 n^4 in 3D P:481, 8 n^3 in 2D P:464). */
 double fd_apply_flops(const fd_plan* plan);
 int fd_plan_destroy(fd_plan* plan);

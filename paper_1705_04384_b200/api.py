@@ -279,6 +279,18 @@ def fd_apply_host(plan, r_host, s_host):
     return s_host
 
 
+def fd_apply_host_async(plan, r_host, s_host):
+    """Streaming host-buffer apply (double-buffered, overlapped copies); complete with fd_host_sync."""
+    if r_host.dtype != np.float64 or s_host.dtype != np.float64 or r_host.size != plan.N or s_host.size != plan.N:
+        raise ValueError("fd_apply_host_async: float64 host arrays of the local length expected")
+    check(plan.ctx._lib.fd_apply_host_async(plan.handle, _dptr(r_host), _dptr(s_host)), "fd_apply_host_async")
+    return s_host
+
+
+def fd_host_sync(plan):
+    check(plan.ctx._lib.fd_host_sync(plan.handle), "fd_host_sync")
+
+
 def colloc_assemble(ctx, d, p, ne, geometry, geo_params=(), matrix_free=False, wind=0, wind_params=()):
     """The collocation operator A_C: stored tensor-window values (colloc_assemble) or, with
     matrix_free=True, the sum-factorised on-the-fly operator (colloc_matrix_free, 3D).  wind != 0: the

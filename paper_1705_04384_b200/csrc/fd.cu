@@ -35,6 +35,11 @@ struct fd_plan {
   double* lam_inner = nullptr;  // sum of the eigenvalues of directions 1..d-1 over the flattened inner index
   DevBuf t0, t1;                // ping-pong scratch
   DevBuf host_io;               // device staging for fd_apply_host
+  // fd_apply_host_async: two device staging buffers, copy streams and events (created on first use)
+  DevBuf aio[2];
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  int aslot = 0;
   int cfg[3] = {0, 0, 0};       // autotuned GEMM tile configuration per mode (fd_gemm.cu)
   float cfg_ms[3] = {0, 0, 0};
   // complex pairs: D_l has 2x2 blocks [[a, b], [-b, a]]; the divide becomes small block solves
@@ -862,6 +867,46 @@ int fd_apply_host(fd_plan* P, const double* r_host, double* s_host) {
   return FDIGA_OK;
 }
 
+int fd_apply_host_async(fd_plan* P, const double* r_host, double* s_host) {
+  FDIGA_CHECK(P && r_host && s_host, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  fdiga_ctx* ctx = P->ctx;
+  FDIGA_TRY(bind(ctx));
+  if (!P->s_h2d) {
+    FDIGA_CUDA(cudaStreamCreateWithFlags(&P->s_h2d, cudaStreamNonBlocking));
+    FDIGA_CUDA(cudaStreamCreateWithFlags(&P->s_d2h, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      FDIGA_CUDA(cudaEventCreateWithFlags(&P->ev_in[k], cudaEventDisableTiming));
+      FDIGA_CUDA(cudaEventCreateWithFlags(&P->ev_done[k], cudaEventDisableTiming));
+      FDIGA_CUDA(cudaEventCreateWithFlags(&P->ev_out[k], cudaEventDisableTiming));
+      FDIGA_CUDA(cudaEventRecord(P->ev_out[k], P->s_d2h));  // both slots start free
+    }
+  }
+  const int k = P->aslot;
+  P->aslot ^= 1;
+  FDIGA_TRY(P->aio[k].ensure(std::max<int64_t>(1, P->Nloc)));
+  double* buf = P->aio[k].p;
+  const size_t bytes = (size_t)P->Nloc * 8;
+  // H2D into slot k once its previous result left the device; apply on the context stream; D2H behind it
+  FDIGA_CUDA(cudaStreamWaitEvent(P->s_h2d, P->ev_out[k], 0));
+  FDIGA_CUDA(cudaMemcpyAsync(buf, r_host, bytes, cudaMemcpyHostToDevice, P->s_h2d));
+  FDIGA_CUDA(cudaEventRecord(P->ev_in[k], P->s_h2d));
+  FDIGA_CUDA(cudaStreamWaitEvent(ctx->stream, P->ev_in[k], 0));
+  FDIGA_TRY(fd_apply(P, buf, buf));
+  FDIGA_CUDA(cudaEventRecord(P->ev_done[k], ctx->stream));
+  FDIGA_CUDA(cudaStreamWaitEvent(P->s_d2h, P->ev_done[k], 0));
+  FDIGA_CUDA(cudaMemcpyAsync(s_host, buf, bytes, cudaMemcpyDeviceToHost, P->s_d2h));
+  FDIGA_CUDA(cudaEventRecord(P->ev_out[k], P->s_d2h));
+  return FDIGA_OK;
+}
+
+int fd_host_sync(fd_plan* P) {
+  FDIGA_CHECK(P, FDIGA_ERR_INVALID_ARG, "NULL plan");
+  FDIGA_TRY(bind(P->ctx));
+  if (P->s_d2h) FDIGA_CUDA(cudaStreamSynchronize(P->s_d2h));
+  FDIGA_CUDA(cudaStreamSynchronize(P->ctx->stream));
+  return FDIGA_OK;
+}
+
 double fd_apply_flops(const fd_plan* P) {
   if (!P) return 0;
   double s = 0;
@@ -886,6 +931,19 @@ int fd_plan_destroy(fd_plan* P) {
   P->t0.release();
   P->t1.release();
   P->host_io.release();
+  if (P->s_h2d) {
+    cudaStreamSynchronize(P->s_d2h);
+    cudaStreamSynchronize(P->s_h2d);
+    cudaStreamDestroy(P->s_h2d);
+    cudaStreamDestroy(P->s_d2h);
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(P->ev_in[k]);
+      cudaEventDestroy(P->ev_done[k]);
+      cudaEventDestroy(P->ev_out[k]);
+    }
+  }
+  P->aio[0].release();
+  P->aio[1].release();
   delete P;
   return FDIGA_OK;
 }

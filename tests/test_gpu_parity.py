@@ -547,3 +547,17 @@ def test_wq_solvers_match_oracle_counts(ctx, cfg):
     assert rep["converged"] and abs(rep["iters"] - ref["iters"]) <= 1
     rb = fd.bicgstab_solve(ctx, A, P, b, x)
     assert rb["converged"] and abs(rb["iters"] - ref["bicgstab_iters"]) <= 1.0
+
+
+def test_fd_apply_host_async_matches_sync(ctx):
+    ns = (30, 31, 32)
+    f, rng = _random_factors(ns, 21)
+    plan = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
+    N = int(np.prod(ns))
+    ins = [torch.from_numpy(rng.standard_normal(N)).pin_memory() for _ in range(5)]
+    outs = [torch.empty(N, dtype=torch.float64).pin_memory() for _ in range(5)]
+    for a, b in zip(ins, outs):
+        fd.fd_apply_host_async(plan, a.numpy(), b.numpy())
+    fd.fd_host_sync(plan)
+    for a, b in zip(ins, outs):
+        assert rel(b.numpy(), fastdiag.apply(f, a.numpy())) <= 1e-12
