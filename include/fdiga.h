@@ -14,7 +14,8 @@
  *     On nranks > 1 a vector argument holds only this rank's slab of the last index
  *     i_d in [begin, end) (fdiga_slab).
  *   - Matrices passed from the host are row-major FP64, copied before the call returns
- *     (the caller keeps ownership).  Handles own all device memory they allocate.
+ *     (the caller keeps ownership).  Handles own all device memory they allocate; plans and operators
+ *     must be destroyed before the context they were created on.
  *   - Device vector arguments are caller-owned device pointers (e.g. torch data_ptr()).
  *   - Stream semantics: fd_apply and stencil_matvec are asynchronous on the context's stream;
  *     fd_setup*, colloc_assemble, stencil_create and gmres_solve synchronise before returning.

@@ -5,6 +5,7 @@ vectors as torch float64 CUDA tensors (their data_ptr is passed through), and ev
 hot path runs in the library's kernels.  torch provides device memory and streams only.
 """
 import ctypes as C
+import weakref
 
 import numpy as np
 
@@ -111,6 +112,7 @@ class Context:
         self.handle = h
         self.device = device
         self.nranks, self.rank = int(nranks), int(rank)
+        self._children = weakref.WeakSet()  # plans / operators: destroyed before the context (C ABI rule)
 
     def slab(self, n_last):
         b, e = C.c_int64(), C.c_int64()
@@ -122,6 +124,8 @@ class Context:
 
     def close(self):
         if self.handle:
+            for child in list(self._children):
+                child.close()
             self._lib.fdiga_ctx_destroy(self.handle)
             self.handle = None
 
@@ -137,6 +141,7 @@ class FDPlan:
 
     def __init__(self, ctx, handle, ns):
         self.ctx, self.handle, self.n = ctx, handle, list(ns)
+        ctx._children.add(self)
         self.N_global = int(np.prod(self.n))
         self.slab = ctx.slab(self.n[-1])           # this rank's planes of the last axis
         self.N = (self.slab[1] - self.slab[0]) * (self.N_global // self.n[-1])   # local vector length
@@ -154,7 +159,8 @@ class FDPlan:
 
     def close(self):
         if self.handle:
-            self.ctx._lib.fd_plan_destroy(self.handle)
+            if self.ctx.handle:  # a closed context already destroyed its children
+                self.ctx._lib.fd_plan_destroy(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -169,6 +175,7 @@ class Stencil:
 
     def __init__(self, ctx, handle):
         self.ctx, self.handle = ctx, handle
+        ctx._children.add(self)
         nnz = C.c_int64()
         n = (C.c_int64 * 3)(1, 1, 1)
         check(ctx._lib.stencil_info(handle, C.byref(nnz), n, None, None), "stencil_info")
@@ -193,7 +200,8 @@ class Stencil:
 
     def close(self):
         if self.handle:
-            self.ctx._lib.stencil_destroy(self.handle)
+            if self.ctx.handle:
+                self.ctx._lib.stencil_destroy(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -382,7 +390,7 @@ def gmres_solve(ctx, A, P, b, x, m=30, rtol=1e-8, max_iters=1000, orth=ORTH_CGS2
         rep.history_cap = max_iters
     st = ctx._lib.gmres_solve(ctx.handle, A.handle, P.handle if P is not None else None, _devptr(b, A.N),
                               _devptr(x, A.N), C.byref(opts), C.byref(rep))
-    if st != 0 and (raise_on_nonconvergence or st != -8):
+    if st != 0 and (raise_on_nonconvergence or st not in (-8, -9)):  # NOT_CONVERGED / BREAKDOWN reported
         check(st, "gmres_solve")
     out = dict(iters=rep.iters, restarts=rep.restarts, converged=bool(rep.converged), reorth=rep.reorth,
                rel_res_true=rep.rel_res_true, rel_res_implicit=rep.rel_res_implicit, t_total_ms=rep.t_total_ms,

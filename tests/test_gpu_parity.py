@@ -561,3 +561,87 @@ def test_fd_apply_host_async_matches_sync(ctx):
     fd.fd_host_sync(plan)
     for a, b in zip(ins, outs):
         assert rel(b.numpy(), fastdiag.apply(f, a.numpy())) <= 1e-12
+
+
+# ----------------------------------------------------------------------------- degenerate and edge cases
+
+def _small_system(ctx):
+    c = get_config(2)
+    A = fd.colloc_assemble(ctx, 2, 3, 12, c.geometry, c.geo_params)
+    M, K = fd.colloc_1d_factors(3, 12)
+    P = fd.fd_setup(ctx, [M] * 2, [K] * 2)
+    return A, P
+
+
+def test_solvers_zero_rhs(ctx):
+    A, P = _small_system(ctx)
+    b = torch.zeros(A.N, dtype=torch.float64, device=DEV)
+    x = torch.full_like(b, 7.0)
+    rep = fd.gmres_solve(ctx, A, P, b, x)
+    assert rep["converged"] and rep["iters"] == 0 and float(x.abs().max()) == 0.0
+    x.fill_(7.0)
+    rep = fd.bicgstab_solve(ctx, A, P, b, x)
+    assert rep["converged"] and rep["iters"] == 0.0 and float(x.abs().max()) == 0.0
+
+
+def test_gmres_initial_guess_is_solution(ctx):
+    A, P = _small_system(ctx)
+    b = gpu(rhs(2, A.N, rep=9))
+    x = torch.empty_like(b)
+    fd.gmres_solve(ctx, A, P, b, x, rtol=1e-12)
+    rep = fd.gmres_solve(ctx, A, P, b, x, rtol=1e-8, use_x0=True)
+    assert rep["converged"] and rep["iters"] == 0
+    rep = fd.bicgstab_solve(ctx, A, P, b, x, rtol=1e-8, use_x0=True)
+    assert rep["converged"] and rep["iters"] == 0.0
+
+
+def test_gmres_restart_length_one_matches_oracle(ctx):
+    c = get_config(2)
+    A, P = _small_system(ctx)
+    disc = assembly.Discretisation(2, 3, 12, c.geometry, c.geo_params)
+    f = fastdiag.setup([disc.M] * 2, [disc.K] * 2)
+    bh = rhs(2, disc.N, rep=4)
+    x = torch.empty(disc.N, dtype=torch.float64, device=DEV)
+    P2 = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
+    rep = fd.gmres_solve(ctx, A, P2, gpu(bh), x, m=1, max_iters=3000)
+    xo, repo = krylov.gmres(disc.matvec, bh, precond=lambda v: fastdiag.apply(f, v), m=1, max_iters=3000)
+    assert rep["converged"] and repo["converged"]
+    assert abs(rep["iters"] - repo["iters"]) <= max(2, repo["iters"] // 20)
+    assert rep["restarts"] == rep["iters"]  # GMRES(1): one step per cycle
+
+
+def test_solvers_report_breakdown_on_nan(ctx):
+    A, P = _small_system(ctx)
+    bh = rhs(2, A.N)
+    bh[5] = np.nan
+    b = gpu(bh)
+    x = torch.empty_like(b)
+    rep = fd.gmres_solve(ctx, A, P, b, x, raise_on_nonconvergence=False)
+    assert rep["status"] == -9 and not rep["converged"]
+    rep = fd.bicgstab_solve(ctx, A, P, b, x, raise_on_failure=False)
+    assert rep["status"] == -9 and rep["breakdown"]
+
+
+def test_api_argument_errors(ctx):
+    A, P = _small_system(ctx)
+    x = torch.zeros(A.N, dtype=torch.float64, device=DEV)
+    with pytest.raises(fd.FdigaError) as e:
+        fd.stencil_matvec(A, x, x)          # aliasing is rejected by the library
+    assert e.value.status == -1
+    with pytest.raises(ValueError):
+        fd.fd_apply(P, x[:-1], x[:-1])      # wrong length (binding check)
+    with pytest.raises(TypeError):
+        fd.fd_apply(P, x.float(), x.float())
+    with pytest.raises(fd.FdigaError):
+        fd.gmres_solve(ctx, A, P, x, torch.zeros_like(x), m=40)   # m > 31
+
+
+def test_fd_apply_large_2d_ragged(ctx):
+    # a large, ragged 2D apply (n = 3001 and 2049: 6.1M DOF) against the oracle's mode products
+    ns = (3001, 2049)
+    f, rng = _random_factors(ns, 77)
+    plan = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
+    r = rng.standard_normal(int(np.prod(ns)))
+    s = torch.empty(r.size, dtype=torch.float64, device=DEV)
+    fd.fd_apply(plan, gpu(r), s)
+    assert rel(host(s), fastdiag.apply(f, r)) <= 1e-12

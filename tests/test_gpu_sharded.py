@@ -306,3 +306,30 @@ def test_sharded_wq_matvec():
 
     y = np.concatenate(run_ranks(3, work))
     assert rel(y, Ao @ x) <= 1e-12
+
+
+def test_sharded_gmres_more_ranks_than_planes():
+    # cfg3 geometry with ne = 2 (n = 3 planes) over 5 ranks: two ranks own no rows but take part in
+    # every collective
+    _, M, K, _ = splines.colloc_1d(2, 3)
+    n = M.shape[0]
+    b = rhs(3, n ** 3, rep=2)
+
+    def work(ctx, rank):
+        A = fd.colloc_assemble(ctx, 3, 3, 2, 2, (0.1,))
+        P = fd.fd_setup(ctx, [M] * 3, [K] * 3)
+        lo, hi = slab_rows(n, 5, rank, n * n)
+        bt = torch.from_numpy(b[lo:hi].copy()).to(DEV)
+        x = torch.empty_like(bt)
+        rep = fd.gmres_solve(ctx, A, P, bt, x, rtol=1e-10)
+        torch.cuda.current_stream().synchronize()
+        out = (rep, x.cpu().numpy())
+        P.close()
+        A.close()
+        return out
+
+    res = run_ranks(5, work)
+    assert all(r[0]["converged"] and r[0]["iters"] == res[0][0]["iters"] for r in res)
+    disc = assembly.Discretisation(3, 3, 2, 2, (0.1,))
+    x = np.concatenate([r[1] for r in res])
+    assert np.linalg.norm(b - disc.matvec(x)) / np.linalg.norm(b) <= 1e-9
