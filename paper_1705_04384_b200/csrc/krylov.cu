@@ -54,7 +54,7 @@ struct GmState {
 // whole number of 16-byte units; elements >= N are masked.
 constexpr int SC = RT;  // elements per chunk (one per thread)
 
-enum { GS_DOT = 0, GS_UPD_DOT = 1, GS_UPD = 2 };
+enum { GS_DOT = 0, GS_UPD_DOT = 1, GS_UPD = 2, GS_UPD_SCALE = 3 };
 
 template <int K>
 __host__ __device__ constexpr int gs_stages() {
@@ -67,10 +67,11 @@ __host__ __device__ constexpr size_t gs_smem_bytes() {
 }
 
 // acc[i] (i < K) = V_i . w or V_i . w' and acc[K] = w.w or w'.w' with w' = w - V hs (GS_UPD_DOT / GS_UPD,
-// w' stored back to global)
+// w' stored back to global); GS_UPD_SCALE stores scale * w' into `out` instead (no dots)
 template <int K, int MODE>
 __device__ __forceinline__ void gs_stream(const double* __restrict__ V, int64_t ldv, double* w, int64_t N,
-                                          const double* hs, double (&acc)[K + 1]) {
+                                          const double* hs, double (&acc)[K + 1], double* out = nullptr,
+                                          double scale = 1.0) {
   constexpr int S = gs_stages<K>();
   extern __shared__ __align__(128) double gsm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(gsm + (size_t)S * (K + 1) * SC);
@@ -109,9 +110,12 @@ __device__ __forceinline__ void gs_stream(const double* __restrict__ V, int64_t 
       if (MODE != GS_DOT) {
 #pragma unroll
         for (int i = 0; i < K; ++i) wv = fma(-hs[i], buf[i * SC + tid], wv);
-        w[e] = wv;
+        if (MODE == GS_UPD_SCALE)
+          out[e] = scale * wv;
+        else
+          w[e] = wv;
       }
-      if (MODE != GS_UPD) {
+      if (MODE != GS_UPD && MODE != GS_UPD_SCALE) {
 #pragma unroll
         for (int i = 0; i < K; ++i) acc[i] = fma(buf[i * SC + tid], wv, acc[i]);
       }
@@ -140,17 +144,49 @@ __global__ void __launch_bounds__(RT) arnoldi_pass1(const double* __restrict__ V
 }
 
 // pass 2: w <- w - V h1 ; h2[i] = V_i . w (new w), h2[k] = ||w||^2 (V read once, from shared memory)
+__device__ void arnoldi_close_step(GmState* st, int j, int m, double wn2, double* hist, int hist_cap);
+
+// close == 1 (CGS2, single rank): the last block also closes step j with the Pythagorean norm
+// ||w''||^2 = ||w'||^2 - ||h2||^2 of the second projection (h2 is O(eps kappa) small after the first one,
+// so the subtraction loses nothing), which lets pass 3 write v_{j+1} directly without a reduction.
 template <int K>
 __global__ void __launch_bounds__(RT) arnoldi_pass2(const double* __restrict__ V, int64_t ldv, int /*k (= K)*/,
                                                     double* __restrict__ w, int64_t N, double* part, GmState* st,
-                                                    double* hout) {
+                                                    double* hout, int j, int m, double* hist, int hist_cap,
+                                                    int close) {
   if (st->stop) return;
   __shared__ double hs[KMAX];
   if (threadIdx.x < K) hs[threadIdx.x] = st->h1[threadIdx.x];
   __syncthreads();
   double acc[K + 1];
   gs_stream<K, GS_UPD_DOT>(V, ldv, w, N, hs, acc);
-  reduce_last<K + 1>(acc, K + 1, part, &st->counter[1], hout);
+  if (reduce_last<K + 1>(acc, K + 1, part, &st->counter[1], hout) && close && threadIdx.x == 0) {
+    double wn2 = hout[K];
+    for (int i = 0; i < K; ++i) wn2 -= hout[i] * hout[i];
+    arnoldi_close_step(st, j, m, wn2, hist, hist_cap);
+  }
+}
+
+// sharded CGS2: close step j from the all-reduced h2 (Pythagorean norm, as above)
+__global__ void close_step_pyth_kernel(GmState* st, int j, int m, double* hist, int hist_cap) {
+  if (st->stop) return;
+  const int k = j + 1;
+  double wn2 = st->h2[k];
+  for (int i = 0; i < k; ++i) wn2 -= st->h2[i] * st->h2[i];
+  arnoldi_close_step(st, j, m, wn2, hist, hist_cap);
+}
+
+// CGS2 pass 3: v_{j+1} = (w' - V h2) / h_{j+1,j} written straight into the basis (no reduction)
+template <int K>
+__global__ void __launch_bounds__(RT) arnoldi_pass3n(const double* __restrict__ V, int64_t ldv,
+                                                     double* __restrict__ w, int64_t N, GmState* st,
+                                                     double* vnext) {
+  if (st->stop) return;
+  __shared__ double hs[KMAX];
+  if (threadIdx.x < K) hs[threadIdx.x] = st->h2[threadIdx.x];
+  __syncthreads();
+  double acc[K + 1];
+  gs_stream<K, GS_UPD_SCALE>(V, ldv, w, N, hs, acc, vnext, st->invh);
 }
 
 // Givens rotations / convergence test for step j (one thread), once h = h1 + h2 and ||w''||^2 are known.
@@ -355,6 +391,7 @@ int gs_grid(fdiga_ctx* ctx, int64_t N, size_t* smem) {
     FDIGA_CUDA(cudaFuncSetAttribute(arnoldi_pass1<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
     FDIGA_CUDA(cudaFuncSetAttribute(arnoldi_pass2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
     FDIGA_CUDA(cudaFuncSetAttribute(arnoldi_pass3<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
+    FDIGA_CUDA(cudaFuncSetAttribute(arnoldi_pass3n<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
     attr = true;
   }
   const int per_sm = std::max(1, std::min(8, (int)((227 * 1024) / (*smem + 1024))));
@@ -386,11 +423,20 @@ int passes_k(fdiga_ctx* ctx, const Ws& W, int j, int m, int hist_cap) {
   count_launch(ctx);
   if (W.sh) FDIGA_TRY(comm_allreduce(ctx, st->h1l, st->h1, K + 1));
   if (W.orth == FDIGA_ORTH_CGS2) {
-    // classical Gram-Schmidt twice: pass 2 fuses the update with the second projection
-    arnoldi_pass2<K><<<grid, RT, smem, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, W.sh ? st->h2l : st->h2);
+    // classical Gram-Schmidt twice: pass 2 fuses the update with the second projection and (Pythagorean
+    // norm) closes the step; pass 3 writes the normalised v_{j+1}.  Two reductions per step.
+    arnoldi_pass2<K><<<grid, RT, smem, ctx->stream>>>(W.V, W.ldv, K, W.w, W.N, W.part, st, W.sh ? st->h2l : st->h2,
+                                                      j, m, W.hist, hist_cap, W.sh ? 0 : 1);
     count_launch(ctx);
-    if (W.sh) FDIGA_TRY(comm_allreduce(ctx, st->h2l, st->h2, K + 1));
-    return pass3_k<K>(ctx, W, j, m, hist_cap, P3_CLOSE);
+    if (W.sh) {
+      FDIGA_TRY(comm_allreduce(ctx, st->h2l, st->h2, K + 1));
+      close_step_pyth_kernel<<<1, 1, 0, ctx->stream>>>(st, j, m, W.hist, hist_cap);
+      count_launch(ctx);
+    }
+    arnoldi_pass3n<K><<<grid, RT, smem, ctx->stream>>>(W.V, W.ldv, W.w, W.N, st, W.V + (int64_t)(j + 1) * W.ldv);
+    count_launch(ctx);
+    FDIGA_CUDA(cudaGetLastError());
+    return FDIGA_OK;
   }
   // classical Gram-Schmidt with DGKS re-orthogonalisation: update, test, and only when the test fails a
   // second projection + update (device flag; the launches are no-ops otherwise)
@@ -434,8 +480,10 @@ int enqueue_cycle(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const Ws& W, int
     }
     const int k = j + 1;
     FDIGA_TRY(launch_passes(ctx, W, k, j, m, hist_cap));
-    next_basis_kernel<<<W.nblk, RT, 0, ctx->stream>>>(W.w, W.V + (int64_t)(j + 1) * W.ldv, W.N, W.st);
-    count_launch(ctx);
+    if (W.orth != FDIGA_ORTH_CGS2) {  // CGS2's pass 3 already wrote v_{j+1}
+      next_basis_kernel<<<W.nblk, RT, 0, ctx->stream>>>(W.w, W.V + (int64_t)(j + 1) * W.ldv, W.N, W.st);
+      count_launch(ctx);
+    }
     FDIGA_CUDA(cudaGetLastError());
   }
   return FDIGA_OK;
