@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
   // ---- epilogue: optional eigenvalue-sum divide (eq:FD3D diagonal term), store
   const bool c_vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((p.ldc & 1) == 0) &&
                      (BL == BLayout::NK || ((p.inner & 1) == 0 && (p.bstride & 1) == 0));
-  if (T::NP) {
+  if constexpr (T::NP != 0) {
     // accumulator (i, j, h) is physical column warp_n WTN + (2 lc + h) NJ + j: pairs (j, j + 1) adjacent
 #pragma unroll
     for (int h = 0; h < 2; ++h)
@@ -323,8 +323,7 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
           }
         }
       }
-    return;
-  }
+  } else {
 #pragma unroll
   for (int j = 0; j < T::NJ; ++j) {
     const int col = n0 + warp_n * T::WTN + j * 8 + 2 * lc;
@@ -367,6 +366,7 @@ __global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) 
       }
     }
   }
+  }  // NP == 0
 }
 
 }  // namespace fdiga

@@ -79,11 +79,12 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
   __shared__ int lo_s[2][3], bx_s[2][3];
   int buf = 0;
   if (blockIdx.x < ntiles) mf_issue_box(A, blockIdx.x, xs, lo_s[0], bx_s[0]);
-  const int64_t n1 = A.n1, n12 = A.n1 * A.n2;
+  const int64_t n12 = A.n1 * A.n2;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
   const int tl = (int)tile, t1 = (int)A.t1, t2 = (int)A.t2;
   const int q1 = tl % t1, q2 = (tl / t1) % t2, q3 = tl / (t1 * t2);
-  const int64_t a1 = q1 * T, a2 = q2 * T, a3 = A.o + q3 * T;  // first row of the tile (global)
+  const int a1 = q1 * T, a2 = q2 * T, a3 = (int)A.o + q3 * T;  // first row of the tile (global; 32-bit)
+  const int n1i = (int)A.n1, n2i = (int)A.n2, n3i = (int)A.n3, Wt = A.W;
   const int m1 = (int)(A.n1 - a1 < T ? A.n1 - a1 : T), m2 = (int)(A.n2 - a2 < T ? A.n2 - a2 : T),
             m3 = (int)(A.e - a3 < T ? A.e - a3 : T);
   cp_async_wait<0>();
@@ -94,15 +95,15 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
   {
     const int i1 = tid & (T - 1);
     if (i1 < m1) {
-      const int64_t g1 = a1 + i1;
+      const int g1 = a1 + i1;
       const int w = __ldg(A.w1 + g1), o = __ldg(A.st1 + g1) - lo[0];
       double d0[WM], d1[WM], d2[WM];
 #pragma unroll
       for (int c = 0; c < WM; ++c) {
         const bool on = c < w;
-        d0[c] = on ? __ldg(A.tab1 + (0 * n1 + g1) * A.W + c) : 0.0;
-        d1[c] = on ? __ldg(A.tab1 + (1 * n1 + g1) * A.W + c) : 0.0;
-        d2[c] = on ? __ldg(A.tab1 + (2 * n1 + g1) * A.W + c) : 0.0;
+        d0[c] = on ? __ldg(A.tab1 + (0 * n1i + g1) * Wt + c) : 0.0;
+        d1[c] = on ? __ldg(A.tab1 + (1 * n1i + g1) * Wt + c) : 0.0;
+        d2[c] = on ? __ldg(A.tab1 + (2 * n1i + g1) * Wt + c) : 0.0;
       }
       const int npair = b3 * b2;
       double* o0 = x1 + (0 * T + i1) * ps1;
@@ -144,15 +145,15 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
   {
     const int i1 = tid & (T - 1), i2 = (tid / T) & (T - 1), jg = tid / (T * T);
     if (i1 < m1 && i2 < m2) {
-      const int64_t g2 = a2 + i2;
+      const int g2 = a2 + i2;
       const int w = __ldg(A.w2 + g2), o = __ldg(A.st2 + g2) - lo[1];
       double d0[WM], d1[WM], d2[WM];
 #pragma unroll
       for (int c = 0; c < WM; ++c) {
         const bool on = c < w;
-        d0[c] = on ? __ldg(A.tab2 + (0 * A.n2 + g2) * A.W + c) : 0.0;
-        d1[c] = on ? __ldg(A.tab2 + (1 * A.n2 + g2) * A.W + c) : 0.0;
-        d2[c] = on ? __ldg(A.tab2 + (2 * A.n2 + g2) * A.W + c) : 0.0;
+        d0[c] = on ? __ldg(A.tab2 + (0 * n2i + g2) * Wt + c) : 0.0;
+        d1[c] = on ? __ldg(A.tab2 + (1 * n2i + g2) * Wt + c) : 0.0;
+        d2[c] = on ? __ldg(A.tab2 + (2 * n2i + g2) * Wt + c) : 0.0;
       }
       const double* in0 = x1 + (0 * T + i1) * ps1;
       const double* in1 = x1 + (1 * T + i1) * ps1;
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
     const int pix = tid & (T * T - 1), i1 = pix % T, i2 = pix / T;  // i1 fastest: coalesced y stores
     if (i1 < m1 && i2 < m2) {
       const int st = T * T * pb3;
-      const int64_t g1 = a1 + i1, g2 = a2 + i2;
+      const int g1 = a1 + i1, g2 = a2 + i2;
       const double xi1 = __ldg(A.tau1 + g1);
       double sn[3], cs[3];
       sn[0] = __ldg(A.trig1 + 2 * g1);
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
         colloc_coeffs<3>(geometry_jh(A.geo, xi1, sn, cs), G, beta, A.geo.wind ? wv : nullptr);
       }
       for (int i3 = tid / (T * T); i3 < m3; i3 += NT / (T * T)) {
-        const int64_t g3 = a3 + i3;
+        const int g3 = a3 + i3;
         const int w = __ldg(A.w3 + g3), o = __ldg(A.st3 + g3) - lo[2];
         double z[9], f0[WM], f1[WM], f2[WM];
 #pragma unroll
@@ -216,9 +217,9 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
 #pragma unroll
         for (int c = 0; c < WM; ++c) {
           const bool on = c < w;
-          f0[c] = on ? __ldg(A.tab3 + (0 * A.n3 + g3) * A.W + c) : 0.0;
-          f1[c] = on ? __ldg(A.tab3 + (1 * A.n3 + g3) * A.W + c) : 0.0;
-          f2[c] = on ? __ldg(A.tab3 + (2 * A.n3 + g3) * A.W + c) : 0.0;
+          f0[c] = on ? __ldg(A.tab3 + (0 * n3i + g3) * Wt + c) : 0.0;
+          f1[c] = on ? __ldg(A.tab3 + (1 * n3i + g3) * Wt + c) : 0.0;
+          f2[c] = on ? __ldg(A.tab3 + (2 * n3i + g3) * Wt + c) : 0.0;
         }
         const double* in = x12 + pix * pb3 + o;
 #pragma unroll
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
         }
         double yv = beta[2] * z[0] - G[2][2] * z[1] + beta[1] * z[2] - 2.0 * G[1][2] * z[3] - G[1][1] * z[4] +
                     beta[0] * z[5] - 2.0 * G[0][2] * z[6] - 2.0 * G[0][1] * z[7] - G[0][0] * z[8];
-        A.y[(g3 - A.o) * n12 + g2 * n1 + g1] = yv;
+        A.y[(int64_t)(g3 - (int)A.o) * n12 + g2 * n1i + g1] = yv;
       }
     }
   }
