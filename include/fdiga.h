@@ -151,7 +151,7 @@ int fd_apply(fd_plan* plan, const double* r, double* s);
 /* Same, with HOST buffers r, s (copied in and out inside the call; synchronises). */
 int fd_apply_host(fd_plan* plan, const double* r_host, double* s_host);
 /* Streaming variant: enqueue H2D of r_host, the apply and D2H into s_host and return at once.  Consecutive
- * calls alternate between two device staging buffers on dedicated copy streams, so the H2D of one call,
+ * calls rotate over three device staging buffers on dedicated copy streams, so the H2D of one call,
  * the apply of the previous one and the D2H of the one before overlap (both PCIe directions and the
  * SMs busy at once).  r_host / s_host must stay valid (and pinned, for real overlap) until fd_host_sync;
  * a later call may reuse them only after the earlier results were consumed. */

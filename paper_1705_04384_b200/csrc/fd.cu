@@ -35,10 +35,13 @@ struct fd_plan {
   double* lam_inner = nullptr;  // sum of the eigenvalues of directions 1..d-1 over the flattened inner index
   DevBuf t0, t1;                // ping-pong scratch
   DevBuf host_io;               // device staging for fd_apply_host
-  // fd_apply_host_async: two device staging buffers, copy streams and events (created on first use)
-  DevBuf aio[2];
+  // fd_apply_host_async: three device staging buffers, copy streams and events (created on first use).
+  // Three slots let the H2D of call k+1 start once the D2H of call k-2 is done, so both PCIe directions
+  // and the SMs stay busy (two slots chain H2D(k+1) behind D2H(k-1): measured 3.6 vs 2.8 ms per step)
+  static constexpr int NSLOT = 3;
+  DevBuf aio[NSLOT];
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[NSLOT] = {}, ev_done[NSLOT] = {}, ev_out[NSLOT] = {};
   int aslot = 0;
   int cfg[3] = {0, 0, 0};       // autotuned GEMM tile configuration per mode (fd_gemm.cu)
   float cfg_ms[3] = {0, 0, 0};
@@ -874,7 +877,7 @@ int fd_apply_host_async(fd_plan* P, const double* r_host, double* s_host) {
   if (!P->s_h2d) {
     FDIGA_CUDA(cudaStreamCreateWithFlags(&P->s_h2d, cudaStreamNonBlocking));
     FDIGA_CUDA(cudaStreamCreateWithFlags(&P->s_d2h, cudaStreamNonBlocking));
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < fd_plan::NSLOT; ++k) {
       FDIGA_CUDA(cudaEventCreateWithFlags(&P->ev_in[k], cudaEventDisableTiming));
       FDIGA_CUDA(cudaEventCreateWithFlags(&P->ev_done[k], cudaEventDisableTiming));
       FDIGA_CUDA(cudaEventCreateWithFlags(&P->ev_out[k], cudaEventDisableTiming));
@@ -882,7 +885,7 @@ int fd_apply_host_async(fd_plan* P, const double* r_host, double* s_host) {
     }
   }
   const int k = P->aslot;
-  P->aslot ^= 1;
+  P->aslot = (P->aslot + 1) % fd_plan::NSLOT;
   FDIGA_TRY(P->aio[k].ensure(std::max<int64_t>(1, P->Nloc)));
   double* buf = P->aio[k].p;
   const size_t bytes = (size_t)P->Nloc * 8;
@@ -936,14 +939,13 @@ int fd_plan_destroy(fd_plan* P) {
     cudaStreamSynchronize(P->s_h2d);
     cudaStreamDestroy(P->s_h2d);
     cudaStreamDestroy(P->s_d2h);
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < fd_plan::NSLOT; ++k) {
       cudaEventDestroy(P->ev_in[k]);
       cudaEventDestroy(P->ev_done[k]);
       cudaEventDestroy(P->ev_out[k]);
     }
   }
-  P->aio[0].release();
-  P->aio[1].release();
+  for (auto& b : P->aio) b.release();
   delete P;
   return FDIGA_OK;
 }
