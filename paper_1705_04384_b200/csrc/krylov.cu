@@ -54,7 +54,7 @@ struct GmState {
 // whole number of 16-byte units; elements >= N are masked.
 constexpr int SC = RT;  // elements per chunk (one per thread)
 
-enum { GS_DOT = 0, GS_UPD_DOT = 1, GS_UPD = 2, GS_UPD_SCALE = 3 };
+enum { GS_DOT = 0, GS_UPD_DOT = 1, GS_UPD = 2, GS_UPD_SCALE = 3, GS_LINCOMB = 4 };
 
 template <int K>
 __host__ __device__ constexpr int gs_stages() {
@@ -105,7 +105,12 @@ __device__ __forceinline__ void gs_stream(const double* __restrict__ V, int64_t 
     mbar_wait(&full[s], (uint32_t)((it / S) & 1));
     const double* buf = gsm + (size_t)s * (K + 1) * SC;
     const int64_t e = c * SC + tid;
-    if (e < N) {
+    if (e < N && MODE == GS_LINCOMB) {  // out = sum_i hs[i] V_i
+      double sacc = 0.0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) sacc = fma(hs[i], buf[i * SC + tid], sacc);
+      out[e] = sacc;
+    } else if (e < N) {
       double wv = buf[K * SC + tid];
       if (MODE != GS_DOT) {
 #pragma unroll
@@ -174,6 +179,17 @@ __global__ void close_step_pyth_kernel(GmState* st, int j, int m, double* hist, 
   double wn2 = st->h2[k];
   for (int i = 0; i < k; ++i) wn2 -= st->h2[i] * st->h2[i];
   arnoldi_close_step(st, j, m, wn2, hist, hist_cap);
+}
+
+// cycle close: out = sum_{i < K} y_i V_i, streamed like the Gram-Schmidt passes (w slot: row 0 again)
+template <int K>
+__global__ void __launch_bounds__(RT) lincomb_stream(const double* __restrict__ V, int64_t ldv,
+                                                     double* __restrict__ out, int64_t N, const GmState* st) {
+  __shared__ double hs[KMAX];
+  if (threadIdx.x < K) hs[threadIdx.x] = st->y[threadIdx.x];
+  __syncthreads();
+  double acc[K + 1];
+  gs_stream<K, GS_LINCOMB>(V, ldv, const_cast<double*>(V), N, hs, acc, out, 1.0);
 }
 
 // CGS2 pass 3: v_{j+1} = (w' - V h2) / h_{j+1,j} written straight into the basis (no reduction)
@@ -392,6 +408,7 @@ int gs_grid(fdiga_ctx* ctx, int64_t N, size_t* smem) {
     FDIGA_CUDA(cudaFuncSetAttribute(arnoldi_pass2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
     FDIGA_CUDA(cudaFuncSetAttribute(arnoldi_pass3<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
     FDIGA_CUDA(cudaFuncSetAttribute(arnoldi_pass3n<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
+    FDIGA_CUDA(cudaFuncSetAttribute(lincomb_stream<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
     attr = true;
   }
   const int per_sm = std::max(1, std::min(8, (int)((227 * 1024) / (*smem + 1024))));
@@ -445,6 +462,35 @@ int passes_k(fdiga_ctx* ctx, const Ws& W, int j, int m, int hist_cap) {
   count_launch(ctx);
   if (W.sh) FDIGA_TRY(comm_allreduce(ctx, st->h2l, st->h2, K + 1));
   return pass3_k<K>(ctx, W, j, m, hist_cap, P3_CLOSE_IF_REORTH);
+}
+
+template <int K>
+int lincomb_k(fdiga_ctx* ctx, const Ws& W, double* out) {
+  size_t smem = 0;
+  const int grid = gs_grid<K>(ctx, W.N, &smem);
+  lincomb_stream<K><<<grid, RT, smem, ctx->stream>>>(W.V, W.ldv, out, W.N, W.st);
+  count_launch(ctx);
+  FDIGA_CUDA(cudaGetLastError());
+  return FDIGA_OK;
+}
+
+int launch_lincomb(fdiga_ctx* ctx, const Ws& W, int k, double* out) {
+  switch (k) {
+#define FDIGA_K(K) \
+  case K:          \
+    return lincomb_k<K>(ctx, W, out);
+    FDIGA_K(1) FDIGA_K(2) FDIGA_K(3) FDIGA_K(4) FDIGA_K(5) FDIGA_K(6) FDIGA_K(7) FDIGA_K(8)
+    FDIGA_K(9) FDIGA_K(10) FDIGA_K(11) FDIGA_K(12) FDIGA_K(13) FDIGA_K(14) FDIGA_K(15) FDIGA_K(16)
+    FDIGA_K(17) FDIGA_K(18) FDIGA_K(19) FDIGA_K(20) FDIGA_K(21) FDIGA_K(22) FDIGA_K(23) FDIGA_K(24)
+    FDIGA_K(25) FDIGA_K(26) FDIGA_K(27) FDIGA_K(28) FDIGA_K(29) FDIGA_K(30) FDIGA_K(31)
+#undef FDIGA_K
+    default:
+      break;
+  }
+  lincomb_kernel<<<W.nblk, RT, 0, ctx->stream>>>(W.V, W.ldv, out, W.N, W.st);  // k = 0 or out of range
+  count_launch(ctx);
+  FDIGA_CUDA(cudaGetLastError());
+  return FDIGA_OK;
 }
 
 // The three CGS2 passes of step j with k = j + 1 basis vectors (one instantiation per k: fully
@@ -647,8 +693,14 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
       FDIGA_TRY(enqueue_cycle(ctx, A, P, W, m, hist_cap));  // loopback transport: not capturable
     }
     solve_y_kernel<<<1, 1, 0, st>>>(W.st);
-    lincomb_kernel<<<W.nblk, RT, 0, st>>>(W.V, W.ldv, W.w, W.N, W.st);
-    count_launch(ctx, 2);
+    count_launch(ctx);
+    // the cycle's basis size k is decided on the device: read it (one small copy per cycle) so the
+    // combination x += P^{-1}(V y) streams exactly k rows with the TMA-fed kernel
+    FDIGA_CUDA(cudaMemcpyAsync(ctx->pinned, &W.st->k, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FDIGA_CUDA(cudaStreamSynchronize(st));
+    int kcyc = 0;
+    std::memcpy(&kcyc, ctx->pinned, sizeof(int));
+    FDIGA_TRY(launch_lincomb(ctx, W, kcyc, W.w));
     FDIGA_CUDA(cudaGetLastError());
     if (P) {
       FDIGA_TRY(fd_apply(P, W.w, W.z));
