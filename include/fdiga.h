@@ -221,15 +221,19 @@ int colloc_1d_convection(int p, int64_t ne, const double* wt, double* H);
 
 /* -------------------------------------------------------------------- GMRES ---- */
 
-enum { FDIGA_ORTH_CGS_DGKS = 0, FDIGA_ORTH_CGS2 = 1 };
+enum { FDIGA_ORTH_CGS_DGKS = 0, FDIGA_ORTH_CGS2 = 1, FDIGA_ORTH_DCGS2 = 2 };
 
 typedef struct {
   int m;             /* restart length (default 30) */
   double rtol;       /* stop when ||b - A x|| <= rtol ||b|| (default 1e-8) */
   int max_iters;     /* Arnoldi steps over all cycles (default 1000) */
-  int orth;          /* FDIGA_ORTH_CGS2 (default with opts == NULL): classical Gram-Schmidt twice;
+  int orth;          /* FDIGA_ORTH_DCGS2 is the default with opts == NULL.
+                        FDIGA_ORTH_CGS2: classical Gram-Schmidt twice;
                         FDIGA_ORTH_CGS_DGKS: the second pass only when ||w'|| < ||w|| / sqrt(2) (with the FD
-                        preconditioner A P^{-1} ~ I, so that test fails at every step and CGS2 is faster) */
+                        preconditioner A P^{-1} ~ I, so that test fails at every step and CGS2 is faster);
+                        FDIGA_ORTH_DCGS2: CGS2 with the second projection delayed by one step and fused with
+                        the next step's first (one reduction and two passes over the basis per step, the
+                        Arnoldi relation unchanged up to rounding; one extra P^{-1} + A application per cycle) */
   int use_x0;        /* 1: x holds the initial guess; 0: x0 = 0 */
 } gmres_opts;
 

@@ -13,6 +13,7 @@ from ._lib import (BicgstabOpts, BicgstabReport, FdSetupOpts, GmresOpts, GmresRe
 
 ORTH_CGS_DGKS = 0
 ORTH_CGS2 = 1
+ORTH_DCGS2 = 2
 
 
 def _dptr(a):
@@ -378,7 +379,7 @@ def colloc_1d_factors(p, ne):
     return M, K
 
 
-def gmres_solve(ctx, A, P, b, x, m=30, rtol=1e-8, max_iters=1000, orth=ORTH_CGS2, use_x0=False,
+def gmres_solve(ctx, A, P, b, x, m=30, rtol=1e-8, max_iters=1000, orth=ORTH_DCGS2, use_x0=False,
                 history=False, raise_on_nonconvergence=True):
     """Right-preconditioned GMRES(m); returns the report as a dict."""
     opts = GmresOpts(int(m), float(rtol), int(max_iters), int(orth), int(use_x0))

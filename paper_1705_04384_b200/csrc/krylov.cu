@@ -8,6 +8,8 @@
 //     pass 3  w''= w' - V h', ||w''||^2          (the last block also applies the Givens rotations,
 //                                                 updates g and tests |g_{j+1}| <= rtol ||b||)
 //     v_{j+1} = w'' / h_{j+1,j}
+// or (FDIGA_ORTH_DCGS2, the default) the same two projections with the second one delayed by a step and
+// fused into the next step's first pass: two passes and one reduction per step (see dcgs_decide).
 // Each pass reduces through per-block partials and a "last block" that sums them in fixed order
 // (deterministic, no second launch).  The m steps of one cycle are captured once into a CUDA graph
 // (cached on the context); after convergence is declared a device flag turns the remaining launches
@@ -45,6 +47,11 @@ struct GmState {
   int reorth;      // CGS + DGKS: the current step needs the second pass
   int nreorth;     // second passes taken
   unsigned int counter[NCNT];
+  // DCGS2 (delayed re-orthogonalisation): raw (unrotated) Hessenberg, the reduced [a; b; rho; c] of the
+  // step, and the coefficients of its update pass
+  double Hraw[(KMAX + 1) * KMAX];
+  double dred[2 * KMAX + 2], dredl[2 * KMAX + 2];
+  double pa[KMAX], pb[KMAX], gam, invb;
 };
 
 // ---- streaming Gram-Schmidt passes.  The k basis vectors and w are streamed through shared memory by
@@ -135,6 +142,125 @@ __device__ __forceinline__ void gs_stream(const double* __restrict__ V, int64_t 
       }
     }
   }
+}
+
+// DCGS2 streaming: the K rows of Q, then u and z (EXTRA = 2) or u only (EXTRA = 1, the cycle's last
+// column); PASS 0 = dots, PASS 1 = the update writing q_K (into out) and u_{K+1} (into u, in place).
+template <int K>
+__host__ __device__ constexpr int dc_stages() {
+  return (200 * 1024) / ((K + 2) * SC * 8) >= 4 ? 4 : ((200 * 1024) / ((K + 2) * SC * 8) >= 3 ? 3 : 2);
+}
+template <int K>
+__host__ __device__ constexpr size_t dc_smem_bytes() {
+  return (size_t)dc_stages<K>() * (K + 2) * SC * 8 + 64;
+}
+
+template <int K, int EXTRA, int PASS>
+__device__ __forceinline__ void dc_stream(const double* __restrict__ V, int64_t ldv, const double* u,
+                                          const double* z, int64_t N, const GmState* st, double (&acc)[2 * K + 2],
+                                          double* out, double* uout) {
+  constexpr int S = dc_stages<K>();
+  constexpr int ROWS = K + EXTRA;
+  extern __shared__ __align__(128) double dsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)S * (K + 2) * SC);
+  __shared__ double pa[KMAX + 1], pb[KMAX + 1];
+  const int tid = threadIdx.x;
+  if (PASS == 1 && tid < K) {
+    pa[tid] = st->pa[tid];
+    pb[tid] = st->pb[tid];
+  }
+#pragma unroll
+  for (int i = 0; i < 2 * K + 2; ++i) acc[i] = 0.0;
+  const int64_t nchunk = (N + SC - 1) / SC;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t c, int s) {
+    const int lane = tid & 31;
+    const int64_t e0 = c * SC;
+    const uint32_t bytes = (uint32_t)((ldv - e0 < SC ? ldv - e0 : SC) * 8);
+    double* dst = dsm + (size_t)s * (K + 2) * SC;
+    if (lane == 0) mbar_arrive_expect_tx(&full[s], ROWS * bytes);
+    __syncwarp();
+    if (lane < ROWS)
+      bulk_g2s(dst + lane * SC, lane < K ? V + lane * ldv + e0 : (lane == K ? u + e0 : z + e0), bytes, &full[s]);
+  };
+  if (tid < 32)
+    for (int s = 0; s < S; ++s) {
+      const int64_t c = blockIdx.x + (int64_t)s * gridDim.x;
+      if (c < nchunk) issue(c, s);
+    }
+  const double gam = PASS == 1 ? st->gam : 0.0, ib = PASS == 1 ? st->invb : 0.0;
+  int it = 0;
+  for (int64_t c = blockIdx.x; c < nchunk; c += gridDim.x, ++it) {
+    const int s = it % S;
+    mbar_wait(&full[s], (uint32_t)((it / S) & 1));
+    const double* buf = dsm + (size_t)s * (K + 2) * SC;
+    const int64_t e = c * SC + tid;
+    if (e < N) {
+      const double uv = buf[K * SC + tid];
+      const double zv = EXTRA == 2 ? buf[(K + 1) * SC + tid] : 0.0;
+      if (PASS == 0) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          const double q = buf[i * SC + tid];
+          acc[i] = fma(q, uv, acc[i]);
+          if (EXTRA == 2) acc[K + i] = fma(q, zv, acc[K + i]);
+        }
+        acc[2 * K] = fma(uv, uv, acc[2 * K]);
+        if (EXTRA == 2) acc[2 * K + 1] = fma(uv, zv, acc[2 * K + 1]);
+      } else {
+        double qv = uv, nz = zv;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          const double q = buf[i * SC + tid];
+          qv = fma(-pa[i], q, qv);
+          nz = fma(-pb[i], q, nz);
+        }
+        qv *= ib;
+        out[e] = qv;
+        uout[e] = (nz - gam * qv) * ib;
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int64_t cn = c + (int64_t)S * gridDim.x;
+      if (cn < nchunk) {
+        fence_proxy_async();
+        issue(cn, s);
+      }
+    }
+  }
+}
+
+__device__ void dcgs_decide(GmState* st, int j, int m, const double* red, int withz, double* hist, int hist_cap);
+__device__ void arnoldi_close_step(GmState* st, int j, int m, double wn2, double* hist, int hist_cap);
+
+// DCGS2 pass A: [a; b; rho; c] (reduction); the last block decides (single rank) or leaves partials
+template <int K, int EXTRA>
+__global__ void __launch_bounds__(RT) dcgs_passA(const double* __restrict__ V, int64_t ldv, const double* u,
+                                                 const double* z, int64_t N, double* part, GmState* st, int m,
+                                                 double* hist, int hist_cap, int close) {
+  if (st->stop) return;
+  double acc[2 * K + 2];
+  dc_stream<K, EXTRA, 0>(V, ldv, u, z, N, st, acc, nullptr, nullptr);
+  // pack [a (K), b (K), rho, c] contiguously for the reduction
+  double* out = close ? st->dred : st->dredl;
+  if (reduce_last<2 * K + 2>(acc, 2 * K + 2, part, &st->counter[0], out) && close && threadIdx.x == 0)
+    dcgs_decide(st, K, m, out, EXTRA == 2, hist, hist_cap);
+}
+
+// DCGS2 pass B: q_K and u_{K+1}
+// (u and uout alias for K >= 1: every element is read from shared memory before its own thread writes it)
+template <int K>
+__global__ void __launch_bounds__(RT) dcgs_passB(const double* __restrict__ V, int64_t ldv, const double* u,
+                                                 const double* z, int64_t N, GmState* st, double* qout,
+                                                 double* uout) {
+  if (st->stop) return;
+  double acc[2 * K + 2];
+  dc_stream<K, 2, 1>(V, ldv, u, z, N, st, acc, qout, uout);
 }
 
 // pass 1: h[i] = V_i . w (i < k), h[k] = w . w
@@ -240,6 +366,65 @@ __device__ void arnoldi_close_step(GmState* st, int j, int m, double wn2, double
   st->invh = hn > 0.0 ? 1.0 / hn : 0.0;
   if (bad) st->breakdown = 1;
   if (bad || fabs(st->g[k]) <= st->target || hn == 0.0 || st->iters >= st->max_iters || k >= m) st->stop = 1;
+}
+
+// ---- DCGS2: classical Gram-Schmidt twice with the second pass delayed by one step (one reduction per
+// step).  Step j holds Q_j = [q_0..q_{j-1}] (final) and u_j, the candidate for q_j projected once.  With
+// z = B u_j (B = A P^{-1}):
+//   pass A (one reduction):  a = Q_j^T u_j,  b = Q_j^T z,  rho = u_j.u_j,  c = u_j.z
+//   decide:  beta^2 = rho - |a|^2 (Pythagoras: a is the O(eps kappa) second projection);  column j-1 of the
+//            Hessenberg = h1_{j-1} + a, H[j][j-1] = beta  -> Givens / convergence;  gamma = (c - a.b) / beta;
+//            the first-pass coefficients of column j: h1_j = ([b; gamma] - Hraw a) / beta  (because
+//            B q_j = (z - Q_{j+1} Hraw a) / beta)
+//   pass B:  q_j = (u_j - Q_j a) / beta  (final),  u_{j+1} = (z - Q_j b - gamma q_j) / beta
+// Two streamed passes over Q_j per step instead of CGS2's three, and the same columns (iteration counts)
+// as CGS2; the convergence of column j-1 is seen one operator application later (at step j).
+__device__ void dcgs_decide(GmState* st, int j, int m, const double* red, int withz, double* hist, int hist_cap) {
+  const double* a = red;
+  const double* b = red + j;
+  const double rho = red[2 * j], c = red[2 * j + 1];
+  double aa = 0.0;
+  for (int i = 0; i < j; ++i) aa += a[i] * a[i];
+  const double b2 = rho - aa;
+  double beta;
+  if (j == 0) {
+    beta = sqrt(fmax(b2, 0.0));
+    st->g[0] *= beta;  // r = ||r|| u_0 = ||r|| beta q_0
+    if (!(beta > 0.0) || !isfinite(beta)) {
+      st->breakdown = !isfinite(beta);
+      st->stop = 1;
+      return;
+    }
+  } else {
+    for (int i = 0; i < j; ++i) {
+      st->h2[i] = a[i];
+      st->Hraw[i * KMAX + (j - 1)] = st->h1[i] + a[i];
+    }
+    beta = sqrt(fmax(b2, 0.0));
+    st->Hraw[j * KMAX + (j - 1)] = beta;
+    arnoldi_close_step(st, j - 1, m, b2, hist, hist_cap);
+    if (st->stop || !withz) return;
+  }
+  const double ib = 1.0 / beta;
+  double ab = 0.0;
+  for (int i = 0; i < j; ++i) ab += a[i] * b[i];
+  const double gam = (c - ab) * ib;
+  for (int i = 0; i <= j; ++i) {
+    double ha = 0.0;  // (Hraw a)_i: column l of Hraw has rows 0..l+1
+    for (int l = i > 0 ? i - 1 : 0; l < j; ++l) ha += st->Hraw[i * KMAX + l] * a[l];
+    st->h1[i] = ((i < j ? b[i] : gam) - ha) * ib;
+  }
+  for (int i = 0; i < j; ++i) {
+    st->pa[i] = a[i];
+    st->pb[i] = b[i];
+  }
+  st->gam = gam;
+  st->invb = ib;
+}
+
+__global__ void dcgs_decide_kernel(GmState* st, int j, int m, int withz, double* hist, int hist_cap) {
+  if (st->stop) return;
+  dcgs_decide(st, j, m, st->dred, withz, hist, hist_cap);
 }
 
 // CGS + DGKS decision after the first update (one thread): Daniel-Gragg-Kaufman-Stewart test
@@ -393,7 +578,7 @@ struct Ws {
   int nblk;
   bool sh;  // nranks > 1: reductions are all-reduced between the passes
   int orth; // FDIGA_ORTH_*
-  double *V, *z, *w, *part, *hist;
+  double *V, *z, *w, *u, *part, *hist;  // u: DCGS2's once-projected candidate u_j
   GmState* st;
 };
 
@@ -464,6 +649,52 @@ int passes_k(fdiga_ctx* ctx, const Ws& W, int j, int m, int hist_cap) {
   return pass3_k<K>(ctx, W, j, m, hist_cap, P3_CLOSE_IF_REORTH);
 }
 
+// DCGS2 step j = K (EXTRA = 2: pass A, decide, pass B) or the cycle's closing pass A over K = m (EXTRA = 1)
+template <int K, int EXTRA>
+int dcgs_k(fdiga_ctx* ctx, const Ws& W, const double* u, int m, int hist_cap) {
+  GmState* st = W.st;
+  constexpr size_t smem = dc_smem_bytes<K>();
+  static bool attr = false;
+  if (!attr) {
+    FDIGA_CUDA(cudaFuncSetAttribute(dcgs_passA<K, EXTRA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (EXTRA == 2)
+      FDIGA_CUDA(cudaFuncSetAttribute(dcgs_passB<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int per_sm = std::max(1, std::min(8, (int)((227 * 1024) / (smem + 1024))));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((W.N + SC - 1) / SC, (int64_t)ctx->sm_count * per_sm));
+  dcgs_passA<K, EXTRA><<<grid, RT, smem, ctx->stream>>>(W.V, W.ldv, u, W.w, W.N, W.part, st, m, W.hist, hist_cap,
+                                                        W.sh ? 0 : 1);
+  count_launch(ctx);
+  if (W.sh) {
+    FDIGA_TRY(comm_allreduce(ctx, st->dredl, st->dred, 2 * K + 2));
+    dcgs_decide_kernel<<<1, 1, 0, ctx->stream>>>(st, K, m, EXTRA == 2, W.hist, hist_cap);
+    count_launch(ctx);
+  }
+  if (EXTRA == 2) {
+    dcgs_passB<K><<<grid, RT, smem, ctx->stream>>>(W.V, W.ldv, u, W.w, W.N, st, W.V + (int64_t)K * W.ldv, W.u);
+    count_launch(ctx);
+  }
+  FDIGA_CUDA(cudaGetLastError());
+  return FDIGA_OK;
+}
+
+int launch_dcgs(fdiga_ctx* ctx, const Ws& W, int j, const double* u, int m, int hist_cap, bool closing) {
+  switch (j) {
+#define FDIGA_K(K)                                                                                   \
+  case K:                                                                                            \
+    return closing ? dcgs_k<K, 1>(ctx, W, u, m, hist_cap) : dcgs_k<K, 2>(ctx, W, u, m, hist_cap);
+    FDIGA_K(0) FDIGA_K(1) FDIGA_K(2) FDIGA_K(3) FDIGA_K(4) FDIGA_K(5) FDIGA_K(6) FDIGA_K(7) FDIGA_K(8)
+    FDIGA_K(9) FDIGA_K(10) FDIGA_K(11) FDIGA_K(12) FDIGA_K(13) FDIGA_K(14) FDIGA_K(15) FDIGA_K(16)
+    FDIGA_K(17) FDIGA_K(18) FDIGA_K(19) FDIGA_K(20) FDIGA_K(21) FDIGA_K(22) FDIGA_K(23) FDIGA_K(24)
+    FDIGA_K(25) FDIGA_K(26) FDIGA_K(27) FDIGA_K(28) FDIGA_K(29) FDIGA_K(30) FDIGA_K(31)
+#undef FDIGA_K
+    default:
+      break;
+  }
+  FDIGA_CHECK(false, FDIGA_ERR_INVALID_ARG, "basis size %d out of range", j);
+}
+
 template <int K>
 int lincomb_k(fdiga_ctx* ctx, const Ws& W, double* out) {
   size_t smem = 0;
@@ -516,6 +747,21 @@ int launch_passes(fdiga_ctx* ctx, const Ws& W, int k, int j, int m, int hist_cap
 // Enqueue the m Arnoldi steps of one cycle on ctx->stream (captured by the caller).
 int enqueue_cycle(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const Ws& W, int m, int hist_cap) {
   const int* stop = &W.st->stop;
+  if (W.orth == FDIGA_ORTH_DCGS2) {
+    // z = B u_j with u_0 = v_0 (the normalised residual) and u_j (j >= 1) in W.u; the first pass B reads
+    // u_0 from V row 0 and writes q_0 over it and u_1 into W.u
+    for (int j = 0; j < m; ++j) {
+      const double* u = j == 0 ? W.V : W.u;
+      if (P) {
+        FDIGA_TRY(fd_apply_ex(P, u, W.z, stop));
+        FDIGA_TRY(stencil_matvec_ex(A, W.z, W.w, stop));
+      } else {
+        FDIGA_TRY(stencil_matvec_ex(A, u, W.w, stop));
+      }
+      FDIGA_TRY(launch_dcgs(ctx, W, j, u, m, hist_cap, false));
+    }
+    return launch_dcgs(ctx, W, m, m == 0 ? W.V : W.u, m, hist_cap, true);
+  }
   for (int j = 0; j < m; ++j) {
     double* vj = W.V + (int64_t)j * W.ldv;
     if (P) {
@@ -545,6 +791,7 @@ struct GmresGraph {
   int64_t N = 0;
   double* V = nullptr;
   double* hist = nullptr;
+  double *z = nullptr, *part = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaStream_t cap_stream = nullptr;
 };
@@ -576,9 +823,9 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   Ws W;
   W.N = stencil_local_rows(A);
   W.sh = ctx->sharded;
-  W.orth = opts ? opts->orth : FDIGA_ORTH_CGS2;
-  FDIGA_CHECK(W.orth == FDIGA_ORTH_CGS_DGKS || W.orth == FDIGA_ORTH_CGS2, FDIGA_ERR_INVALID_ARG, "unknown orth %d",
-              W.orth);
+  W.orth = opts ? opts->orth : FDIGA_ORTH_DCGS2;
+  FDIGA_CHECK(W.orth == FDIGA_ORTH_CGS_DGKS || W.orth == FDIGA_ORTH_CGS2 || W.orth == FDIGA_ORTH_DCGS2,
+              FDIGA_ERR_INVALID_ARG, "unknown orth %d", W.orth);
   const bool use_graph = comm_capturable(ctx);
   FDIGA_CHECK(!P || fd_plan_local_size(P) == W.N, FDIGA_ERR_INVALID_ARG,
               "preconditioner and operator sizes differ (%lld vs %lld local rows)",
@@ -588,12 +835,13 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   const int hist_cap = std::max(max_iters, 1);
   const size_t st_doubles = (sizeof(GmState) + 7) / 8;
   FDIGA_TRY(ctx->ws[0].ensure((size_t)(m + 1) * W.ldv));
-  FDIGA_TRY(ctx->ws[1].ensure((size_t)2 * W.ldv));
-  FDIGA_TRY(ctx->ws[2].ensure((size_t)std::max(W.nblk, 8 * ctx->sm_count) * (KMAX + 1)));
+  FDIGA_TRY(ctx->ws[1].ensure((size_t)3 * W.ldv));
+  FDIGA_TRY(ctx->ws[2].ensure((size_t)std::max(W.nblk, 8 * ctx->sm_count) * (2 * KMAX + 2)));
   FDIGA_TRY(ctx->ws[3].ensure(st_doubles + hist_cap));
   W.V = ctx->ws[0].p;
   W.z = ctx->ws[1].p;
   W.w = ctx->ws[1].p + W.ldv;
+  W.u = ctx->ws[1].p + 2 * W.ldv;
   W.part = ctx->ws[2].p;
   W.st = reinterpret_cast<GmState*>(ctx->ws[3].p);
   W.hist = ctx->ws[3].p + st_doubles;
@@ -603,7 +851,7 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   // ---- the captured cycle (once per (A, P, m, N, workspace))
   GmresGraph* G = static_cast<GmresGraph*>(ctx->gmres_graph);
   if (G && (G->A != A || G->P != P || G->m != m || G->N != W.N || G->V != W.V || G->hist != W.hist ||
-            G->hist_cap != hist_cap || G->orth != W.orth)) {
+            G->hist_cap != hist_cap || G->orth != W.orth || G->z != W.z || G->part != W.part)) {
     destroy_gmres_graph(ctx);
     G = nullptr;
   }
@@ -618,6 +866,8 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
     G->hist = W.hist;
     G->hist_cap = hist_cap;
     G->orth = W.orth;
+    G->z = W.z;
+    G->part = W.part;
     FDIGA_CUDA(cudaStreamCreateWithFlags(&G->cap_stream, cudaStreamNonBlocking));
     FDIGA_CUDA(cudaStreamSynchronize(st));
     cudaStream_t saved = ctx->stream;
@@ -721,7 +971,7 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
     rep->iters = hs.iters;
     rep->restarts = cycles;
     rep->converged = (status == FDIGA_OK) ? 1 : 0;
-    rep->reorth = W.orth == FDIGA_ORTH_CGS2 ? hs.iters : hs.nreorth;  // second Gram-Schmidt passes
+    rep->reorth = W.orth != FDIGA_ORTH_CGS_DGKS ? hs.iters : hs.nreorth;  // second Gram-Schmidt passes
     rep->rel_res_true = hs.rel_true;
     rep->rel_res_implicit = hs.rel_implicit;
     rep->t_total_ms = ms;

@@ -449,19 +449,42 @@ def test_matrix_free_gmres_and_bicgstab(ctx, cfg):
 
 @pytest.mark.parametrize("cfg", [2, 5])
 def test_gmres_orthogonalisation_variants_agree(ctx, cfg):
-    # CGS + DGKS (default) and CGS2 take the same number of steps (orthogonalisation-
-    # independent counts) and reach the same solution
+    # CGS + DGKS, CGS2 and DCGS2 (default) take the same number of steps (SURVEY.md §0.8:
+    # orthogonalisation-independent counts) and reach the same solution
     c = get_config(cfg)
     A = fd.colloc_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params, matrix_free=(c.d == 3))
     _, M, K, _ = splines.colloc_1d(c.ne, c.p)
     P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
     b = gpu(rhs(cfg, A.N))
     x1, x2 = torch.empty_like(b), torch.empty_like(b)
-    r1 = fd.gmres_solve(ctx, A, P, b, x1, orth=fd.ORTH_CGS_DGKS)
-    r2 = fd.gmres_solve(ctx, A, P, b, x2, orth=fd.ORTH_CGS2)
-    assert r1["iters"] == r2["iters"] == GOLD["configs"][str(cfg)]["iters"]
+    x3 = torch.empty_like(b)
+    r1 = fd.gmres_solve(ctx, A, P, b, x1, orth=fd.ORTH_CGS_DGKS, history=True)
+    r2 = fd.gmres_solve(ctx, A, P, b, x2, orth=fd.ORTH_CGS2, history=True)
+    r3 = fd.gmres_solve(ctx, A, P, b, x3, orth=fd.ORTH_DCGS2, history=True)
+    assert r1["iters"] == r2["iters"] == r3["iters"] == GOLD["configs"][str(cfg)]["iters"]
     assert r2["reorth"] == r2["iters"] and 0 <= r1["reorth"] <= r1["iters"]
-    assert rel(host(x1), host(x2)) <= 1e-7
+    assert rel(host(x1), host(x2)) <= 1e-7 and rel(host(x3), host(x2)) <= 1e-7
+    assert r3["rel_res_true"] <= 1e-8
+    # delayed re-orthogonalisation builds the same Hessenberg columns: the implicit residuals agree
+    np.testing.assert_allclose(r3["history"], r2["history"], rtol=1e-6)
+
+
+@pytest.mark.parametrize("m", [1, 2, 5, 30])
+def test_gmres_dcgs2_matches_oracle(ctx, m):
+    # DCGS2 across restart lengths (m = 1: one step and the closing pass per cycle), preconditioned and
+    # restarted: the oracle's GMRES(m) iteration count and solution
+    A = fd.colloc_assemble(ctx, 2, 3, 16, 1, (1.0, 2.0))
+    disc = assembly.Discretisation(2, 3, 16, 1, (1.0, 2.0))
+    f = fastdiag.setup([disc.M] * 2, [disc.K] * 2)
+    P = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
+    bh = rhs(2, disc.N, rep=5)
+    x = torch.empty(disc.N, dtype=torch.float64, device=DEV)
+    rep = fd.gmres_solve(ctx, A, P, gpu(bh), x, m=m, max_iters=3000, rtol=1e-10, orth=fd.ORTH_DCGS2)
+    xo, repo = krylov.gmres(disc.matvec, bh, precond=lambda v: fastdiag.apply(f, v), m=m, max_iters=3000,
+                            rtol=1e-10)
+    assert rep["converged"] and repo["converged"]
+    assert abs(rep["iters"] - repo["iters"]) <= max(2, repo["iters"] // 50), (rep, repo)
+    assert rel(host(x), xo) <= 1e-6
 
 
 # ----------------------------------------------------------------------------- NEXT-4: convection-diffusion

@@ -142,8 +142,8 @@ def test_sharded_matvec_matches_oracle(cfg, ne, nranks):
 
 # ----------------------------------------------------------------------------- GMRES
 
-@pytest.mark.parametrize("cfg,nranks", [(3, 2), (3, 4), (5, 8)])
-def test_sharded_gmres_iterations_match_oracle(cfg, nranks):
+@pytest.mark.parametrize("cfg,nranks,orth", [(3, 2, 2), (3, 4, 1), (3, 4, 2), (5, 8, 2), (5, 8, 0)])
+def test_sharded_gmres_iterations_match_oracle(cfg, nranks, orth):
     c = get_config(cfg)
     _, M, K, _ = splines.colloc_1d(c.ne, c.p)
     n = M.shape[0]
@@ -155,7 +155,7 @@ def test_sharded_gmres_iterations_match_oracle(cfg, nranks):
         lo, hi = slab_rows(n, nranks, rank, n * n)
         bt = torch.from_numpy(b[lo:hi].copy()).to(DEV)
         x = torch.empty_like(bt)
-        rep = fd.gmres_solve(ctx, A, P, bt, x)
+        rep = fd.gmres_solve(ctx, A, P, bt, x, orth=orth)
         torch.cuda.current_stream().synchronize()
         out = (rep, x.cpu().numpy())
         P.close()
@@ -208,7 +208,8 @@ def test_nccl_one_rank_fd_apply_and_matvec(nccl_ctx):
     A.close()
 
 
-def test_nccl_one_rank_gmres_captured(nccl_ctx):
+@pytest.mark.parametrize("orth", [1, 2])
+def test_nccl_one_rank_gmres_captured(nccl_ctx, orth):
     c = get_config(3)
     _, M, K, _ = splines.colloc_1d(c.ne, c.p)
     A = fd.colloc_assemble(nccl_ctx, 3, c.p, c.ne, c.geometry, c.geo_params)
@@ -216,7 +217,7 @@ def test_nccl_one_rank_gmres_captured(nccl_ctx):
     b = torch.from_numpy(rhs(3, A.N)).to(DEV)
     x = torch.empty_like(b)
     for _ in range(2):  # second solve replays the cached graph
-        rep = fd.gmres_solve(nccl_ctx, A, P, b, x)
+        rep = fd.gmres_solve(nccl_ctx, A, P, b, x, orth=orth)
         assert rep["converged"] and abs(rep["iters"] - GOLD["configs"]["3"]["iters"]) <= 1
         assert rep["rel_res_true"] <= 1e-8
     P.close()

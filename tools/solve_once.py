@@ -15,7 +15,7 @@ ap.add_argument("--cfg", type=int, default=5)
 ap.add_argument("--solver", default="gmres")
 ap.add_argument("--matrix-free", action="store_true")
 ap.add_argument("--reps", type=int, default=2)
-ap.add_argument("--orth", type=int, default=1)
+ap.add_argument("--orth", type=int, default=2)
 a = ap.parse_args()
 c = get_config(a.cfg)
 ctx = fd.Context(0, stream=torch.cuda.current_stream().cuda_stream)
