@@ -53,9 +53,12 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int KV_ = 0, int NP_ = 0>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int KV_ = 0, int NP_ = 0, int MINB_ = 1>
 struct TileCfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  // MINB: resident CTAs per SM the register allocation must allow (__launch_bounds__ min blocks); 4 x 64x64
+  // CTAs per SM (config 16) measured no faster than 3 at n = 256: the loss is not wave quantisation
+  static constexpr int MINB = MINB_;
   // NP = 1 (KN layout, with KV, warp tiles 64 wide): n-permuted fragments.  Within a warp tile the
   // logical column (MMA j, lane row r) is the physical column r NJ + j, so a thread's NJ B fragments of
   // one k are NJ consecutive doubles (16-byte loads) and its accumulators map to two runs of NJ
@@ -91,7 +94,7 @@ struct TileCfg {
 
 // VA / VB: doubles per cp.async chunk for A / B (2 needs 16-byte aligned rows, else 1).
 template <class T, BLayout BL, int VA, int VB>
-__global__ void __launch_bounds__(T::THREADS, 1) dmma_gemm_kernel(GemmParams p) {
+__global__ void __launch_bounds__(T::THREADS, T::MINB) dmma_gemm_kernel(GemmParams p) {
   // programmatic dependent launch: this grid may start while the previous kernel of the stream drains;
   // nothing it produced (the B/A operand, the skip flag) is read before its completion is awaited here
   asm volatile("griddepcontrol.wait;\n" ::: "memory");

@@ -884,9 +884,10 @@ int fd_apply_host_async(fd_plan* P, const double* r_host, double* s_host) {
       FDIGA_CUDA(cudaEventRecord(P->ev_out[k], P->s_d2h));  // both slots start free
     }
   }
+  // every slot is allocated up front: a cudaMalloc on a later call would synchronise the device mid-stream
+  for (int j = 0; j < fd_plan::NSLOT; ++j) FDIGA_TRY(P->aio[j].ensure(std::max<int64_t>(1, P->Nloc)));
   const int k = P->aslot;
   P->aslot = (P->aslot + 1) % fd_plan::NSLOT;
-  FDIGA_TRY(P->aio[k].ensure(std::max<int64_t>(1, P->Nloc)));
   double* buf = P->aio[k].p;
   const size_t bytes = (size_t)P->Nloc * 8;
   // H2D into slot k once its previous result left the device; apply on the context stream; D2H behind it

@@ -35,6 +35,9 @@ int launch_variant(fdiga_ctx* ctx, cudaStream_t stream, GemmParams p) {
   static bool attr_set = false;  // per instantiation (single device per process is assumed here)
   if (!attr_set) {
     FDIGA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // the whole unified L1/shared array as shared memory: several CTAs of 54-76 KB per SM
+    FDIGA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    (int)cudaSharedmemCarveoutMaxShared));
     attr_set = true;
   }
   p.tiles_m = (p.M + T::BM - 1) / T::BM;
@@ -106,12 +109,14 @@ using NK12 = TileCfg<64, 128, 16, 2, 2, 3, 1>;  // NK6 with k-permuted 16-byte f
 using NK13 = TileCfg<64, 128, 16, 2, 2, 4, 1>;  // 4 stages
 using NK14 = TileCfg<128, 64, 16, 2, 2, 4, 1>;  // warp 64x32
 using NK15 = TileCfg<128, 128, 16, 2, 4, 4, 1>; // NK0 with k-permuted fragments
-
+// 4 CTAs per SM (<= 128 registers, 3 stages of k-permuted 16-byte fragments: 54-55 KB of shared memory)
+using KN16 = TileCfg<64, 64, 16, 2, 2, 3, 1, 0, 4>;
+using NK16 = TileCfg<64, 64, 16, 2, 2, 3, 1, 0, 4>;
 const char* kKnNames[] = {"128x128", "144x128", "72x128", "88x128", "64x64", "72x64",
-                          "128x64", "128x128k32", "144x64", "72x32", "72x16", "64x64kv", "64x128kv", "64x128np", "64x128np4", "128x128np"};
+                          "128x64", "128x128k32", "144x64", "72x32", "72x16", "64x64kv", "64x128kv", "64x128np", "64x128np4", "128x128np", "64x64kv3m4"};
 const char* kNkNames[] = {"128x128", "128x144", "128x72", "128x88", "64x64", "64x72",
-                          "64x128", "128x128k32", "64x144", "32x72", "16x72", "64x64kv", "64x128kv", "64x128kv4", "128x64kv", "128x128kv"};
-constexpr int kNumCfg = 16;
+                          "64x128", "128x128k32", "64x144", "32x72", "16x72", "64x64kv", "64x128kv", "64x128kv4", "128x64kv", "128x128kv", "64x64kv3m4"};
+constexpr int kNumCfg = 17;
 
 }  // namespace
 
@@ -141,6 +146,7 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 13: return launch_cfg<KN13, BLayout::KN>(ctx, stream, p);
       case 14: return launch_cfg<KN14, BLayout::KN>(ctx, stream, p);
       case 15: return launch_cfg<KN15, BLayout::KN>(ctx, stream, p);
+      case 16: return launch_cfg<KN16, BLayout::KN>(ctx, stream, p);
     }
   } else {
     switch (cfg) {
@@ -160,6 +166,7 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 13: return launch_cfg<NK13, BLayout::NK>(ctx, stream, p);
       case 14: return launch_cfg<NK14, BLayout::NK>(ctx, stream, p);
       case 15: return launch_cfg<NK15, BLayout::NK>(ctx, stream, p);
+      case 16: return launch_cfg<NK16, BLayout::NK>(ctx, stream, p);
     }
   }
   set_error("bad GEMM configuration %d", cfg);
