@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libfdiga.so")
-SOURCES = ["ctx.cu", "comm.cu", "fd_gemm.cu", "fd.cu", "stencil.cu", "krylov.cu", "bicgstab.cu", "matfree.cu", "wq.cu"]
+SOURCES = ["ctx.cu", "comm.cu", "fd_gemm.cu", "fd.cu", "stencil.cu", "krylov.cu", "bicgstab.cu", "matfree.cu", "wq.cu", "oz.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

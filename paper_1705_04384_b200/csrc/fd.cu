@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "fd_gemm.cuh"
+#include "oz.cuh"
 
 using namespace fdiga;
 
@@ -55,6 +56,9 @@ struct fd_plan {
   // (Nloc = (e - o) Nin values, Nin = n_1..n_{d-1}); the mode-d sandwich runs in the transposed layout
   // T(n_d x len) over the inner-index chunk [q0, q0 + len).
   int64_t Nin = 0, o = 0, e = 0, q0 = 0, len = 0, Nloc = 0;
+  // int8-split tcgen05 mode products (oz.cu): digit planes of the factors and of the data per mode
+  bool oz = false;
+  OzOperand ozW[3], ozU[3], ozX[3];
 };
 
 namespace {
@@ -307,6 +311,78 @@ int broadcast_factors(fd_plan* P) {
   return FDIGA_OK;
 }
 
+// int8-split tensor-core mode products (oz.cu): 3D, single rank, real spectra, n_l <= 256.  Enabled by
+// FDIGA_FD_OZ=1 (default off while it is being measured).
+bool oz_eligible(const fd_plan* P) {
+  const char* e = getenv("FDIGA_FD_OZ");
+  if (!(e && e[0] == '1')) return false;
+  if (P->d != 3 || P->ctx->sharded || P->has_pairs) return false;
+  for (int l = 0; l < 3; ++l)
+    if (P->n[l] > OZ_MAXKP) return false;
+  return true;
+}
+
+int oz_setup(fd_plan* P) {
+  if (!oz_eligible(P)) return FDIGA_OK;
+  cudaStream_t st = P->ctx->stream;
+  for (int l = 0; l < 3; ++l) {
+    FDIGA_TRY(oz_operand_alloc(P->ozW[l], P->n[l], P->n[l], OZ_BN));
+    FDIGA_TRY(oz_operand_alloc(P->ozU[l], P->n[l], P->n[l], OZ_BN));
+    FDIGA_TRY(oz_split(P->ctx, st, P->W[l], P->n[l], P->n[l], 1, P->ld[l], P->ozW[l], nullptr));
+    FDIGA_TRY(oz_split(P->ctx, st, P->U[l], P->n[l], P->n[l], 1, P->ld[l], P->ozU[l], nullptr));
+    FDIGA_TRY(oz_operand_alloc(P->ozX[l], P->N / P->n[l], P->n[l], OZ_BM));
+  }
+  FDIGA_CUDA(cudaStreamSynchronize(st));
+  P->oz = true;
+  return FDIGA_OK;
+}
+
+// one mode product on the int8 path: split the data along axis l, contract with the factor digits
+int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, const double* lamD,
+            const double* lamF, const int* skip) {
+  const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
+  OzOperand& Xz = P->ozX[l];
+  cudaStream_t st = P->ctx->stream;
+  OzGemmArgs g{};
+  g.X = &Xz;
+  g.F = &Fz;
+  g.y = Y;
+  g.lamD = lamD;
+  g.lamF = lamF;
+  g.skip = skip;
+  if (l == 0) {  // data rows (i3, i2), k = i1
+    FDIGA_TRY(oz_split(P->ctx, st, X, n2 * n3, n1, 1, n1, Xz, skip));
+    g.inner = n2 * n3;
+    g.bstride = 0;
+    g.mstride = n1;
+    g.fstride = 1;
+  } else if (l == 1) {  // data rows (i3, i1), k = i2
+    FDIGA_TRY(oz_split(P->ctx, st, X, n3, n2, n1, 0, Xz, skip));
+    g.inner = n1;
+    g.bstride = n1 * n2;
+    g.mstride = 1;
+    g.fstride = n1;
+  } else {  // data rows (i2, i1), k = i3
+    FDIGA_TRY(oz_split(P->ctx, st, X, 1, n3, n1 * n2, 0, Xz, skip));
+    g.inner = n1 * n2;
+    g.bstride = 0;
+    g.mstride = 1;
+    g.fstride = n1 * n2;
+  }
+  return oz_gemm(P->ctx, st, g);
+}
+
+int fd_apply_oz(fd_plan* P, const double* r, double* s, const int* skip) {
+  double* a = P->t0.p;
+  double* b = P->t1.p;
+  FDIGA_TRY(oz_mode(P, 0, P->ozW[0], r, a, nullptr, nullptr, skip));
+  FDIGA_TRY(oz_mode(P, 1, P->ozW[1], a, b, nullptr, nullptr, skip));
+  FDIGA_TRY(oz_mode(P, 2, P->ozW[2], b, a, P->lam_inner, P->lam[2], skip));
+  FDIGA_TRY(oz_mode(P, 2, P->ozU[2], a, b, nullptr, nullptr, skip));
+  FDIGA_TRY(oz_mode(P, 1, P->ozU[1], b, a, nullptr, nullptr, skip));
+  return oz_mode(P, 0, P->ozU[0], a, s, nullptr, nullptr, skip);
+}
+
 int finish_plan(fd_plan* P) {
   const int d = P->d;
   if (P->ctx->sharded) FDIGA_TRY(broadcast_factors(P));
@@ -392,6 +468,7 @@ int finish_plan(fd_plan* P) {
   }
   FDIGA_CUDA(cudaDeviceSynchronize());  // uploads complete before any stream uses the plan
   FDIGA_TRY(autotune_plan(P));
+  FDIGA_TRY(oz_setup(P));
   return FDIGA_OK;
 }
 
@@ -624,6 +701,7 @@ int fd_apply_ex(fd_plan* P, const double* r, double* s, const int* skip) {
   // (P:434): plain last forward product, then the small block solves in place
   const bool fused = !P->has_pairs;
   if (ctx->sharded) return fd_apply_sharded(P, r, s, skip);
+  if (P->oz) return fd_apply_oz(P, r, s, skip);
   if (P->d == 2) {
     // fwd: mode 1 (W_1), mode 2 (W_2) + divide by lam_2[i2] + lam_1[i1]; bwd: mode 2 (U_2), mode 1 (U_1)
     FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2, skip));
@@ -931,6 +1009,9 @@ int fd_plan_destroy(fd_plan* P) {
   for (int l = 0; l < 3; ++l) {
     cudaFree(P->lam_im[l]);
     cudaFree(P->lead[l]);
+    P->ozW[l].release();
+    P->ozU[l].release();
+    P->ozX[l].release();
   }
   P->t0.release();
   P->t1.release();

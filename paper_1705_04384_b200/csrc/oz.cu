@@ -1,0 +1,514 @@
+// FD mode products on tcgen05 int8 tensor cores with exact digit splitting (see oz.cuh).
+//
+//   oz_split_*_kernel : FP64 operand -> S int8 digit planes + per-row exponents (HBM-bound pass)
+//   oz_gemm_kernel    : persistent, warp-specialised tcgen05 GEMM.  Warp 4 streams the data digit planes
+//                       through a TMA (SWIZZLE_128B) ring; warp 5 issues tcgen05.mma.kind::i8 from one
+//                       thread into S int32 accumulators in TMEM (one per digit-pair weight t = i + j);
+//                       warps 0-3 read them back with tcgen05.ld, combine in FP64, scale by the row
+//                       exponents, optionally divide by the eigenvalue sums, and store.  The factor's
+//                       digit planes for the CTA's column tile stay resident in shared memory.
+#include <cuda.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+
+#include "oz.cuh"
+#include "ptx.cuh"
+
+namespace fdiga {
+
+void OzOperand::release() {
+  if (digits) cudaFree(digits);
+  if (exps) cudaFree(exps);
+  digits = nullptr;
+  exps = nullptr;
+  rows = rows_p = kp = 0;
+}
+
+namespace {
+
+// ---------------------------------------------------------------------------------------------
+// digit split
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ int row_exponent(double mx) {
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): every |x| <= mx < 2^e
+  return e;
+}
+
+// 8 consecutive values (scaled to (-1, 1)) -> S packed 8-byte digit words
+__device__ __forceinline__ void split8(const double (&v)[8], int e, uint64_t (&w)[OZ_S]) {
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = ldexp(v[j], -e);
+#pragma unroll
+  for (int s = 0; s < OZ_S; ++s) {
+    uint64_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double a = r[j] * 128.0;  // exact (power-of-two scaling)
+      const double q = trunc(a);      // |q| <= 127 since |a| < 128
+      r[j] = a - q;                   // exact: the fractional part
+      word |= (uint64_t)(uint8_t)(int8_t)(int)q << (8 * j);
+    }
+    w[s] = word;
+  }
+}
+
+// inner == 1: rows of K contiguous values.  One warp per row, 8 values per lane per 256-wide chunk.
+template <int NCH>
+__global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __restrict__ x, int64_t rows, int K, int64_t ldx,
+                                                            int8_t* __restrict__ digits, int32_t* __restrict__ exps,
+                                                            int64_t rows_p, int kp, const int* skip) {
+  if (skip && *skip) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t m = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (m >= rows) return;
+  const double* xr = x + m * ldx;
+  double v[NCH][8];
+  double mx = 0.0;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = c * 256 + lane * 8 + j;
+      v[c][j] = k < K ? xr[k] : 0.0;
+      mx = fmax(mx, fabs(v[c][j]));
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int e = row_exponent(mx);
+  if (lane == 0) exps[m] = e;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int k0 = c * 256 + lane * 8;
+    if (k0 >= kp) break;
+    uint64_t w[OZ_S];
+    split8(v[c], e, w);
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s)
+      *reinterpret_cast<uint64_t*>(digits + ((int64_t)s * rows_p + m) * kp + k0) = w[s];
+  }
+}
+
+// inner > 1: the contracted index k is strided; rows m = b inner + i.  A block stages a K x 32 tile
+// (coalesced over i), takes the column maxima, and writes the digit rows k-contiguous (transposed).
+__global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __restrict__ x, int64_t batch, int K,
+                                                            int64_t inner, int8_t* __restrict__ digits,
+                                                            int32_t* __restrict__ exps, int64_t rows_p, int kp,
+                                                            const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ double tile[];  // [K][33]
+  __shared__ double pmax[8][32];
+  __shared__ int es[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tiles_i = (inner + 31) / 32;
+  const int64_t b = blockIdx.x / tiles_i;
+  const int64_t i0 = (blockIdx.x % tiles_i) * 32;
+  const double* xb = x + b * K * inner;
+  double mx = 0.0;
+  for (int k = warp; k < K; k += 8) {
+    const double v = (i0 + lane < inner) ? xb[(int64_t)k * inner + i0 + lane] : 0.0;
+    tile[k * 33 + lane] = v;
+    mx = fmax(mx, fabs(v));
+  }
+  pmax[warp][lane] = mx;
+  __syncthreads();
+  if (warp == 0) {
+    double m2 = pmax[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) m2 = fmax(m2, pmax[w][lane]);
+    const int e = row_exponent(m2);
+    es[lane] = e;
+    if (i0 + lane < inner) exps[b * inner + i0 + lane] = e;
+  }
+  __syncthreads();
+  const int cpr = kp / 8;  // 8-byte chunks per digit row
+  for (int item = threadIdx.x; item < 32 * cpr; item += 256) {
+    const int i = item / cpr, c = item % cpr;
+    if (i0 + i >= inner) continue;
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = c * 8 + j;
+      v[j] = k < K ? tile[k * 33 + i] : 0.0;
+    }
+    uint64_t w[OZ_S];
+    split8(v, es[i], w);
+    const int64_t m = b * inner + i0 + i;
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s)
+      *reinterpret_cast<uint64_t*>(digits + ((int64_t)s * rows_p + m) * kp + c * 8) = w[s];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// tcgen05 GEMM
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// K-major operand tile of 128-byte rows written by TMA with SWIZZLE_128B: 8-row atoms 1024 B apart
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+constexpr int OZ_STAGES = 6;
+// data digit order within a k chunk: digit i feeds S - i digit pairs, so heavy and light stages alternate to
+// keep the TMA ring ahead of the MMAs (digit 0 first: it initialises every accumulator)
+__device__ __forceinline__ int oz_digit(int pos) { return (pos & 1) ? OZ_S - 1 - (pos >> 1) : (pos >> 1); }
+constexpr int OZ_XBYTES = OZ_BM * OZ_BK;  // one data digit plane chunk: 128 rows x 128 B
+constexpr int OZ_FBYTES = OZ_BN * OZ_BK;  // one factor digit plane chunk: 64 rows x 128 B
+constexpr uint32_t OZ_IDESC = (2u << 4)   // D: s32
+                              | (1u << 7) // A: s8
+                              | (1u << 10)  // B: s8
+                              | ((uint32_t)(OZ_BN >> 3) << 17) | ((uint32_t)(OZ_BM >> 4) << 24);
+
+struct OzKernelArgs {
+  int64_t M, Nf;     // data rows, factor rows
+  int64_t x_rows_p, f_rows_p;
+  int KC;            // 128-wide k chunks
+  int mt, nt;        // tiles along M and Nf
+  const int32_t* ex;
+  const int32_t* ef;
+  double* y;
+  int64_t inner, bstride, mstride, fstride;
+  const double* lamD;
+  const double* lamF;
+  const int* skip;
+  int dbg;  // experiments (FDIGA_OZ_DBG): bit 0 = no epilogue work, bit 1 = no MMAs
+};
+
+// 2^k for |k| <= 2044 as a product of two normal powers (each built from its bits)
+__device__ __forceinline__ double pow2(int k) {
+  k = max(-2044, min(2044, k));
+  const int k1 = k / 2, k2 = k - k1;
+  return __longlong_as_double((long long)(k1 + 1023) << 52) * __longlong_as_double((long long)(k2 + 1023) << 52);
+}
+
+template <bool LAM>
+__global__ void __launch_bounds__(192, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap xmap,
+                                                         const __grid_constant__ CUtensorMap fmap, OzKernelArgs a) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (a.skip && *a.skip) return;
+  extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
+  const int KC = a.KC;
+  uint8_t* sF = smem;                                 // [S][KC] factor chunks (resident)
+  uint8_t* sX = smem + OZ_S * KC * OZ_FBYTES;         // data ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_STAGES * OZ_XBYTES);
+  uint64_t* empty = full + OZ_STAGES;
+  uint64_t* fbar = empty + OZ_STAGES;
+  uint64_t* tfull = fbar + 1;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+  double* sLF = reinterpret_cast<double*>(tempty + 2);  // eigenvalues of the CTA's factor rows (divide)
+  double* sSF = sLF + OZ_BN;                              // 2^(e_f - 7 (S + 1)) of the CTA's factor rows
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(fbar, 1);
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  // tile sequence of this CTA: column tile nt0 fixed, row tiles strided
+  const int per_nt = gridDim.x / a.nt;
+  const int nt0 = blockIdx.x % a.nt;
+  const int mt_first = blockIdx.x / a.nt;
+  const int n0 = nt0 * OZ_BN;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      // resident factor digit planes of this column tile
+      mbar_arrive_expect_tx(fbar, (uint32_t)(OZ_S * KC * OZ_FBYTES));
+      for (int s = 0; s < OZ_S; ++s)
+        for (int kc = 0; kc < KC; ++kc)
+          tma_load_2d(sF + (s * KC + kc) * OZ_FBYTES, &fmap, kc * OZ_BK, (int)(s * a.f_rows_p + n0), fbar);
+      uint32_t g = 0;
+      for (int mt = mt_first; mt < a.mt; mt += per_nt) {
+        const int m0 = mt * OZ_BM;
+        for (int kc = 0; kc < KC; ++kc)
+          for (int pos = 0; pos < OZ_S; ++pos, ++g) {
+            const int i = oz_digit(pos);
+            const uint32_t st = g % OZ_STAGES;
+            if (g >= OZ_STAGES) mbar_wait(&empty[st], ((g / OZ_STAGES) - 1) & 1);
+            mbar_arrive_expect_tx(&full[st], OZ_XBYTES);
+            tma_load_2d(sX + st * OZ_XBYTES, &xmap, kc * OZ_BK, (int)(i * a.x_rows_p + m0), &full[st]);
+          }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      mbar_wait(fbar, 0);
+      tc_fence_after();
+      const uint32_t sf0 = smem_u32(sF), sx0 = smem_u32(sX);
+      uint32_t g = 0, tl = 0;
+      for (int mt = mt_first; mt < a.mt; mt += per_nt, ++tl) {
+        if (tl > 0) {
+          mbar_wait(tempty, (tl - 1) & 1);  // the epilogue has read the previous tile's accumulators
+          tc_fence_after();
+        }
+        for (int kc = 0; kc < KC; ++kc)
+          for (int pos = 0; pos < OZ_S; ++pos, ++g) {
+            const int i = oz_digit(pos);
+            const uint32_t st = g % OZ_STAGES;
+            mbar_wait(&full[st], (g / OZ_STAGES) & 1);
+            tc_fence_after();
+            const uint64_t da = sdesc_sw128(sx0 + st * OZ_XBYTES);
+            // digit pairs (i + 1, j + 1) with i + j + 2 <= S + 1 -> accumulator i + j
+            for (int j = 0; j + i < OZ_S; ++j) {
+              const uint64_t db = sdesc_sw128(sf0 + (j * KC + kc) * OZ_FBYTES);
+              const uint32_t td = tbase + (uint32_t)((i + j) * OZ_BN);
+              if (!(a.dbg & 2))
+#pragma unroll
+                for (int kk = 0; kk < OZ_BK / 32; ++kk)
+                  mma_i8(td, da + 2 * kk, db + 2 * kk, OZ_IDESC, (kc | i | kk) ? 1u : 0u);
+            }
+            tc_commit(&empty[st]);  // frees the ring slot when these MMAs have read it
+          }
+        tc_commit(tfull);
+      }
+    }
+  } else {
+    // epilogue: warp w owns TMEM lanes 32w..32w+31 = data rows m0 + 32w + lane
+    if (threadIdx.x < OZ_BN) {
+      const int64_t f = n0 + threadIdx.x;
+      sSF[threadIdx.x] = pow2(f < a.Nf ? a.ef[f] - 7 * (OZ_S + 1) : 0);
+      sLF[threadIdx.x] = (LAM && f < a.Nf) ? a.lamF[f] : 0.0;
+    }
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");  // epilogue warps only
+    uint32_t tl = 0;
+    for (int mt = mt_first; mt < a.mt; mt += per_nt, ++tl) {
+      mbar_wait(tfull, tl & 1);
+      tc_fence_after();
+      const int64_t m = (int64_t)mt * OZ_BM + warp * 32 + lane;
+      const bool mv = m < a.M;
+      const int64_t mm = mv ? m : 0;
+      const int64_t row_off = (mm / a.inner) * a.bstride + (mm % a.inner) * a.mstride;
+      const double sx = pow2(mv ? a.ex[mm] : 0);
+      const double lamd = (LAM && mv) ? a.lamD[mm] : 0.0;
+      const uint32_t taddr = tbase + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < ((a.dbg & 1) ? 0 : OZ_BN); c += 8) {
+        uint32_t v[OZ_S][8];
+#pragma unroll
+        for (int t = 0; t < OZ_S; ++t)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(v[t][0]), "=r"(v[t][1]), "=r"(v[t][2]), "=r"(v[t][3]), "=r"(v[t][4]), "=r"(v[t][5]),
+                         "=r"(v[t][6]), "=r"(v[t][7])
+                       : "r"(taddr + (uint32_t)(t * OZ_BN + c)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (!mv) continue;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int64_t f = n0 + c + q;
+          // sum_t 2^{-7(t+2)} C_t in units of 2^{-7(S+1)}: the weighted integers are summed exactly in two
+          // int64 halves (|C_t| < 2^26), then converted and added once
+          static_assert(OZ_S == 7, "digit-weight combination written for S = 7");
+          const long long lo = (long long)(int32_t)v[6][q] + (long long)(int32_t)v[5][q] * (1ll << 7) +
+                               (long long)(int32_t)v[4][q] * (1ll << 14) + (long long)(int32_t)v[3][q] * (1ll << 21);
+          const long long hi = (long long)(int32_t)v[2][q] + (long long)(int32_t)v[1][q] * (1ll << 7) +
+                               (long long)(int32_t)v[0][q] * (1ll << 14);
+          const double s = fma((double)hi, 268435456.0, (double)lo);  // hi 2^28 + lo
+          // two exact power-of-two scalings: the factor row's (with the digit weight) and the data row's
+          double yv = (s * sSF[c + q]) * sx;
+          if (LAM) yv = yv / (lamd + sLF[c + q]);
+          if (f < a.Nf) a.y[row_off + f * a.fstride] = yv;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+}
+
+// ---------------------------------------------------------------------------------------------
+// host
+// ---------------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int get_encode(EncodeTiledFn* fn) {
+  static EncodeTiledFn f = nullptr;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (err == cudaSuccess && q == cudaDriverEntryPointSuccess) f = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  FDIGA_CHECK(f, FDIGA_ERR_CUDA, "cuTensorMapEncodeTiled not available (%s)", cudaGetErrorString(err));
+  *fn = f;
+  return FDIGA_OK;
+}
+
+constexpr size_t oz_smem_bytes(int KC) {
+  return 1024 + (size_t)OZ_S * KC * OZ_FBYTES + (size_t)OZ_STAGES * OZ_XBYTES + (2 * OZ_STAGES + 3) * 8 + 16 +
+         OZ_BN * 2 * sizeof(double);
+}
+
+}  // namespace
+
+int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows) {
+  const int64_t kp = (k + OZ_BK - 1) / OZ_BK * OZ_BK;
+  const int64_t rows_p = (rows + box_rows - 1) / box_rows * box_rows;
+  FDIGA_CHECK(kp <= OZ_MAXKP, FDIGA_ERR_NOT_SUPPORTED, "int8-split FD: contraction length %lld > %d",
+              (long long)k, OZ_MAXKP);
+  if (op.digits && op.rows_p == rows_p && op.kp == kp && op.box_rows == box_rows) {
+    op.rows = rows;
+    return FDIGA_OK;
+  }
+  op.release();
+  FDIGA_CUDA(cudaMalloc(&op.digits, (size_t)OZ_S * rows_p * kp));
+  FDIGA_CUDA(cudaMemset(op.digits, 0, (size_t)OZ_S * rows_p * kp));
+  FDIGA_CUDA(cudaMalloc(&op.exps, (size_t)rows_p * sizeof(int32_t)));
+  FDIGA_CUDA(cudaMemset(op.exps, 0, (size_t)rows_p * sizeof(int32_t)));
+  op.rows = rows;
+  op.rows_p = rows_p;
+  op.kp = kp;
+  op.box_rows = box_rows;
+  EncodeTiledFn enc;
+  FDIGA_TRY(get_encode(&enc));
+  cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)(OZ_S * rows_p)};
+  cuuint64_t strides[1] = {(cuuint64_t)kp};
+  cuuint32_t box[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  static_assert(sizeof(CUtensorMap) <= sizeof(op.tmap), "tensor map size");
+  const CUresult r = enc(reinterpret_cast<CUtensorMap*>(op.tmap), CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, op.digits, dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  FDIGA_CHECK(r == CUDA_SUCCESS, FDIGA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return FDIGA_OK;
+}
+
+int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch, int64_t K, int64_t inner,
+             int64_t ldx, OzOperand& op, const int* skip) {
+  const int64_t rows = batch * inner;
+  FDIGA_CHECK(rows == op.rows && K <= op.kp, FDIGA_ERR_INVALID_ARG, "oz_split: operand shape mismatch");
+  if (rows == 0) return FDIGA_OK;
+  if (inner == 1) {
+    const unsigned grid = (unsigned)((rows + 7) / 8);
+    if (op.kp <= 256)
+      oz_split_rows_kernel<1><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.rows_p, (int)op.kp, skip);
+    else
+      oz_split_rows_kernel<2><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.rows_p, (int)op.kp, skip);
+  } else {
+    const size_t smem = (size_t)K * 33 * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      FDIGA_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    const int64_t tiles = batch * ((inner + 31) / 32);
+    oz_split_cols_kernel<<<(unsigned)tiles, 256, smem, stream>>>(x, batch, (int)K, inner, op.digits, op.exps,
+                                                                  op.rows_p, (int)op.kp, skip);
+  }
+  count_launch(ctx);
+  FDIGA_CUDA(cudaGetLastError());
+  return FDIGA_OK;
+}
+
+int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
+  const OzOperand& X = *g.X;
+  const OzOperand& F = *g.F;
+  FDIGA_CHECK(X.kp == F.kp && X.box_rows == OZ_BM && F.box_rows == OZ_BN, FDIGA_ERR_INVALID_ARG,
+              "oz_gemm: operand mismatch");
+  if (X.rows == 0 || F.rows == 0) return FDIGA_OK;
+  OzKernelArgs a{};
+  a.M = X.rows;
+  a.Nf = F.rows;
+  a.x_rows_p = X.rows_p;
+  a.f_rows_p = F.rows_p;
+  a.KC = (int)(X.kp / OZ_BK);
+  a.mt = (int)(X.rows_p / OZ_BM);
+  a.nt = (int)(F.rows_p / OZ_BN);
+  a.ex = X.exps;
+  a.ef = F.exps;
+  a.y = g.y;
+  a.inner = g.inner;
+  a.bstride = g.bstride;
+  a.mstride = g.mstride;
+  a.fstride = g.fstride;
+  a.lamD = g.lamD;
+  a.lamF = g.lamF;
+  a.skip = g.skip;
+  {
+    static const int dbg = getenv("FDIGA_OZ_DBG") ? atoi(getenv("FDIGA_OZ_DBG")) : 0;
+    a.dbg = dbg;
+  }
+  FDIGA_CHECK(a.nt <= ctx->sm_count, FDIGA_ERR_NOT_SUPPORTED, "oz_gemm: too many column tiles");
+  const size_t smem = oz_smem_bytes(a.KC);
+  static bool attr = false;
+  if (!attr) {
+    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)oz_smem_bytes(OZ_MAXKP / OZ_BK)));
+    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)oz_smem_bytes(OZ_MAXKP / OZ_BK)));
+    attr = true;
+  }
+  // persistent grid: a multiple of the column-tile count, at most one CTA per SM (TMEM: 512 columns)
+  int64_t grid = (int64_t)(ctx->sm_count / a.nt) * a.nt;
+  grid = std::min<int64_t>(grid, (int64_t)a.mt * a.nt);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = 0;
+  cfg.attrs = attr_pdl;
+  cfg.numAttrs = 1;
+  if (a.lamD)
+    FDIGA_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<true>, *reinterpret_cast<const CUtensorMap*>(X.tmap),
+                                  *reinterpret_cast<const CUtensorMap*>(F.tmap), a));
+  else
+    FDIGA_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<false>, *reinterpret_cast<const CUtensorMap*>(X.tmap),
+                                  *reinterpret_cast<const CUtensorMap*>(F.tmap), a));
+  count_launch(ctx);
+  FDIGA_CUDA(cudaGetLastError());
+  return FDIGA_OK;
+}
+
+}  // namespace fdiga

@@ -1,0 +1,53 @@
+// FD mode products on the 5th-generation tensor cores: FP64 contractions by exact int8 splitting
+// ("Ozaki scheme") on tcgen05.mma.kind::i8 with TMEM accumulators (oz.cu).
+//
+// Every operand row (a row of the factor W_l / U_l, or a fibre of the data tensor along the contracted
+// axis) is written as x = 2^e sum_{i=1..S} a_i 2^{-7i} with int8 digits a_i (|a_i| <= 127, truncated, so
+// the split is exact up to 2^{-7S} of the row's magnitude).  A contraction sum_k f_k x_k is then
+//   2^{e_f + e_x} sum_{t=2..S+1} 2^{-7t} C_t,   C_t = sum_{i+j=t} sum_k f_{k,j} x_{k,i}   (int32, exact)
+// and only the final FP64 combination of the S integer accumulators rounds.  The digit pairs with
+// i + j > S + 1 are dropped: with S = 7 both the split and the dropped pairs are below 2^{-48} of the
+// row magnitudes, i.e. of the order of FP64 rounding of the same dot product.
+#pragma once
+#include "common.cuh"
+
+namespace fdiga {
+
+constexpr int OZ_S = 7;      // int8 digits per operand
+constexpr int OZ_BM = 128;   // data rows per tile (TMEM lanes)
+constexpr int OZ_BN = 64;    // factor rows per tile (TMEM columns per accumulator)
+constexpr int OZ_BK = 128;   // bytes (= k) per TMA box row (SWIZZLE_128B)
+constexpr int OZ_MAXKP = 256;  // resident factor slices: S x BN x Kp bytes of shared memory
+
+// Split operand: S digit planes [S][rows_p][kp] (int8, k contiguous, zero padded) and the row
+// exponents e[rows_p]; the tensor map views the planes as a 2D [S rows_p] x [kp] int8 matrix.
+struct OzOperand {
+  int8_t* digits = nullptr;
+  int32_t* exps = nullptr;
+  int64_t rows = 0, rows_p = 0, kp = 0;
+  int box_rows = 0;
+  alignas(64) unsigned char tmap[128];  // CUtensorMap
+  void release();
+};
+
+// Allocate (or grow) an operand for `rows` rows of k values; box_rows = OZ_BM (data) or OZ_BN (factor).
+int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows);
+// Split x (element (b, k, i) at x[b K inner + k inner + i]; for inner == 1 row b at x[b ldx]) into op,
+// row m = b inner + i, on `stream`.
+int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch, int64_t K, int64_t inner,
+             int64_t ldx, OzOperand& op, const int* skip);
+
+// y[off(m, f)] = sum_k F[f][k] X[m][k]  (/ (lamD[m] + lamF[f]) when lamD != nullptr), for data rows m < M
+// and factor rows f < Nf, off(m, f) = (m / inner) bstride + (m % inner) mstride + f fstride.
+struct OzGemmArgs {
+  const OzOperand* X;  // data (M rows)
+  const OzOperand* F;  // factor (Nf rows)
+  double* y;
+  int64_t inner, bstride, mstride, fstride;
+  const double* lamD;
+  const double* lamF;
+  const int* skip;
+};
+int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& a);
+
+}  // namespace fdiga
