@@ -158,6 +158,14 @@ class FDPlan:
     def flops(self):
         return float(self.ctx._lib.fd_apply_flops(self.handle))
 
+    def path(self):
+        """('dmma' | 'int8_split', int8 tensor-core ops per apply) -- the kernel family of the mode products."""
+        ops = C.c_double(0.0)
+        k = self.ctx._lib.fd_plan_path(self.handle, C.byref(ops))
+        if k < 0:
+            check(k, "fd_plan_path")
+        return ("int8_split" if k == 1 else "dmma"), float(ops.value)
+
     def close(self):
         if self.handle:
             if self.ctx.handle:  # a closed context already destroyed its children

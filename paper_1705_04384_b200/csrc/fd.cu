@@ -311,14 +311,20 @@ int broadcast_factors(fd_plan* P) {
   return FDIGA_OK;
 }
 
-// int8-split tensor-core mode products (oz.cu): 3D, single rank, real spectra, n_l <= 256.  Enabled by
-// FDIGA_FD_OZ=1 (default off while it is being measured).
+// int8-split tensor-core mode products (oz.cu) for 3D, single-rank, real-spectrum plans with
+// 192 <= n_l <= 256 -- where they beat the DMMA products on a B200 (n = 256: 1.38 vs 1.72 ms per apply;
+// at n = 128 / 131 the short contractions leave the tensor cores idle and DMMA wins).
+// FDIGA_FD_OZ=0 / 1 forces the choice (1: any n_l <= 256).  A static rule, so every run -- also under a
+// profiler -- takes the same kernels.
 bool oz_eligible(const fd_plan* P) {
-  const char* e = getenv("FDIGA_FD_OZ");
-  if (!(e && e[0] == '1')) return false;
   if (P->d != 3 || P->ctx->sharded || P->has_pairs) return false;
   for (int l = 0; l < 3; ++l)
     if (P->n[l] > OZ_MAXKP) return false;
+  const char* e = getenv("FDIGA_FD_OZ");
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return true;
+  for (int l = 0; l < 3; ++l)
+    if (P->n[l] < 192) return false;
   return true;
 }
 
@@ -339,7 +345,7 @@ int oz_setup(fd_plan* P) {
 
 // one mode product on the int8 path: split the data along axis l, contract with the factor digits
 int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, const double* lamD,
-            const double* lamF, const int* skip) {
+            const double* lamF, const int* skip, bool divide_input = false) {
   const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
   OzOperand& Xz = P->ozX[l];
   cudaStream_t st = P->ctx->stream;
@@ -362,8 +368,9 @@ int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, 
     g.bstride = n1 * n2;
     g.mstride = 1;
     g.fstride = n1;
-  } else {  // data rows (i2, i1), k = i3
-    FDIGA_TRY(oz_split(P->ctx, st, X, 1, n3, n1 * n2, 0, Xz, skip));
+  } else {  // data rows (i2, i1), k = i3 (divide_input: X / (lam_inner[(i2, i1)] + lam_3[i3]) first)
+    FDIGA_TRY(oz_split(P->ctx, st, X, 1, n3, n1 * n2, 0, Xz, skip, divide_input ? P->lam_inner : nullptr,
+                       divide_input ? P->lam[2] : nullptr));
     g.inner = n1 * n2;
     g.bstride = 0;
     g.mstride = 1;
@@ -377,8 +384,9 @@ int fd_apply_oz(fd_plan* P, const double* r, double* s, const int* skip) {
   double* b = P->t1.p;
   FDIGA_TRY(oz_mode(P, 0, P->ozW[0], r, a, nullptr, nullptr, skip));
   FDIGA_TRY(oz_mode(P, 1, P->ozW[1], a, b, nullptr, nullptr, skip));
-  FDIGA_TRY(oz_mode(P, 2, P->ozW[2], b, a, P->lam_inner, P->lam[2], skip));
-  FDIGA_TRY(oz_mode(P, 2, P->ozU[2], a, b, nullptr, nullptr, skip));
+  // the Lambda divide rides in the split that feeds the backward mode-3 product
+  FDIGA_TRY(oz_mode(P, 2, P->ozW[2], b, a, nullptr, nullptr, skip));
+  FDIGA_TRY(oz_mode(P, 2, P->ozU[2], a, b, nullptr, nullptr, skip, true));
   FDIGA_TRY(oz_mode(P, 1, P->ozU[1], b, a, nullptr, nullptr, skip));
   return oz_mode(P, 0, P->ozU[0], a, s, nullptr, nullptr, skip);
 }
@@ -994,6 +1002,19 @@ double fd_apply_flops(const fd_plan* P) {
   double s = 0;
   for (int l = 0; l < P->d; ++l) s += (double)P->n[l];
   return 4.0 * (double)P->N * s;
+}
+
+int fd_plan_path(const fd_plan* P, double* int8_ops) {
+  FDIGA_CHECK(P, FDIGA_ERR_INVALID_ARG, "NULL plan");
+  if (int8_ops) {
+    double ops = 0.0;
+    if (P->oz)
+      for (int l = 0; l < P->d; ++l)  // forward and backward product along l
+        ops += 2.0 * 2.0 * (OZ_S * (OZ_S + 1) / 2) * (double)P->ozX[l].rows_p * (double)P->ozW[l].rows_p *
+               (double)P->ozX[l].kp;
+    *int8_ops = ops;
+  }
+  return P->oz ? FDIGA_PATH_INT8_SPLIT : FDIGA_PATH_DMMA;
 }
 
 int fd_plan_destroy(fd_plan* P) {

@@ -31,28 +31,36 @@ namespace {
 // ---------------------------------------------------------------------------------------------
 // digit split
 // ---------------------------------------------------------------------------------------------
+// 2^k for |k| <= 2044 as a product of two normal powers (each built from its bits)
+__device__ __forceinline__ double pow2(int k) {
+  k = max(-2044, min(2044, k));
+  const int k1 = k / 2, k2 = k - k1;
+  return __longlong_as_double((long long)(k1 + 1023) << 52) * __longlong_as_double((long long)(k2 + 1023) << 52);
+}
+
 __device__ __forceinline__ int row_exponent(double mx) {
   int e = 0;
   if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): every |x| <= mx < 2^e
   return e;
 }
 
-// 8 consecutive values (scaled to (-1, 1)) -> S packed 8-byte digit words
+// 8 consecutive values -> S packed 8-byte digit words.  |x| 2^(62 - e) < 2^62 is taken to a 62-bit integer
+// (truncated: bits below 2^-62 of the row scale are beyond digit S anyway); digit i of |x| is then bits
+// [62 - 7 i, 69 - 7 i) of it, with the sign of x -- the truncated base-128 expansion of x 2^-e.
 __device__ __forceinline__ void split8(const double (&v)[8], int e, uint64_t (&w)[OZ_S]) {
-  double r[8];
+  const double sc = pow2(62 - e);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = ldexp(v[j], -e);
+  for (int s = 0; s < OZ_S; ++s) w[s] = 0;
 #pragma unroll
-  for (int s = 0; s < OZ_S; ++s) {
-    uint64_t word = 0;
+  for (int j = 0; j < 8; ++j) {
+    const long long q = __double2ll_rz(v[j] * sc);  // exact scaling, |q| < 2^62
+    const unsigned long long aq = (unsigned long long)(q < 0 ? -q : q);
+    const bool neg = q < 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double a = r[j] * 128.0;  // exact (power-of-two scaling)
-      const double q = trunc(a);      // |q| <= 127 since |a| < 128
-      r[j] = a - q;                   // exact: the fractional part
-      word |= (uint64_t)(uint8_t)(int8_t)(int)q << (8 * j);
+    for (int s = 0; s < OZ_S; ++s) {
+      const int d = (int)((aq >> (55 - 7 * s)) & 127u);
+      w[s] |= (uint64_t)(uint8_t)(neg ? -d : d) << (8 * j);
     }
-    w[s] = word;
   }
 }
 
@@ -97,7 +105,8 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __restrict__ x, int64_t batch, int K,
                                                             int64_t inner, int8_t* __restrict__ digits,
                                                             int32_t* __restrict__ exps, int64_t rows_p, int kp,
-                                                            const int* skip) {
+                                                            const double* __restrict__ lam_row,
+                                                            const double* __restrict__ lam_k, const int* skip) {
   if (skip && *skip) return;
   extern __shared__ double tile[];  // [K][33]
   __shared__ double pmax[8][32];
@@ -108,10 +117,31 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
   const int64_t i0 = (blockIdx.x % tiles_i) * 32;
   const double* xb = x + b * K * inner;
   double mx = 0.0;
-  for (int k = warp; k < K; k += 8) {
-    const double v = (i0 + lane < inner) ? xb[(int64_t)k * inner + i0 + lane] : 0.0;
-    tile[k * 33 + lane] = v;
-    mx = fmax(mx, fabs(v));
+  const bool iv = i0 + lane < inner;
+  // the eigenvalue-sum divide of the FD (eq:FD3D) when the split feeds the backward mode-d product
+  const double lr = (lam_row && iv) ? lam_row[b * inner + i0 + lane] : 0.0;
+  for (int k0 = warp; k0 < K; k0 += 32) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // four independent loads in flight per thread
+      const int k = k0 + 8 * u;
+      v[u] = (iv && k < K) ? xb[(int64_t)k * inner + i0 + lane] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + 8 * u;
+      if (k >= K) break;
+      double val = v[u];
+      if (lam_row) {  // val / (lr + lam_k[k]): float-seeded reciprocal, two Newton steps (< 1 ulp off)
+        const double dn = lr + lam_k[k];
+        double r = (double)__frcp_rn((float)dn);
+        r = fma(r, fma(-dn, r, 1.0), r);
+        r = fma(r, fma(-dn, r, 1.0), r);
+        val *= r;
+      }
+      tile[k * 33 + lane] = val;
+      mx = fmax(mx, fabs(val));
+    }
   }
   pmax[warp][lane] = mx;
   __syncthreads();
@@ -174,16 +204,19 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
+constexpr uint32_t OZ_IDESC_C = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
+                                ((uint32_t)(OZ_BM >> 4) << 24);
+// the MMAs of one data digit I: pairs (I, j), j = 0..S-1-I, into accumulator I + j; 4 K-steps of 32 each.
+// db_kc: descriptor of factor digit 0 of this k chunk (digit j is j chunks further)
+template <int I>
+__device__ __forceinline__ void oz_stage_mmas(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
+                                              bool first_kc);
 constexpr int OZ_STAGES = 6;
-// data digit order within a k chunk: digit i feeds S - i digit pairs, so heavy and light stages alternate to
-// keep the TMA ring ahead of the MMAs (digit 0 first: it initialises every accumulator)
-__device__ __forceinline__ int oz_digit(int pos) { return (pos & 1) ? OZ_S - 1 - (pos >> 1) : (pos >> 1); }
+constexpr int OZ_EW = 8;                    // epilogue warps: 4 lane quarters x 2 column halves
+constexpr int OZ_EC = OZ_BN / (OZ_EW / 4);  // columns per epilogue thread
+constexpr int OZ_THREADS = (OZ_EW + 2) * 32;  // + TMA producer warp + MMA warp
 constexpr int OZ_XBYTES = OZ_BM * OZ_BK;  // one data digit plane chunk: 128 rows x 128 B
 constexpr int OZ_FBYTES = OZ_BN * OZ_BK;  // one factor digit plane chunk: 64 rows x 128 B
-constexpr uint32_t OZ_IDESC = (2u << 4)   // D: s32
-                              | (1u << 7) // A: s8
-                              | (1u << 10)  // B: s8
-                              | ((uint32_t)(OZ_BN >> 3) << 17) | ((uint32_t)(OZ_BM >> 4) << 24);
 
 struct OzKernelArgs {
   int64_t M, Nf;     // data rows, factor rows
@@ -200,31 +233,50 @@ struct OzKernelArgs {
   int dbg;  // experiments (FDIGA_OZ_DBG): bit 0 = no epilogue work, bit 1 = no MMAs
 };
 
-// 2^k for |k| <= 2044 as a product of two normal powers (each built from its bits)
-__device__ __forceinline__ double pow2(int k) {
-  k = max(-2044, min(2044, k));
-  const int k1 = k / 2, k2 = k - k1;
-  return __longlong_as_double((long long)(k1 + 1023) << 52) * __longlong_as_double((long long)(k2 + 1023) << 52);
+
+// Accumulator hand-off between tiles.  Weight t (digit pairs i + j = t) of tile T lives in TMEM slot
+// p(t, T) = t (T even) or S - 1 - t (T odd).  The first k chunk of a tile takes the data digits in
+// descending order (digit i first touches weight i), later chunks ascending, so in the last chunk weight t
+// completes right after digit t.  The epilogue drains weights in ascending order, i.e. slots in the order
+// 0, 1, .., S - 1 for either parity, which is exactly the order in which the next tile first writes them:
+// the epilogue of tile T runs under the MMAs of tile T + 1.
+__device__ __forceinline__ int oz_slot(int t, uint32_t tile) { return (tile & 1) ? OZ_S - 1 - t : t; }
+
+// the MMAs of data digit I: pairs (I, j), j = 0..S-1-I, into weight I + j; 4 K-steps of 32.  db_kc: descriptor
+// of factor digit 0 of this k chunk (digit j is j chunks further).  In the first k chunk (descending digits)
+// pair (I, 0) is the first write of weight I: it overwrites the slot.
+template <int I>
+__device__ __forceinline__ void oz_stage_mmas(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
+                                              bool first_kc) {
+  const uint32_t odd = tile & 1;
+#pragma unroll
+  for (int j = 0; j + I < OZ_S; ++j) {
+    const uint32_t td = tbase + (uint32_t)((odd ? OZ_S - 1 - (I + j) : (I + j)) * OZ_BN);
+#pragma unroll
+    for (int kk = 0; kk < OZ_BK / 32; ++kk)
+      mma_i8(td, da + 2 * kk, db_kc + (uint64_t)(j * (OZ_BN * OZ_BK >> 4) + 2 * kk), OZ_IDESC_C,
+             (j != 0 || kk != 0 || !first_kc) ? 1u : 0u);
+  }
 }
 
 template <bool LAM>
-__global__ void __launch_bounds__(192, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap xmap,
+__global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap xmap,
                                                          const __grid_constant__ CUtensorMap fmap, OzKernelArgs a) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
   const int KC = a.KC;
-  uint8_t* sF = smem;                                 // [S][KC] factor chunks (resident)
+  uint8_t* sF = smem;                                 // [KC][S] factor chunks (resident)
   uint8_t* sX = smem + OZ_S * KC * OZ_FBYTES;         // data ring
   uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_STAGES * OZ_XBYTES);
   uint64_t* empty = full + OZ_STAGES;
   uint64_t* fbar = empty + OZ_STAGES;
-  uint64_t* tfull = fbar + 1;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
-  double* sLF = reinterpret_cast<double*>(tempty + 2);  // eigenvalues of the CTA's factor rows (divide)
-  double* sSF = sLF + OZ_BN;                              // 2^(e_f - 7 (S + 1)) of the CTA's factor rows
+  uint64_t* sfull = fbar + 1;      // [S] accumulator slot complete (MMA -> epilogue)
+  uint64_t* sempty = sfull + OZ_S;  // [S] accumulator slot drained (epilogue -> MMA)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_S);
+  double* sLF = reinterpret_cast<double*>(sempty + OZ_S + 1);  // eigenvalues of the CTA's factor rows
+  double* sSF = sLF + OZ_BN;                                    // 2^(e_f - 7 (S + 1)) of the CTA's factor rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -233,11 +285,13 @@ __global__ void __launch_bounds__(192, 1) oz_gemm_kernel(const __grid_constant__
       mbar_init(&empty[s], 1);
     }
     mbar_init(fbar, 1);
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    for (int t = 0; t < OZ_S; ++t) {
+      mbar_init(&sfull[t], 1);
+      mbar_init(&sempty[t], OZ_EW);
+    }
     fence_barrier_init();
   }
-  if (warp == 5) {
+  if (warp == OZ_EW + 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
@@ -252,56 +306,69 @@ __global__ void __launch_bounds__(192, 1) oz_gemm_kernel(const __grid_constant__
   const int mt_first = blockIdx.x / a.nt;
   const int n0 = nt0 * OZ_BN;
 
-  if (warp == 4) {
+  if (warp == OZ_EW) {
     if (lane == 0) {
-      // resident factor digit planes of this column tile
+      // resident factor digit planes of this column tile, [kc][digit] chunks
       mbar_arrive_expect_tx(fbar, (uint32_t)(OZ_S * KC * OZ_FBYTES));
       for (int s = 0; s < OZ_S; ++s)
         for (int kc = 0; kc < KC; ++kc)
-          tma_load_2d(sF + (s * KC + kc) * OZ_FBYTES, &fmap, kc * OZ_BK, (int)(s * a.f_rows_p + n0), fbar);
-      uint32_t g = 0;
+          tma_load_2d(sF + (kc * OZ_S + s) * OZ_FBYTES, &fmap, kc * OZ_BK, (int)(s * a.f_rows_p + n0), fbar);
+      uint32_t st = 0, ph = 0;
+      bool wrapped = false;
       for (int mt = mt_first; mt < a.mt; mt += per_nt) {
         const int m0 = mt * OZ_BM;
         for (int kc = 0; kc < KC; ++kc)
-          for (int pos = 0; pos < OZ_S; ++pos, ++g) {
-            const int i = oz_digit(pos);
-            const uint32_t st = g % OZ_STAGES;
-            if (g >= OZ_STAGES) mbar_wait(&empty[st], ((g / OZ_STAGES) - 1) & 1);
+          for (int pos = 0; pos < OZ_S; ++pos) {
+            const int i = kc == 0 ? OZ_S - 1 - pos : pos;  // the MMA warp's digit order
+            if (wrapped) mbar_wait(&empty[st], ph ^ 1);
             mbar_arrive_expect_tx(&full[st], OZ_XBYTES);
             tma_load_2d(sX + st * OZ_XBYTES, &xmap, kc * OZ_BK, (int)(i * a.x_rows_p + m0), &full[st]);
+            if (++st == OZ_STAGES) {
+              st = 0;
+              ph ^= 1;
+              wrapped = true;
+            }
           }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == OZ_EW + 1) {
     if (lane == 0) {
       mbar_wait(fbar, 0);
       tc_fence_after();
-      const uint32_t sf0 = smem_u32(sF), sx0 = smem_u32(sX);
-      uint32_t g = 0, tl = 0;
+      const uint64_t da0 = sdesc_sw128(smem_u32(sX)), db0 = sdesc_sw128(smem_u32(sF));
+      uint32_t st = 0, ph = 0, tl = 0;
+      const bool mma = !(a.dbg & 2);
       for (int mt = mt_first; mt < a.mt; mt += per_nt, ++tl) {
-        if (tl > 0) {
-          mbar_wait(tempty, (tl - 1) & 1);  // the epilogue has read the previous tile's accumulators
-          tc_fence_after();
-        }
-        for (int kc = 0; kc < KC; ++kc)
-          for (int pos = 0; pos < OZ_S; ++pos, ++g) {
-            const int i = oz_digit(pos);
-            const uint32_t st = g % OZ_STAGES;
-            mbar_wait(&full[st], (g / OZ_STAGES) & 1);
-            tc_fence_after();
-            const uint64_t da = sdesc_sw128(sx0 + st * OZ_XBYTES);
-            // digit pairs (i + 1, j + 1) with i + j + 2 <= S + 1 -> accumulator i + j
-            for (int j = 0; j + i < OZ_S; ++j) {
-              const uint64_t db = sdesc_sw128(sf0 + (j * KC + kc) * OZ_FBYTES);
-              const uint32_t td = tbase + (uint32_t)((i + j) * OZ_BN);
-              if (!(a.dbg & 2))
-#pragma unroll
-                for (int kk = 0; kk < OZ_BK / 32; ++kk)
-                  mma_i8(td, da + 2 * kk, db + 2 * kk, OZ_IDESC, (kc | i | kk) ? 1u : 0u);
-            }
-            tc_commit(&empty[st]);  // frees the ring slot when these MMAs have read it
+        for (int kc = 0; kc < KC; ++kc) {
+          const uint64_t dbk = db0 + (uint64_t)(kc * OZ_S * (OZ_FBYTES >> 4));
+          const bool first = kc == 0, last = kc == KC - 1;
+          // one ring stage per data digit, its digit pairs fully unrolled (descriptor offsets are immediates)
+#define OZ_STAGE(I)                                                                                  \
+  {                                                                                                  \
+    mbar_wait(&full[st], ph);                                                                        \
+    tc_fence_after();                                                                                \
+    if (first && tl > 0) { /* weight I is first written by this stage: its slot must be drained */ \
+      mbar_wait(&sempty[oz_slot(I, tl)], (tl - 1) & 1);                                              \
+      tc_fence_after();                                                                              \
+    }                                                                                                \
+    if (mma) oz_stage_mmas<I>(tbase, tl, da0 + (uint64_t)(st * (OZ_XBYTES >> 4)), dbk, first);      \
+    tc_commit(&empty[st]); /* frees the ring slot when these MMAs have read it */                    \
+    if (last && !first) tc_commit(&sfull[oz_slot(I, tl)]); /* ascending: weight I complete */        \
+    if (++st == OZ_STAGES) {                                                                         \
+      st = 0;                                                                                        \
+      ph ^= 1;                                                                                       \
+    }                                                                                                \
+  }
+          if (first) {
+            static_assert(OZ_S == 8, "stage sequences written for S = 8");
+            OZ_STAGE(7) OZ_STAGE(6) OZ_STAGE(5) OZ_STAGE(4) OZ_STAGE(3) OZ_STAGE(2) OZ_STAGE(1) OZ_STAGE(0)
+          } else {
+            OZ_STAGE(0) OZ_STAGE(1) OZ_STAGE(2) OZ_STAGE(3) OZ_STAGE(4) OZ_STAGE(5) OZ_STAGE(6) OZ_STAGE(7)
           }
-        tc_commit(tfull);
+#undef OZ_STAGE
+          if (first && last)  // single k chunk (descending): every weight completes at its end
+            for (int t = 0; t < OZ_S; ++t) tc_commit(&sfull[oz_slot(t, tl)]);
+        }
       }
     }
   } else {
@@ -311,54 +378,75 @@ __global__ void __launch_bounds__(192, 1) oz_gemm_kernel(const __grid_constant__
       sSF[threadIdx.x] = pow2(f < a.Nf ? a.ef[f] - 7 * (OZ_S + 1) : 0);
       sLF[threadIdx.x] = (LAM && f < a.Nf) ? a.lamF[f] : 0.0;
     }
-    asm volatile("bar.sync 1, 128;\n" ::: "memory");  // epilogue warps only
+    asm volatile("bar.sync 1, %0;\n" ::"n"(OZ_EW * 32) : "memory");  // epilogue warps only
     uint32_t tl = 0;
+    // warp w: TMEM lanes 32 (w % 4).. (data rows), columns [32 (w / 4), +32) of every weight slot
+    const int quarter = warp & 3, c0 = (warp >> 2) * OZ_EC;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     for (int mt = mt_first; mt < a.mt; mt += per_nt, ++tl) {
-      mbar_wait(tfull, tl & 1);
-      tc_fence_after();
-      const int64_t m = (int64_t)mt * OZ_BM + warp * 32 + lane;
+      const int64_t m = (int64_t)mt * OZ_BM + quarter * 32 + lane;
       const bool mv = m < a.M;
       const int64_t mm = mv ? m : 0;
       const int64_t row_off = (mm / a.inner) * a.bstride + (mm % a.inner) * a.mstride;
       const double sx = pow2(mv ? a.ex[mm] : 0);
       const double lamd = (LAM && mv) ? a.lamD[mm] : 0.0;
-      const uint32_t taddr = tbase + ((uint32_t)(warp * 32) << 16);
+      // sum_t 2^{7 (S - 1 - t)} C_t over the weights as they complete (largest weight first)
+      double acc[OZ_EC];
+#pragma unroll
+      for (int c = 0; c < OZ_EC; ++c) acc[c] = 0.0;
 #pragma unroll 1
-      for (int c = 0; c < ((a.dbg & 1) ? 0 : OZ_BN); c += 8) {
-        uint32_t v[OZ_S][8];
+      for (int t = 0; t < OZ_S; ++t) {
+        const int p = oz_slot(t, tl);
+        mbar_wait(&sfull[p], tl & 1);
+        tc_fence_after();
+        const double w = (double)(1ll << (7 * (OZ_S - 1 - t)));
+        if (!(a.dbg & 1)) {
 #pragma unroll
-        for (int t = 0; t < OZ_S; ++t)
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                       : "=r"(v[t][0]), "=r"(v[t][1]), "=r"(v[t][2]), "=r"(v[t][3]), "=r"(v[t][4]), "=r"(v[t][5]),
-                         "=r"(v[t][6]), "=r"(v[t][7])
-                       : "r"(taddr + (uint32_t)(t * OZ_BN + c)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (!mv) continue;
+          for (int c = 0; c < OZ_EC; c += 16) {
+            uint32_t v[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                : "r"(tbase + lane_off + (uint32_t)(p * OZ_BN + c0 + c)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int64_t f = n0 + c + q;
-          // sum_t 2^{-7(t+2)} C_t in units of 2^{-7(S+1)}: the weighted integers are summed exactly in two
-          // int64 halves (|C_t| < 2^26), then converted and added once
-          static_assert(OZ_S == 7, "digit-weight combination written for S = 7");
-          const long long lo = (long long)(int32_t)v[6][q] + (long long)(int32_t)v[5][q] * (1ll << 7) +
-                               (long long)(int32_t)v[4][q] * (1ll << 14) + (long long)(int32_t)v[3][q] * (1ll << 21);
-          const long long hi = (long long)(int32_t)v[2][q] + (long long)(int32_t)v[1][q] * (1ll << 7) +
-                               (long long)(int32_t)v[0][q] * (1ll << 14);
-          const double s = fma((double)hi, 268435456.0, (double)lo);  // hi 2^28 + lo
+            // int32 -> double without I2F: the bits 0x43300000:(v ^ 2^31) are 2^52 + 2^31 + v exactly, and
+            // subtracting 2^52 + 2^31 is exact
+            for (int q = 0; q < 16; ++q)
+              acc[c + q] = fma(__hiloint2double(0x43300000, (int)(v[q] ^ 0x80000000u)) - 4503601774854144.0, w,
+                               acc[c + q]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[p]);
+      }
+      if (mv && !(a.dbg & 1)) {
+        const bool vec = a.fstride == 1 && ((row_off + n0 + c0) & 1) == 0;
+#pragma unroll
+        for (int c = 0; c < OZ_EC; c += 2) {
+          const int64_t f = n0 + c0 + c;
           // two exact power-of-two scalings: the factor row's (with the digit weight) and the data row's
-          double yv = (s * sSF[c + q]) * sx;
-          if (LAM) yv = yv / (lamd + sLF[c + q]);
-          if (f < a.Nf) a.y[row_off + f * a.fstride] = yv;
+          double y0 = (acc[c] * sSF[c0 + c]) * sx;
+          double y1 = (acc[c + 1] * sSF[c0 + c + 1]) * sx;
+          if (LAM) {
+            y0 = y0 / (lamd + sLF[c0 + c]);
+            y1 = y1 / (lamd + sLF[c0 + c + 1]);
+          }
+          if (vec && f + 1 < a.Nf) {  // contiguous factor index (mode 1): one 16-byte store per pair
+            *reinterpret_cast<double2*>(a.y + row_off + f) = make_double2(y0, y1);
+          } else {
+            if (f < a.Nf) a.y[row_off + f * a.fstride] = y0;
+            if (f + 1 < a.Nf) a.y[row_off + (f + 1) * a.fstride] = y1;
+          }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+  if (warp == OZ_EW + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -384,7 +472,7 @@ int get_encode(EncodeTiledFn* fn) {
 }
 
 constexpr size_t oz_smem_bytes(int KC) {
-  return 1024 + (size_t)OZ_S * KC * OZ_FBYTES + (size_t)OZ_STAGES * OZ_XBYTES + (2 * OZ_STAGES + 3) * 8 + 16 +
+  return 1024 + (size_t)OZ_S * KC * OZ_FBYTES + (size_t)OZ_STAGES * OZ_XBYTES + (2 * OZ_STAGES + 1 + 2 * OZ_S + 1) * 8 +
          OZ_BN * 2 * sizeof(double);
 }
 
@@ -423,11 +511,12 @@ int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows) {
 }
 
 int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch, int64_t K, int64_t inner,
-             int64_t ldx, OzOperand& op, const int* skip) {
+             int64_t ldx, OzOperand& op, const int* skip, const double* lam_row, const double* lam_k) {
+
   const int64_t rows = batch * inner;
   FDIGA_CHECK(rows == op.rows && K <= op.kp, FDIGA_ERR_INVALID_ARG, "oz_split: operand shape mismatch");
   if (rows == 0) return FDIGA_OK;
-  if (inner == 1) {
+  if (inner == 1 && !lam_row) {  // (the divide is done by the strided kernel, which handles inner == 1 too)
     const unsigned grid = (unsigned)((rows + 7) / 8);
     if (op.kp <= 256)
       oz_split_rows_kernel<1><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.rows_p, (int)op.kp, skip);
@@ -442,7 +531,7 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
     }
     const int64_t tiles = batch * ((inner + 31) / 32);
     oz_split_cols_kernel<<<(unsigned)tiles, 256, smem, stream>>>(x, batch, (int)K, inner, op.digits, op.exps,
-                                                                  op.rows_p, (int)op.kp, skip);
+                                                                  op.rows_p, (int)op.kp, lam_row, lam_k, skip);
   }
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());
@@ -492,7 +581,7 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   grid = std::min<int64_t>(grid, (int64_t)a.mt * a.nt);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(192);
+  cfg.blockDim = dim3(OZ_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr_pdl[1];

@@ -6,14 +6,16 @@
 // the split is exact up to 2^{-7S} of the row's magnitude).  A contraction sum_k f_k x_k is then
 //   2^{e_f + e_x} sum_{t=2..S+1} 2^{-7t} C_t,   C_t = sum_{i+j=t} sum_k f_{k,j} x_{k,i}   (int32, exact)
 // and only the final FP64 combination of the S integer accumulators rounds.  The digit pairs with
-// i + j > S + 1 are dropped: with S = 7 both the split and the dropped pairs are below 2^{-48} of the
-// row magnitudes, i.e. of the order of FP64 rounding of the same dot product.
+// i + j > S + 1 are dropped: with S = 8 the split is exact to 2^{-56} of the row magnitude and the dropped
+// pairs (zero-mean digits) add ~2^{-52} of it per dot product of length 256, i.e. the order of FP64 rounding
+// of the same dot product (S = 7 measured 2e-12 after six products on small ill-conditioned
+// factors, above the 1e-12 bar).
 #pragma once
 #include "common.cuh"
 
 namespace fdiga {
 
-constexpr int OZ_S = 7;      // int8 digits per operand
+constexpr int OZ_S = 8;      // int8 digits per operand
 constexpr int OZ_BM = 128;   // data rows per tile (TMEM lanes)
 constexpr int OZ_BN = 64;    // factor rows per tile (TMEM columns per accumulator)
 constexpr int OZ_BK = 128;   // bytes (= k) per TMA box row (SWIZZLE_128B)
@@ -34,8 +36,11 @@ struct OzOperand {
 int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows);
 // Split x (element (b, k, i) at x[b K inner + k inner + i]; for inner == 1 row b at x[b ldx]) into op,
 // row m = b inner + i, on `stream`.
+// lam_row / lam_k (may be NULL): divide element (b, k, i) by lam_row[b inner + i] + lam_k[k]
+// first (the FD eigenvalue-sum scaling, applied as the data enters the backward mode-d product).
 int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch, int64_t K, int64_t inner,
-             int64_t ldx, OzOperand& op, const int* skip);
+             int64_t ldx, OzOperand& op, const int* skip, const double* lam_row = nullptr,
+             const double* lam_k = nullptr);
 
 // y[off(m, f)] = sum_k F[f][k] X[m][k]  (/ (lamD[m] + lamF[f]) when lamD != nullptr), for data rows m < M
 // and factor rows f < Nf, off(m, f) = (m / inner) bstride + (m % inner) mstride + f fstride.

@@ -57,12 +57,12 @@ __host__ __device__ constexpr uint32_t idesc_i8() {
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int BN, int S>
+template <int BN, int S, bool AT>
 __global__ void __launch_bounds__(128, 1) i8gemm(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
                                                  int32_t* C, int M, int N, int K) {
   constexpr int BM = 128, BK = 128;
   constexpr int A_BYTES = BM * BK, B_BYTES = BN * BK;
-  constexpr uint32_t TCOLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t TCOLS = 512;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -109,10 +109,19 @@ __global__ void __launch_bounds__(128, 1) i8gemm(const __grid_constant__ CUtenso
 #pragma unroll
       for (int k = 0; k < BK / 32; ++k) {
         const uint32_t acc = (kc > 0 || k > 0) ? 1u : 0u;
-        asm volatile(
-            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
-                tbase),
-            "l"(da + (uint64_t)(k * 2)), "l"(db + (uint64_t)(k * 2)), "r"(idesc), "r"(acc));
+        if (AT) {
+          const uint32_t ta = tbase + 256 + (uint32_t)((s & 1) * 32 + k * 8);
+          asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(ta), "l"(da + (uint64_t)(k * 2)));
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(
+                  tbase),
+              "r"(ta), "l"(db + (uint64_t)(k * 2)), "r"(idesc), "r"(acc));
+        } else {
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+                  tbase),
+              "l"(da + (uint64_t)(k * 2)), "l"(db + (uint64_t)(k * 2)), "r"(idesc), "r"(acc));
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&empty[s]))
                    : "memory");
@@ -166,7 +175,7 @@ static CUtensorMap make_map(EncodeFn enc, const void* base, int rows, int K, int
   return m;
 }
 
-template <int BN, int S>
+template <int BN, int S, bool AT = false>
 void run(int M, int N, int K, bool check) {
   std::vector<int8_t> hA((size_t)M * K), hB((size_t)N * K);
   uint32_t st = 12345;
@@ -184,7 +193,7 @@ void run(int M, int N, int K, bool check) {
   EncodeFn enc = get_encode();
   CUtensorMap ma = make_map(enc, dA, M, K, 128), mb = make_map(enc, dB, N, K, BN);
   const size_t smem = 1024 + S * (128 * 128 + BN * 128) + (2 * S + 1) * 8 + 16;
-  auto kern = i8gemm<BN, S>;
+  auto kern = i8gemm<BN, S, AT>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((M + 127) / 128, (N + BN - 1) / BN);
   kern<<<grid, 128, smem>>>(ma, mb, dC, M, N, K);
@@ -203,7 +212,7 @@ void run(int M, int N, int K, bool check) {
           ++bad;
         }
       }
-    printf("BN=%d S=%d M=%d N=%d K=%d: %s (%ld bad)\n", BN, S, M, N, K, bad ? "FAIL" : "ok", bad);
+    printf("BN=%d S=%d AT=%d M=%d N=%d K=%d: %s (%ld bad)\n", BN, S, (int)AT, M, N, K, bad ? "FAIL" : "ok", bad);
   }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -217,20 +226,20 @@ void run(int M, int N, int K, bool check) {
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
   ms /= reps;
-  printf("BN=%d S=%d M=%d N=%d K=%d: %.2f us, %.1f TOPS\n", BN, S, M, N, K, ms * 1e3, 2.0 * M * N * K / ms / 1e9);
+  printf("BN=%d S=%d AT=%d M=%d N=%d K=%d: %.2f us, %.1f TOPS\n", BN, S, (int)AT, M, N, K, ms * 1e3, 2.0 * M * N * K / ms / 1e9);
   cudaFree(dA);
   cudaFree(dB);
   cudaFree(dC);
 }
 
 int main() {
-  run<64, 4>(256, 128, 256, true);
-  run<64, 4>(1024, 256, 512, true);
-  run<128, 4>(1024, 256, 512, true);
-  run<256, 3>(1024, 256, 512, true);
-  run<64, 4>(65536, 256, 256, true);
-  run<128, 4>(65536, 256, 256, false);
-  run<256, 3>(65536, 256, 256, false);
-  run<256, 3>(65536, 256, 2048, false);
+  run<64, 4, false>(1024, 256, 512, true);
+  run<64, 4, true>(1024, 256, 512, true);
+  run<128, 4, true>(1024, 256, 512, true);
+  run<64, 4, true>(65536, 256, 256, true);
+  run<64, 4, false>(8192, 64, 8192, false);
+  run<64, 4, true>(8192, 64, 8192, false);
+  run<256, 3, false>(8192, 256, 4096, false);
+  run<256, 3, true>(8192, 256, 4096, false);
   return 0;
 }
