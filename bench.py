@@ -8,7 +8,8 @@ Headline (BASELINE.json metric, configs[3] at n=256 = the north-star target size
   The 134 MB input plus three 134 MB work buffers exceed the 126 MB L2, so no flush is needed.
 Secondary (same JSON line):
   e2e       the same metric through fd_apply_host (pinned host buffers; H2D + apply + D2H timed per step)
-  roofline  FP64 tensor (DMMA) roofline of the mode-product kernel: 12 n^4 flop per apply / t_apply
+  roofline  the dominant kernel's roofline: the int8 tensor-core GEMM (oz_gemm_kernel) on the int8-split path
+            (n = 256 default), else the FP64 DMMA mode product; per-launch work / its own CUDA-event launch time
             against the DMMA peak measured on this pool (profiles/r01_peaks_fp64.jsonl)
   gmres     preconditioned GMRES(30) time-to-1e-8 on configs[1], [2], [4] (assembled on the device,
             b and x resident), iterations, and the stored-operator matvec HBM roofline on configs[4]
@@ -42,6 +43,47 @@ def fp64_peak():
             if rec.get("kind") == "dmma_sustained":
                 best = rec["tflops"]
     return best
+
+
+def int8_peak():
+    """Dense int8 tensor-core peak: MEASURED_PEAKS.json's cuBLAS bf16 (burst) x the nominal int8/bf16 ratio
+    (4.5 / 2.25 PFLOP/s, B200_PROFILING.md).  Our own tcgen05.mma.kind::i8 issue loop measured 4.55 POP/s
+    (tools/tc/mma_rate.cu, profiles/r01_tc_int8_mma_rate.txt)."""
+    try:
+        return 2.0 * json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"], \
+            "2 x MEASURED_PEAKS.json bf16_tflops (nominal int8/bf16 ratio)"
+    except Exception:
+        return 4500.0, "fallback nominal 4.5 POP/s dense int8"
+
+
+def roofline(path, kern, flops, int8_ops, achieved_fp64, fp64_pk, traffic, ws):
+    """The dominant kernel's roofline.  DMMA path: dmma_gemm_kernel, FP64 tensor, 4 N n_l flop per launch.
+    int8 path: oz_gemm_kernel, int8 tensor, 2 M N K ops per digit-pair MMA (36 pairs per mode product)."""
+    fp64_eq = {"achieved": achieved_fp64, "peak": fp64_pk, "unit": "TFLOP/s", "frac": achieved_fp64 / fp64_pk,
+               "what": "whole FD apply: 4 N sum(n_l) FP64 flop / apply time, against the FP64 (DMMA) peak"}
+    if path == "int8_split" and kern and "int8_gemm" in kern:
+        g = kern["int8_gemm"]
+        ach = int8_ops / g["launches_per_apply"] / (g["avg_ms"] * 1e-3) / 1e12
+        pk, src = int8_peak()
+        return {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TOP/s (int8)", "frac": ach / pk,
+                "traffic": traffic.get("oz_gemm") if isinstance(traffic, dict) else None,
+                "kernel": f"oz_gemm_kernel (tcgen05.mma.kind::i8, {g['launches_per_apply']} launches per apply, "
+                          f"{100 * g['share']:.0f}% of the apply; the int8 digit splits are the rest)",
+                "int8_ops_per_apply": int8_ops, "avg_launch_ms": g["avg_ms"], "peak_source": src,
+                "kernels": kern, "fp64_equivalent": fp64_eq}
+    if kern and "dmma" in kern:
+        g = kern["dmma"]
+        ach = flops / g["launches_per_apply"] / (g["avg_ms"] * 1e-3) / 1e12
+    else:
+        ach = achieved_fp64
+    return {"bound": "tensor", "achieved": ach, "peak": fp64_pk, "unit": "TFLOP/s", "frac": ach / fp64_pk,
+            "traffic": (traffic["dmma"] / 6 if isinstance(traffic, dict) and traffic.get("dmma") else None),
+            "kernel": "dmma_gemm_kernel (6 launches per apply: 3 forward + 3 backward mode products)"
+                      + (", per GPU" if ws > 1 else ""),
+            "flops_per_apply": flops,
+            "peak_source": "own DMMA.8x8x4 register loop, sustained 3 s (profiles/r01_peaks_fp64.jsonl); "
+                           "MEASURED_PEAKS.json has no FP64 entry",
+            "kernels": kern, "fp64_equivalent": fp64_eq}
 
 
 def hbm_peak():
@@ -440,7 +482,19 @@ def main():
     value = N / (ms * 1e-3) / 1e9           # all ranks' DOFs / max-over-ranks time
     flops = plan.flops()                     # whole apply (all ranks)
     peak = fp64_peak()
-    achieved = flops / ws / (ms * 1e-3) / 1e12   # per GPU
+    achieved = flops / ws / (ms * 1e-3) / 1e12   # per GPU (FP64-equivalent rate of the whole apply)
+    path, int8_ops = plan.path()
+    # per-kernel durations of the apply (CUDA events after every launch on the ctx stream, single rank):
+    # the dominant kernel's roofline is its own algorithmic work / its own average launch time
+    kern = None
+    if ws == 1:
+        per = {}
+        for _ in range(3):
+            for kind, kms in fd.fd_apply_timed(plan, x, s):
+                per.setdefault(kind, []).append(kms)
+        tot = sum(sum(v) for v in per.values())
+        kern = {k: {"launches_per_apply": len(v) // 3, "avg_ms": float(np.mean(v)), "share": sum(v) / tot}
+                for k, v in per.items()}
 
     # e2e: same metric through the C ABI with pinned host buffers (H2D + apply + D2H per step)
     xh = torch.from_numpy(np.random.default_rng(4001 + rank).standard_normal(plan.N)).pin_memory()
@@ -501,10 +555,11 @@ def main():
         ctx1.close()
         plan_w.close()
         del x1, s1, xw, sw
-    traffic = None
+    traffic = None  # dram bytes per launch of the dominant kernel, from the committed ncu --set full summary
     if os.path.exists(NCU_SUMMARY):
         try:
-            traffic = json.load(open(NCU_SUMMARY)).get("fd_apply_dram_bytes_per_apply")
+            js = json.load(open(NCU_SUMMARY))
+            traffic = {"dmma": js.get("fd_apply_dram_bytes_per_apply"), "oz_gemm": js.get("oz_gemm_dram_bytes_per_launch")}
         except Exception:
             traffic = None
 
@@ -528,13 +583,7 @@ def main():
                        else "vector fits in L2 (no flush)",
                        "parallelism": f"slab-sharded over {ws} GPUs (NCCL all-to-all in the mode-d pass)" if ws > 1
                        else "single GPU"},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "dmma_gemm_kernel (6 launches per apply: 3 forward + 3 backward mode products)"
-                                   + (", per GPU" if ws > 1 else ""),
-                         "flops_per_apply": flops,
-                         "peak_source": "own DMMA.8x8x4 register loop, sustained 3 s (profiles/r01_peaks_fp64.jsonl); "
-                                        "MEASURED_PEAKS.json has no FP64 entry"},
+            "roofline": roofline(path, kern, flops, int8_ops, achieved, peak, traffic, ws),
             "e2e": {"value": N / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
                     "path": "fd_apply_host_async (pinned host buffers; every step H2D + apply + D2H, consecutive "

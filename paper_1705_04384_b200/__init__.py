@@ -7,7 +7,7 @@ to a CPU implementation: importing the API without the built library raises Impo
 from ._lib import LIB_PATH, FdigaError, load  # noqa: F401
 from .api import (ORTH_CGS2, ORTH_DCGS2, bicgstab_solve, ORTH_CGS_DGKS, Context, FDPlan, LoopbackHub, Stencil, colloc_1d_factors,  # noqa: F401
                   colloc_1d_windows, colloc_1d_convection, wq_assemble, galerkin_1d_factors, halo_plan, transpose_plan,
-                  colloc_assemble, fd_apply, fd_apply_host, fd_apply_host_async, fd_host_sync, fd_setup, fd_setup_from_blocks, fd_setup_from_eig,
+                  colloc_assemble, fd_apply, fd_apply_timed, fd_apply_host, fd_apply_host_async, fd_host_sync, fd_setup, fd_setup_from_blocks, fd_setup_from_eig,
                   fd_setup_from_factors, gmres_solve, nccl_unique_id, partition, stencil_create,
                   stencil_matvec)
 

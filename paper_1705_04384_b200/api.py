@@ -288,6 +288,18 @@ def fd_apply(plan, r, s):
     return s
 
 
+def fd_apply_timed(plan, r, s):
+    """One apply with per-kernel CUDA-event durations: list of (kind, ms), kind in {'dmma', 'split', 'int8_gemm'}."""
+    cap = 64
+    ms = (C.c_float * cap)()
+    kind = (C.c_int32 * cap)()
+    cnt = C.c_int(0)
+    check(plan.ctx._lib.fd_apply_timed(plan.handle, _devptr(r, plan.N), _devptr(s, plan.N), ms, kind, cap,
+                                       C.byref(cnt)), "fd_apply_timed")
+    names = {0: "dmma", 1: "split", 2: "int8_gemm"}
+    return [(names[kind[k]], float(ms[k])) for k in range(min(cnt.value, cap))]
+
+
 def fd_apply_host(plan, r_host, s_host):
     """Same with host (numpy, ideally pinned) buffers; H2D + apply + D2H inside the call."""
     if r_host.dtype != np.float64 or s_host.dtype != np.float64 or r_host.size != plan.N or s_host.size != plan.N:

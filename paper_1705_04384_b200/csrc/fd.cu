@@ -59,7 +59,22 @@ struct fd_plan {
   // int8-split tcgen05 mode products (oz.cu): digit planes of the factors and of the data per mode
   bool oz = false;
   OzOperand ozW[3], ozU[3], ozX[3];
+  // fd_apply_timed: an event recorded after every kernel of the apply (nullptr: off)
+  std::vector<cudaEvent_t>* tev = nullptr;
+  std::vector<int>* tkind = nullptr;  // 0 = DMMA mode product, 1 = int8 split, 2 = int8 GEMM
 };
+
+namespace {
+int mark(fd_plan* P, int kind) {
+  if (!P->tev) return FDIGA_OK;
+  cudaEvent_t e;
+  FDIGA_CUDA(cudaEventCreate(&e));
+  FDIGA_CUDA(cudaEventRecord(e, P->ctx->stream));
+  P->tev->push_back(e);
+  P->tkind->push_back(kind);
+  return FDIGA_OK;
+}
+}  // namespace
 
 namespace {
 
@@ -222,14 +237,16 @@ GemmParams model_params(fd_plan* P, int l, const double* F, int64_t ldf, const d
 
 int mode1(fd_plan* P, const double* F, int64_t ldf, const double* X, double* Y, int64_t R, const int* skip) {
   if (R == 0) return FDIGA_OK;
-  return gemm_launch(P->ctx, P->ctx->stream, BLayout::NK, P->cfg[0], mode1_params(P, F, ldf, X, Y, R, skip));
+  FDIGA_TRY(gemm_launch(P->ctx, P->ctx->stream, BLayout::NK, P->cfg[0], mode1_params(P, F, ldf, X, Y, R, skip)));
+  return mark(P, 0);
 }
 
 int model(fd_plan* P, int l, const double* F, int64_t ldf, const double* X, double* Y, int64_t inner,
           int64_t batch, const double* lam_m, const double* lam_n, const int* skip) {
   if (inner * batch == 0) return FDIGA_OK;
-  return gemm_launch(P->ctx, P->ctx->stream, BLayout::KN, P->cfg[l],
-                     model_params(P, l, F, ldf, X, Y, inner, batch, lam_m, lam_n, skip));
+  FDIGA_TRY(gemm_launch(P->ctx, P->ctx->stream, BLayout::KN, P->cfg[l],
+                        model_params(P, l, F, ldf, X, Y, inner, batch, lam_m, lam_n, skip)));
+  return mark(P, 0);
 }
 
 // Pick the tile configuration of every mode product of this plan by timing them on the plan's scratch.
@@ -376,7 +393,9 @@ int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, 
     g.mstride = 1;
     g.fstride = n1 * n2;
   }
-  return oz_gemm(P->ctx, st, g);
+  FDIGA_TRY(mark(P, 1));
+  FDIGA_TRY(oz_gemm(P->ctx, st, g));
+  return mark(P, 2);
 }
 
 int fd_apply_oz(fd_plan* P, const double* r, double* s, const int* skip) {
@@ -1002,6 +1021,40 @@ double fd_apply_flops(const fd_plan* P) {
   double s = 0;
   for (int l = 0; l < P->d; ++l) s += (double)P->n[l];
   return 4.0 * (double)P->N * s;
+}
+
+int fd_apply_timed(fd_plan* P, const double* r, double* s, float* kernel_ms, int* kernel_kind, int cap,
+                   int* count) {
+  FDIGA_CHECK(P && count, FDIGA_ERR_INVALID_ARG, "NULL argument");
+  FDIGA_TRY(bind(P->ctx));
+  FDIGA_CHECK(!P->ctx->sharded, FDIGA_ERR_NOT_SUPPORTED, "fd_apply_timed: single-rank plans only");
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> kind;
+  cudaEvent_t e0;
+  FDIGA_CUDA(cudaEventCreate(&e0));
+  FDIGA_CUDA(cudaEventRecord(e0, P->ctx->stream));
+  P->tev = &ev;
+  P->tkind = &kind;
+  const int rc = fdiga::fd_apply_ex(P, r, s, nullptr);
+  P->tev = nullptr;
+  P->tkind = nullptr;
+  int status = rc;
+  cudaError_t ce = cudaSuccess;
+  if (rc == FDIGA_OK && (ce = cudaStreamSynchronize(P->ctx->stream)) != cudaSuccess) status = FDIGA_ERR_CUDA;
+  *count = (int)ev.size();
+  for (size_t k = 0; k < ev.size(); ++k) {
+    float ms = 0.0f;
+    if (status == FDIGA_OK) cudaEventElapsedTime(&ms, k == 0 ? e0 : ev[k - 1], ev[k]);
+    if ((int)k < cap) {
+      if (kernel_ms) kernel_ms[k] = ms;
+      if (kernel_kind) kernel_kind[k] = kind[k];
+    }
+  }
+  for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  cudaEventDestroy(e0);
+  if (rc != FDIGA_OK) return rc;  // the apply's own message stands
+  FDIGA_CHECK(status == FDIGA_OK, status, "fd_apply_timed: %s", cudaGetErrorString(ce));
+  return FDIGA_OK;
 }
 
 int fd_plan_path(const fd_plan* P, double* int8_ops) {
