@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
                                                             const double* __restrict__ lam_row,
                                                             const double* __restrict__ lam_k, const int* skip) {
   if (skip && *skip) return;
-  extern __shared__ double tile[];  // [K][33]
+  // [K][32] tile, column i of row k stored at i ^ ((k / 8) mod 16): conflict-free both for the row-wise
+  // staging (lanes = i) and for the digit pass (lanes = 8-row chunks c of one column i)
+  extern __shared__ double tile[];
   __shared__ double pmax[8][32];
   __shared__ int es[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -120,15 +122,15 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
   const bool iv = i0 + lane < inner;
   // the eigenvalue-sum divide of the FD (eq:FD3D) when the split feeds the backward mode-d product
   const double lr = (lam_row && iv) ? lam_row[b * inner + i0 + lane] : 0.0;
-  for (int k0 = warp; k0 < K; k0 += 32) {
-    double v[4];
+  for (int k0 = warp; k0 < K; k0 += 64) {
+    double v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // four independent loads in flight per thread
+    for (int u = 0; u < 8; ++u) {  // eight independent loads in flight per thread
       const int k = k0 + 8 * u;
       v[u] = (iv && k < K) ? xb[(int64_t)k * inner + i0 + lane] : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const int k = k0 + 8 * u;
       if (k >= K) break;
       double val = v[u];
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
         r = fma(r, fma(-dn, r, 1.0), r);
         val *= r;
       }
-      tile[k * 33 + lane] = val;
+      tile[k * 32 + (lane ^ ((k >> 3) & 15))] = val;
       mx = fmax(mx, fabs(val));
     }
   }
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int k = c * 8 + j;
-      v[j] = k < K ? tile[k * 33 + i] : 0.0;
+      v[j] = k < K ? tile[k * 32 + (i ^ ((k >> 3) & 15))] : 0.0;
     }
     uint64_t w[OZ_S];
     split8(v, es[i], w);
@@ -523,7 +525,7 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
     else
       oz_split_rows_kernel<2><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.rows_p, (int)op.kp, skip);
   } else {
-    const size_t smem = (size_t)K * 33 * sizeof(double);
+    const size_t smem = (size_t)K * 32 * sizeof(double);
     static bool attr = false;
     if (!attr) {
       FDIGA_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
