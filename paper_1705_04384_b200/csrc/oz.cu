@@ -48,20 +48,35 @@ __device__ __forceinline__ int row_exponent(double mx) {
 // (truncated: bits below 2^-62 of the row scale are beyond digit S anyway); digit i of |x| is then bits
 // [62 - 7 i, 69 - 7 i) of it, with the sign of x -- the truncated base-128 expansion of x 2^-e.
 __device__ __forceinline__ void split8(const double (&v)[8], int e, uint64_t (&w)[OZ_S]) {
+  static_assert(OZ_S == 8, "digit extraction written for 8 digits of 7 bits (bits 6..61 of q)");
   const double sc = pow2(62 - e);
+  uint32_t lo[OZ_S], hi[OZ_S];  // bytes 0-3 / 4-7 of every digit word
 #pragma unroll
-  for (int s = 0; s < OZ_S; ++s) w[s] = 0;
+  for (int s = 0; s < OZ_S; ++s) lo[s] = hi[s] = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const long long q = __double2ll_rz(v[j] * sc);  // exact scaling, |q| < 2^62
     const unsigned long long aq = (unsigned long long)(q < 0 ? -q : q);
-    const bool neg = q < 0;
+    // digits s = 0..7 are bits [55 - 7s, 62 - 7s) of |q|: from 32-bit halves (s = 4 straddles them)
+    const uint32_t h = (uint32_t)(aq >> 32), l = (uint32_t)aq;
+    uint32_t d[OZ_S];
+    d[0] = (h >> 23) & 127u;
+    d[1] = (h >> 16) & 127u;
+    d[2] = (h >> 9) & 127u;
+    d[3] = (h >> 2) & 127u;
+    d[4] = __funnelshift_l(l, h, 5) & 127u;  // bits 27..33
+    d[5] = (l >> 20) & 127u;
+    d[6] = (l >> 13) & 127u;
+    d[7] = (l >> 6) & 127u;
+    const uint32_t neg = q < 0 ? 0xFFu : 0u;
 #pragma unroll
     for (int s = 0; s < OZ_S; ++s) {
-      const int d = (int)((aq >> (55 - 7 * s)) & 127u);
-      w[s] |= (uint64_t)(uint8_t)(neg ? -d : d) << (8 * j);
+      const uint32_t byte = ((d[s] ^ neg) - (neg & 0xFFu ? 0xFFu : 0u)) & 0xFFu;  // two's complement of -d
+      if (j < 4) lo[s] |= byte << (8 * j); else hi[s] |= byte << (8 * (j - 4));
     }
   }
+#pragma unroll
+  for (int s = 0; s < OZ_S; ++s) w[s] = ((uint64_t)hi[s] << 32) | lo[s];
 }
 
 // inner == 1: rows of K contiguous values.  One warp per row, 8 values per lane per 256-wide chunk.
@@ -120,30 +135,27 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
   const double* xb = x + b * K * inner;
   double mx = 0.0;
   const bool iv = i0 + lane < inner;
+  // the whole K x 32 tile in flight at once: 8-byte cp.async (zero-filled outside [0, inner)), no registers
+  for (int k = warp; k < K; k += 8)
+    cp_async8(smem_u32(&tile[k * 32 + (lane ^ ((k >> 3) & 15))]), iv ? xb + (int64_t)k * inner + i0 + lane : xb,
+              iv ? 8 : 0);
+  cp_async_commit();
+  cp_async_wait<0>();
+  // each thread revisits only the elements it copied itself: no barrier needed before this pass
   // the eigenvalue-sum divide of the FD (eq:FD3D) when the split feeds the backward mode-d product
   const double lr = (lam_row && iv) ? lam_row[b * inner + i0 + lane] : 0.0;
-  for (int k0 = warp; k0 < K; k0 += 64) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {  // eight independent loads in flight per thread
-      const int k = k0 + 8 * u;
-      v[u] = (iv && k < K) ? xb[(int64_t)k * inner + i0 + lane] : 0.0;
+  for (int k = warp; k < K; k += 8) {
+    double* tp = &tile[k * 32 + (lane ^ ((k >> 3) & 15))];
+    double val = *tp;
+    if (lam_row) {  // val / (lr + lam_k[k]): float-seeded reciprocal, two Newton steps (< 1 ulp off)
+      const double dn = lr + lam_k[k];
+      double r = (double)__frcp_rn((float)dn);
+      r = fma(r, fma(-dn, r, 1.0), r);
+      r = fma(r, fma(-dn, r, 1.0), r);
+      val *= r;
+      *tp = val;
     }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int k = k0 + 8 * u;
-      if (k >= K) break;
-      double val = v[u];
-      if (lam_row) {  // val / (lr + lam_k[k]): float-seeded reciprocal, two Newton steps (< 1 ulp off)
-        const double dn = lr + lam_k[k];
-        double r = (double)__frcp_rn((float)dn);
-        r = fma(r, fma(-dn, r, 1.0), r);
-        r = fma(r, fma(-dn, r, 1.0), r);
-        val *= r;
-      }
-      tile[k * 32 + (lane ^ ((k >> 3) & 15))] = val;
-      mx = fmax(mx, fabs(val));
-    }
+    mx = fmax(mx, fabs(val));
   }
   pmax[warp][lane] = mx;
   __syncthreads();
