@@ -161,8 +161,8 @@ int fd_host_sync(fd_plan* plan);
 /* Algorithmic flops of one apply: 4 N sum_l n_l (= 12 n^4 in 3D P:481, 8 n^3 in 2D P:464). */
 double fd_apply_flops(const fd_plan* plan);
 /* Kernel family of the mode products: FDIGA_PATH_DMMA (FP64 mma.sync DMMA tiles) or FDIGA_PATH_INT8_SPLIT
- * (exact int8 digit splitting on tcgen05.mma.kind::i8 with TMEM accumulators; 3D single-rank plans with
- * 192 <= n_l <= 256 by default).  int8_ops (may be NULL) receives the int8 tensor-core
+ * (exact int8 digit splitting on tcgen05.mma.kind::i8 with TMEM accumulators; 3D real-spectrum plans with
+ * 192 <= n_l <= 256 by default, single-rank or sharded).  int8_ops (may be NULL) receives the int8 tensor-core
  * operations one apply issues on that path (2 M N K per digit-pair MMA, padded shapes), else 0. */
 enum { FDIGA_PATH_DMMA = 0, FDIGA_PATH_INT8_SPLIT = 1 };
 int fd_plan_path(const fd_plan* plan, double* int8_ops);

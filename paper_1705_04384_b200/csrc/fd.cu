@@ -328,13 +328,13 @@ int broadcast_factors(fd_plan* P) {
   return FDIGA_OK;
 }
 
-// int8-split tensor-core mode products (oz.cu) for 3D, single-rank, real-spectrum plans with
+// int8-split tensor-core mode products (oz.cu) for 3D real-spectrum plans (single-rank or slab-sharded) with
 // 192 <= n_l <= 256 -- where they beat the DMMA products on a B200 (n = 256: 1.38 vs 1.72 ms per apply;
 // at n = 128 / 131 the short contractions leave the tensor cores idle and DMMA wins).
 // FDIGA_FD_OZ=0 / 1 forces the choice (1: any n_l <= 256).  A static rule, so every run -- also under a
 // profiler -- takes the same kernels.
 bool oz_eligible(const fd_plan* P) {
-  if (P->d != 3 || P->ctx->sharded || P->has_pairs) return false;
+  if (P->d != 3 || P->has_pairs) return false;
   for (int l = 0; l < 3; ++l)
     if (P->n[l] > OZ_MAXKP) return false;
   const char* e = getenv("FDIGA_FD_OZ");
@@ -345,53 +345,68 @@ bool oz_eligible(const fd_plan* P) {
   return true;
 }
 
+// Local shapes of the three mode products on this rank: modes 1 and 2 on the slab of c = e - o planes of
+// the last axis, mode 3 on the transposed chunk T(n_3 x len) (single rank: c = n_3, len = n_1 n_2).
+struct OzShapes {
+  int64_t rows[3];
+};
+OzShapes oz_shapes(const fd_plan* P) {
+  const int64_t c = P->e - P->o;
+  return {{P->n[1] * c, P->n[0] * c, P->len}};
+}
+
 int oz_setup(fd_plan* P) {
   if (!oz_eligible(P)) return FDIGA_OK;
   cudaStream_t st = P->ctx->stream;
+  const OzShapes sh = oz_shapes(P);
   for (int l = 0; l < 3; ++l) {
     FDIGA_TRY(oz_operand_alloc(P->ozW[l], P->n[l], P->n[l], OZ_BN));
     FDIGA_TRY(oz_operand_alloc(P->ozU[l], P->n[l], P->n[l], OZ_BN));
     FDIGA_TRY(oz_split(P->ctx, st, P->W[l], P->n[l], P->n[l], 1, P->ld[l], P->ozW[l], nullptr));
     FDIGA_TRY(oz_split(P->ctx, st, P->U[l], P->n[l], P->n[l], 1, P->ld[l], P->ozU[l], nullptr));
-    FDIGA_TRY(oz_operand_alloc(P->ozX[l], P->N / P->n[l], P->n[l], OZ_BM));
+    FDIGA_TRY(oz_operand_alloc(P->ozX[l], sh.rows[l], P->n[l], OZ_BM));
   }
   FDIGA_CUDA(cudaStreamSynchronize(st));
   P->oz = true;
   return FDIGA_OK;
 }
 
-// one mode product on the int8 path: split the data along axis l, contract with the factor digits
-int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, const double* lamD,
-            const double* lamF, const int* skip, bool divide_input = false) {
+// One mode product on the int8 path: split the data along axis l, contract with the factor digits.
+//   l = 0: slab X[i3][i2][i1] (c planes), data rows (i3, i2), k = i1
+//   l = 1: slab, data rows (i3, i1), k = i2 (the split transposes)
+//   l = 2: chunk T[i3][q] (q over len inner indices), data rows q, k = i3; divide_input: X / (lam_inner[q0 + q] +
+//          lam_3[i3]) first (the Lambda divide of eq:FD3D, applied as the data enters the backward product)
+int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, const int* skip,
+            bool divide_input = false) {
   const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
+  const int64_t c = P->e - P->o, len = P->len;
   OzOperand& Xz = P->ozX[l];
   cudaStream_t st = P->ctx->stream;
   OzGemmArgs g{};
   g.X = &Xz;
   g.F = &Fz;
   g.y = Y;
-  g.lamD = lamD;
-  g.lamF = lamF;
   g.skip = skip;
-  if (l == 0) {  // data rows (i3, i2), k = i1
-    FDIGA_TRY(oz_split(P->ctx, st, X, n2 * n3, n1, 1, n1, Xz, skip));
-    g.inner = n2 * n3;
+  if (Xz.rows == 0) return FDIGA_OK;
+  if (l == 0) {
+    FDIGA_TRY(oz_split(P->ctx, st, X, n2 * c, n1, 1, n1, Xz, skip));
+    g.inner = n2 * c;
     g.bstride = 0;
     g.mstride = n1;
     g.fstride = 1;
-  } else if (l == 1) {  // data rows (i3, i1), k = i2
-    FDIGA_TRY(oz_split(P->ctx, st, X, n3, n2, n1, 0, Xz, skip));
+  } else if (l == 1) {
+    FDIGA_TRY(oz_split(P->ctx, st, X, c, n2, n1, 0, Xz, skip));
     g.inner = n1;
     g.bstride = n1 * n2;
     g.mstride = 1;
     g.fstride = n1;
-  } else {  // data rows (i2, i1), k = i3 (divide_input: X / (lam_inner[(i2, i1)] + lam_3[i3]) first)
-    FDIGA_TRY(oz_split(P->ctx, st, X, 1, n3, n1 * n2, 0, Xz, skip, divide_input ? P->lam_inner : nullptr,
+  } else {
+    FDIGA_TRY(oz_split(P->ctx, st, X, 1, n3, len, 0, Xz, skip, divide_input ? P->lam_inner + P->q0 : nullptr,
                        divide_input ? P->lam[2] : nullptr));
-    g.inner = n1 * n2;
+    g.inner = len;
     g.bstride = 0;
     g.mstride = 1;
-    g.fstride = n1 * n2;
+    g.fstride = len;
   }
   FDIGA_TRY(mark(P, 1));
   FDIGA_TRY(oz_gemm(P->ctx, st, g));
@@ -401,13 +416,13 @@ int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, 
 int fd_apply_oz(fd_plan* P, const double* r, double* s, const int* skip) {
   double* a = P->t0.p;
   double* b = P->t1.p;
-  FDIGA_TRY(oz_mode(P, 0, P->ozW[0], r, a, nullptr, nullptr, skip));
-  FDIGA_TRY(oz_mode(P, 1, P->ozW[1], a, b, nullptr, nullptr, skip));
+  FDIGA_TRY(oz_mode(P, 0, P->ozW[0], r, a, skip));
+  FDIGA_TRY(oz_mode(P, 1, P->ozW[1], a, b, skip));
   // the Lambda divide rides in the split that feeds the backward mode-3 product
-  FDIGA_TRY(oz_mode(P, 2, P->ozW[2], b, a, nullptr, nullptr, skip));
-  FDIGA_TRY(oz_mode(P, 2, P->ozU[2], a, b, nullptr, nullptr, skip, true));
-  FDIGA_TRY(oz_mode(P, 1, P->ozU[1], b, a, nullptr, nullptr, skip));
-  return oz_mode(P, 0, P->ozU[0], a, s, nullptr, nullptr, skip);
+  FDIGA_TRY(oz_mode(P, 2, P->ozW[2], b, a, skip));
+  FDIGA_TRY(oz_mode(P, 2, P->ozU[2], a, b, skip, true));
+  FDIGA_TRY(oz_mode(P, 1, P->ozU[1], b, a, skip));
+  return oz_mode(P, 0, P->ozU[0], a, s, skip);
 }
 
 int finish_plan(fd_plan* P) {
@@ -672,7 +687,10 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
   const int64_t n1 = P->n[0], n2 = P->n[1], nd = P->n[d - 1];
   const int64_t c = P->e - P->o, Nin = P->Nin, len = P->len;
   // forward modes 1..d-1 -> b (slab layout)
-  if (d == 3) {
+  if (d == 3 && P->oz) {
+    FDIGA_TRY(oz_mode(P, 0, P->ozW[0], r, a, skip));
+    FDIGA_TRY(oz_mode(P, 1, P->ozW[1], a, b, skip));
+  } else if (d == 3) {
     FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2 * c, skip));
     FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, c, nullptr, nullptr, skip));
   } else {
@@ -697,8 +715,13 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
   }
   plan_msgs(a, b);
   FDIGA_TRY(comm_exchange(ctx, snd, rcv));  // b = T(n_d x len)
-  FDIGA_TRY(model(P, d - 1, P->W[d - 1], P->ld[d - 1], b, a, len, 1, P->lam[d - 1], P->lam_inner + P->q0, skip));
-  FDIGA_TRY(model(P, d - 1, P->U[d - 1], P->ld[d - 1], a, b, len, 1, nullptr, nullptr, skip));
+  if (P->oz) {  // the Lambda divide rides in the split feeding the backward product (chunk offset q0)
+    FDIGA_TRY(oz_mode(P, 2, P->ozW[2], b, a, skip));
+    FDIGA_TRY(oz_mode(P, 2, P->ozU[2], a, b, skip, true));
+  } else {
+    FDIGA_TRY(model(P, d - 1, P->W[d - 1], P->ld[d - 1], b, a, len, 1, P->lam[d - 1], P->lam_inner + P->q0, skip));
+    FDIGA_TRY(model(P, d - 1, P->U[d - 1], P->ld[d - 1], a, b, len, 1, nullptr, nullptr, skip));
+  }
   plan_msgs(a, b);
   FDIGA_TRY(comm_exchange(ctx, rcv, snd));  // reverse: rows of T back to their slab owners, into a
   if (c > 0) {
@@ -706,7 +729,10 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
     count_launch(ctx);
     FDIGA_CUDA(cudaGetLastError());
   }
-  if (d == 3) {
+  if (d == 3 && P->oz) {
+    FDIGA_TRY(oz_mode(P, 1, P->ozU[1], b, a, skip));
+    FDIGA_TRY(oz_mode(P, 0, P->ozU[0], a, s, skip));
+  } else if (d == 3) {
     FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, c, nullptr, nullptr, skip));
     FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2 * c, skip));
   } else {

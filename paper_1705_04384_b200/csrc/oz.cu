@@ -497,6 +497,12 @@ int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows) {
   const int64_t rows_p = (rows + box_rows - 1) / box_rows * box_rows;
   FDIGA_CHECK(kp <= OZ_MAXKP, FDIGA_ERR_NOT_SUPPORTED, "int8-split FD: contraction length %lld > %d",
               (long long)k, OZ_MAXKP);
+  if (rows == 0) {  // a rank without planes / chunk: nothing to split or multiply
+    op.release();
+    op.box_rows = box_rows;
+    op.kp = kp;
+    return FDIGA_OK;
+  }
   if (op.digits && op.rows_p == rows_p && op.kp == kp && op.box_rows == box_rows) {
     op.rows = rows;
     return FDIGA_OK;

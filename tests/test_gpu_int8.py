@@ -2,7 +2,8 @@
 tcgen05.mma.kind::i8, DESIGN.md §5) against the CPU oracle.
 
 The path is forced with FDIGA_FD_OZ=1 (read when a plan is set up) so that ragged, tiny and Poisson shapes
-go through it; the default rule (3D, single rank, 192 <= n_l <= 256) is checked separately.  Bar: the
+go through it; the default rule (3D, real spectra, 192 <= n_l <= 256) is checked separately; the sharded
+variants are in test_gpu_sharded.py.  Bar: the
 north_star's 1e-12 relative l2 for fd_apply, GMRES counts within +-1 of the oracle.
 """
 import json

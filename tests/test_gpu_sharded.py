@@ -97,6 +97,32 @@ def test_sharded_fd_apply_matches_oracle(ns, nranks):
     np.testing.assert_array_equal(np.concatenate([p[1] for p in parts]), np.concatenate([p[0] for p in parts]))
 
 
+@pytest.mark.parametrize("ns,nranks", [((17, 19, 23), 2), ((33, 35, 16), 8), ((5, 6, 3), 4), ((40, 24, 64), 3)])
+def test_sharded_int8_fd_apply_matches_oracle(ns, nranks, monkeypatch):
+    # the int8-split tensor-core mode products on the slab layout and on the transposed
+    # mode-3 chunk (with the Lambda divide offset by the chunk start q0), forced onto small shapes
+    monkeypatch.setenv("FDIGA_FD_OZ", "1")
+    rng = np.random.default_rng(sum(ns) + 10 * nranks)
+    f = fastdiag.factors_from_eig([rng.standard_normal((n, n)) for n in ns], [rng.uniform(1, 100, n) for n in ns])
+    r = rng.standard_normal(int(np.prod(ns)))
+    inner = int(np.prod(ns[:-1]))
+
+    def work(ctx, rank):
+        plan = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
+        assert plan.path()[0] == "int8_split"
+        lo, hi = slab_rows(ns[-1], nranks, rank, inner)
+        x = torch.from_numpy(r[lo:hi].copy()).to(DEV)
+        s = torch.empty_like(x)
+        fd.fd_apply(plan, x, s)
+        torch.cuda.current_stream().synchronize()
+        res = s.cpu().numpy()
+        plan.close()
+        return res
+
+    parts = run_ranks(nranks, work)
+    assert rel(np.concatenate(parts), fastdiag.apply(f, r)) <= 1e-12
+
+
 def test_sharded_fd_setup_broadcasts_rank0_factors():
     # every rank runs the cuSOLVER setup; the plan then holds rank 0's factors bit for bit
     _, M, K, _ = splines.colloc_1d(40, 3)
@@ -206,6 +232,21 @@ def test_nccl_one_rank_fd_apply_and_matvec(nccl_ctx):
     assert rel(y.cpu().numpy(), disc.matvec(x)) <= 1e-12
     plan.close()
     A.close()
+
+
+def test_nccl_one_rank_int8_fd_apply(nccl_ctx, monkeypatch):
+    monkeypatch.setenv("FDIGA_FD_OZ", "1")
+    ns = (33, 35, 37)
+    rng = np.random.default_rng(8)
+    f = fastdiag.factors_from_eig([rng.standard_normal((n, n)) for n in ns], [rng.uniform(1, 100, n) for n in ns])
+    plan = fd.fd_setup_from_factors(nccl_ctx, f.U, f.W, f.lam)
+    assert plan.path()[0] == "int8_split"
+    r = rng.standard_normal(int(np.prod(ns)))
+    s = torch.empty(r.size, dtype=torch.float64, device=DEV)
+    fd.fd_apply(plan, torch.from_numpy(r).to(DEV), s)
+    torch.cuda.synchronize()
+    assert rel(s.cpu().numpy(), fastdiag.apply(f, r)) <= 1e-12
+    plan.close()
 
 
 @pytest.mark.parametrize("orth", [1, 2])
