@@ -1089,7 +1089,7 @@ int fd_plan_path(const fd_plan* P, double* int8_ops) {
     double ops = 0.0;
     if (P->oz)
       for (int l = 0; l < P->d; ++l)  // forward and backward product along l
-        ops += 2.0 * 2.0 * (OZ_S * (OZ_S + 1) / 2) * (double)P->ozX[l].rows_p * (double)P->ozW[l].rows_p *
+        ops += 2.0 * 2.0 * oz_pairs() * (double)P->ozX[l].rows_p * (double)P->ozW[l].rows_p *
                (double)P->ozX[l].kp;
     *int8_ops = ops;
   }

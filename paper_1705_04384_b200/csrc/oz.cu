@@ -48,31 +48,28 @@ __device__ __forceinline__ int row_exponent(double mx) {
 // (truncated: bits below 2^-62 of the row scale are beyond digit S anyway); digit i of |x| is then bits
 // [62 - 7 i, 69 - 7 i) of it, with the sign of x -- the truncated base-128 expansion of x 2^-e.
 __device__ __forceinline__ void split8(const double (&v)[8], int e, uint64_t (&w)[OZ_S]) {
-  static_assert(OZ_S == 8, "digit extraction written for 8 digits of 7 bits (bits 6..61 of q)");
+  static_assert(OZ_S == 7, "digit extraction written for a signed 8-bit leading digit and 6 unsigned bytes");
   const double sc = pow2(62 - e);
   uint32_t lo[OZ_S], hi[OZ_S];  // bytes 0-3 / 4-7 of every digit word
 #pragma unroll
   for (int s = 0; s < OZ_S; ++s) lo[s] = hi[s] = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const long long q = __double2ll_rz(v[j] * sc);  // exact scaling, |q| < 2^62
-    const unsigned long long aq = (unsigned long long)(q < 0 ? -q : q);
-    // digits s = 0..7 are bits [55 - 7s, 62 - 7s) of |q|: from 32-bit halves (s = 4 straddles them)
-    const uint32_t h = (uint32_t)(aq >> 32), l = (uint32_t)aq;
+    // q = floor(x 2^(62 - e)) in [-2^62, 2^62): digit 0 = q >> 55 (signed, [-128, 127]), digits 1..6 = the
+    // unsigned bytes of q at bits 47, 39, .., 7 (two's complement makes the lower digits non-negative)
+    const long long q = __double2ll_rd(v[j] * sc);
+    const uint32_t h = (uint32_t)((unsigned long long)q >> 32), l = (uint32_t)q;
     uint32_t d[OZ_S];
-    d[0] = (h >> 23) & 127u;
-    d[1] = (h >> 16) & 127u;
-    d[2] = (h >> 9) & 127u;
-    d[3] = (h >> 2) & 127u;
-    d[4] = __funnelshift_l(l, h, 5) & 127u;  // bits 27..33
-    d[5] = (l >> 20) & 127u;
-    d[6] = (l >> 13) & 127u;
-    d[7] = (l >> 6) & 127u;
-    const uint32_t neg = q < 0 ? 0xFFu : 0u;
+    d[0] = (h >> 23) & 255u;
+    d[1] = (h >> 15) & 255u;
+    d[2] = (h >> 7) & 255u;
+    d[3] = __funnelshift_l(l, h, 1) & 255u;  // bits 31..38
+    d[4] = (l >> 23) & 255u;
+    d[5] = (l >> 15) & 255u;
+    d[6] = (l >> 7) & 255u;
 #pragma unroll
     for (int s = 0; s < OZ_S; ++s) {
-      const uint32_t byte = ((d[s] ^ neg) - (neg & 0xFFu ? 0xFFu : 0u)) & 0xFFu;  // two's complement of -d
-      if (j < 4) lo[s] |= byte << (8 * j); else hi[s] |= byte << (8 * (j - 4));
+      if (j < 4) lo[s] |= d[s] << (8 * j); else hi[s] |= d[s] << (8 * (j - 4));
     }
   }
 #pragma unroll
@@ -218,10 +215,11 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
-constexpr uint32_t OZ_IDESC_C = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
-                                ((uint32_t)(OZ_BM >> 4) << 24);
-// the MMAs of one data digit I: pairs (I, j), j = 0..S-1-I, into accumulator I + j; 4 K-steps of 32 each.
-// db_kc: descriptor of factor digit 0 of this k chunk (digit j is j chunks further)
+// instruction descriptor: D s32, A / B s8 (signed digit 0) or u8, K-major, N = 64, M = 128
+__host__ __device__ constexpr uint32_t oz_idesc(bool a_signed, bool b_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
+         ((uint32_t)(OZ_BM >> 4) << 24);
+}
 template <int I>
 __device__ __forceinline__ void oz_stage_mmas(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
                                               bool first_kc);
@@ -254,22 +252,26 @@ struct OzKernelArgs {
 // completes right after digit t.  The epilogue drains weights in ascending order, i.e. slots in the order
 // 0, 1, .., S - 1 for either parity, which is exactly the order in which the next tile first writes them:
 // the epilogue of tile T runs under the MMAs of tile T + 1.
-__device__ __forceinline__ int oz_slot(int t, uint32_t tile) { return (tile & 1) ? OZ_S - 1 - t : t; }
+__device__ __forceinline__ int oz_slot(int t, uint32_t tile) { return (tile & 1) ? OZ_NW - 1 - t : t; }
 
-// the MMAs of data digit I: pairs (I, j), j = 0..S-1-I, into weight I + j; 4 K-steps of 32.  db_kc: descriptor
-// of factor digit 0 of this k chunk (digit j is j chunks further).  In the first k chunk (descending digits)
-// pair (I, 0) is the first write of weight I: it overwrites the slot.
+// the MMAs of data digit I: pairs (I, j), j = 0..min(S - 1, NW - 1 - I), into weight I + j; 4 K-steps of 32.
+// db_kc: descriptor of factor digit 0 of this k chunk (digit j is j chunks further).  Digit 0 is signed, the
+// others unsigned: the instruction descriptor is chosen per pair.  In the first k chunk (descending digits)
+// pair (I, 0) is the first write of weight I, and for the first digit (S - 1) also pair (I, 1) of weight
+// I + 1 = NW - 1: those MMAs overwrite their slot.
 template <int I>
 __device__ __forceinline__ void oz_stage_mmas(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
                                               bool first_kc) {
   const uint32_t odd = tile & 1;
 #pragma unroll
-  for (int j = 0; j + I < OZ_S; ++j) {
-    const uint32_t td = tbase + (uint32_t)((odd ? OZ_S - 1 - (I + j) : (I + j)) * OZ_BN);
+  for (int j = 0; j < OZ_S && I + j < OZ_NW; ++j) {
+    const uint32_t td = tbase + (uint32_t)((odd ? OZ_NW - 1 - (I + j) : (I + j)) * OZ_BN);
+    const uint32_t idesc = oz_idesc(I == 0, j == 0);
+    const bool first_touch = first_kc && (j == 0 || I == OZ_S - 1);
 #pragma unroll
     for (int kk = 0; kk < OZ_BK / 32; ++kk)
-      mma_i8(td, da + 2 * kk, db_kc + (uint64_t)(j * (OZ_BN * OZ_BK >> 4) + 2 * kk), OZ_IDESC_C,
-             (j != 0 || kk != 0 || !first_kc) ? 1u : 0u);
+      mma_i8(td, da + 2 * kk, db_kc + (uint64_t)(j * (OZ_BN * OZ_BK >> 4) + 2 * kk), idesc,
+             (kk != 0 || !first_touch) ? 1u : 0u);
   }
 }
 
@@ -286,10 +288,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
   uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_STAGES * OZ_XBYTES);
   uint64_t* empty = full + OZ_STAGES;
   uint64_t* fbar = empty + OZ_STAGES;
-  uint64_t* sfull = fbar + 1;      // [S] accumulator slot complete (MMA -> epilogue)
-  uint64_t* sempty = sfull + OZ_S;  // [S] accumulator slot drained (epilogue -> MMA)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_S);
-  double* sLF = reinterpret_cast<double*>(sempty + OZ_S + 1);  // eigenvalues of the CTA's factor rows
+  uint64_t* sfull = fbar + 1;      // [NW] accumulator slot complete (MMA -> epilogue)
+  uint64_t* sempty = sfull + OZ_NW;  // [NW] accumulator slot drained (epilogue -> MMA)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_NW);
+  double* sLF = reinterpret_cast<double*>(sempty + OZ_NW + 1);  // eigenvalues of the CTA's factor rows
   double* sSF = sLF + OZ_BN;                                    // 2^(e_f - 7 (S + 1)) of the CTA's factor rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
       mbar_init(&empty[s], 1);
     }
     mbar_init(fbar, 1);
-    for (int t = 0; t < OZ_S; ++t) {
+    for (int t = 0; t < OZ_NW; ++t) {
       mbar_init(&sfull[t], 1);
       mbar_init(&sempty[t], OZ_EW);
     }
@@ -361,27 +363,31 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
   {                                                                                                  \
     mbar_wait(&full[st], ph);                                                                        \
     tc_fence_after();                                                                                \
-    if (first && tl > 0) { /* weight I is first written by this stage: its slot must be drained */ \
+    if (first && tl > 0) { /* weights first written by this stage: their slots must be drained */  \
+      if (I == OZ_S - 1) mbar_wait(&sempty[oz_slot(OZ_NW - 1, tl)], (tl - 1) & 1);                  \
       mbar_wait(&sempty[oz_slot(I, tl)], (tl - 1) & 1);                                              \
       tc_fence_after();                                                                              \
     }                                                                                                \
     if (mma) oz_stage_mmas<I>(tbase, tl, da0 + (uint64_t)(st * (OZ_XBYTES >> 4)), dbk, first);      \
     tc_commit(&empty[st]); /* frees the ring slot when these MMAs have read it */                    \
-    if (last && !first) tc_commit(&sfull[oz_slot(I, tl)]); /* ascending: weight I complete */        \
+    if (last && !first) { /* ascending: weight I complete (and the last weight after the last digit) */ \
+      tc_commit(&sfull[oz_slot(I, tl)]);                                                             \
+      if (I == OZ_S - 1) tc_commit(&sfull[oz_slot(OZ_NW - 1, tl)]);                                  \
+    }                                                                                                \
     if (++st == OZ_STAGES) {                                                                         \
       st = 0;                                                                                        \
       ph ^= 1;                                                                                       \
     }                                                                                                \
   }
           if (first) {
-            static_assert(OZ_S == 8, "stage sequences written for S = 8");
-            OZ_STAGE(7) OZ_STAGE(6) OZ_STAGE(5) OZ_STAGE(4) OZ_STAGE(3) OZ_STAGE(2) OZ_STAGE(1) OZ_STAGE(0)
+            static_assert(OZ_S == 7 && OZ_NW == 8, "stage sequences written for 7 digits, 8 weights");
+            OZ_STAGE(6) OZ_STAGE(5) OZ_STAGE(4) OZ_STAGE(3) OZ_STAGE(2) OZ_STAGE(1) OZ_STAGE(0)
           } else {
-            OZ_STAGE(0) OZ_STAGE(1) OZ_STAGE(2) OZ_STAGE(3) OZ_STAGE(4) OZ_STAGE(5) OZ_STAGE(6) OZ_STAGE(7)
+            OZ_STAGE(0) OZ_STAGE(1) OZ_STAGE(2) OZ_STAGE(3) OZ_STAGE(4) OZ_STAGE(5) OZ_STAGE(6)
           }
 #undef OZ_STAGE
           if (first && last)  // single k chunk (descending): every weight completes at its end
-            for (int t = 0; t < OZ_S; ++t) tc_commit(&sfull[oz_slot(t, tl)]);
+            for (int t = 0; t < OZ_NW; ++t) tc_commit(&sfull[oz_slot(t, tl)]);
         }
       }
     }
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
     // epilogue: warp w owns TMEM lanes 32w..32w+31 = data rows m0 + 32w + lane
     if (threadIdx.x < OZ_BN) {
       const int64_t f = n0 + threadIdx.x;
-      sSF[threadIdx.x] = pow2(f < a.Nf ? a.ef[f] - 7 * (OZ_S + 1) : 0);
+      sSF[threadIdx.x] = pow2(f < a.Nf ? a.ef[f] - OZ_WSHIFT : 0);
       sLF[threadIdx.x] = (LAM && f < a.Nf) ? a.lamF[f] : 0.0;
     }
     asm volatile("bar.sync 1, %0;\n" ::"n"(OZ_EW * 32) : "memory");  // epilogue warps only
@@ -404,16 +410,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
       const int64_t row_off = (mm / a.inner) * a.bstride + (mm % a.inner) * a.mstride;
       const double sx = pow2(mv ? a.ex[mm] : 0);
       const double lamd = (LAM && mv) ? a.lamD[mm] : 0.0;
-      // sum_t 2^{7 (S - 1 - t)} C_t over the weights as they complete (largest weight first)
+      // sum_t 2^{8 (NW - 1 - t)} C_t over the weights as they complete (largest weight first)
       double acc[OZ_EC];
 #pragma unroll
       for (int c = 0; c < OZ_EC; ++c) acc[c] = 0.0;
 #pragma unroll 1
-      for (int t = 0; t < OZ_S; ++t) {
+      for (int t = 0; t < OZ_NW; ++t) {
         const int p = oz_slot(t, tl);
         mbar_wait(&sfull[p], tl & 1);
         tc_fence_after();
-        const double w = (double)(1ll << (7 * (OZ_S - 1 - t)));
+        const double w = (double)(1ll << (8 * (OZ_NW - 1 - t)));
         if (!(a.dbg & 1)) {
 #pragma unroll
           for (int c = 0; c < OZ_EC; c += 16) {
@@ -486,7 +492,7 @@ int get_encode(EncodeTiledFn* fn) {
 }
 
 constexpr size_t oz_smem_bytes(int KC) {
-  return 1024 + (size_t)OZ_S * KC * OZ_FBYTES + (size_t)OZ_STAGES * OZ_XBYTES + (2 * OZ_STAGES + 1 + 2 * OZ_S + 1) * 8 +
+  return 1024 + (size_t)OZ_S * KC * OZ_FBYTES + (size_t)OZ_STAGES * OZ_XBYTES + (2 * OZ_STAGES + 1 + 2 * OZ_NW + 1) * 8 +
          OZ_BN * 2 * sizeof(double);
 }
 

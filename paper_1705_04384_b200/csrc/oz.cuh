@@ -2,24 +2,33 @@
 // ("Ozaki scheme") on tcgen05.mma.kind::i8 with TMEM accumulators (oz.cu).
 //
 // Every operand row (a row of the factor W_l / U_l, or a fibre of the data tensor along the contracted
-// axis) is written as x = 2^e sum_{i=1..S} a_i 2^{-7i} with int8 digits a_i (|a_i| <= 127, truncated, so
-// the split is exact up to 2^{-7S} of the row's magnitude).  A contraction sum_k f_k x_k is then
-//   2^{e_f + e_x} sum_{t=2..S+1} 2^{-7t} C_t,   C_t = sum_{i+j=t} sum_k f_{k,j} x_{k,i}   (int32, exact)
-// and only the final FP64 combination of the S integer accumulators rounds.  The digit pairs with
-// i + j > S + 1 are dropped: with S = 8 the split is exact to 2^{-56} of the row magnitude and the dropped
-// pairs (zero-mean digits) add ~2^{-52} of it per dot product of length 256, i.e. the order of FP64 rounding
-// of the same dot product (S = 7 measured 2e-12 after six products on small ill-conditioned
-// factors, above the 1e-12 bar).
+// axis) gets an exponent e with max |x| < 2^e and is written through q = floor(x 2^(62 - e)) in [-2^62, 2^62)
+// as x ~ 2^(e - 62) (a_0 2^55 + sum_{i=1..6} a_i 2^(55 - 8i)), a_0 = q >> 55 a signed byte, a_1..a_6 the
+// unsigned bytes of q below it (exact to 2^(-55) of the row scale).  A contraction sum_k f_k x_k is then
+//   2^(e_f + e_x - 124) sum_t 2^(110 - 8t) C_t,   C_t = sum_{i+j=t} sum_k f_{k,j} x_{k,i}   (int32, exact)
+// for the 8 weights t = 0..7 (34 digit pairs; i + j > 7 dropped), and only the final FP64 combination of the
+// integer accumulators rounds.  The dropped pairs are below 2^(-53) of the row scales per dot product of
+// length 256: FP64-level accuracy.
 #pragma once
 #include "common.cuh"
 
 namespace fdiga {
 
-constexpr int OZ_S = 8;      // int8 digits per operand
+constexpr int OZ_S = 7;      // digit planes per operand (digit 0 signed, 1..6 unsigned)
+constexpr int OZ_NW = 8;     // digit-pair weights t = i + j = 0..7 (= int32 accumulators in TMEM)
+constexpr int OZ_WSHIFT = 14 + 8 * (OZ_NW - 1);  // 2^(e_x + e_f - WSHIFT) scales sum_t 2^(8 (NW - 1 - t)) C_t
 constexpr int OZ_BM = 128;   // data rows per tile (TMEM lanes)
 constexpr int OZ_BN = 64;    // factor rows per tile (TMEM columns per accumulator)
 constexpr int OZ_BK = 128;   // bytes (= k) per TMA box row (SWIZZLE_128B)
 constexpr int OZ_MAXKP = 256;  // resident factor slices: S x BN x Kp bytes of shared memory
+
+// digit pairs (i, j), i, j < S, i + j < NW: the MMAs per k step of a tile
+constexpr int oz_pairs() {
+  int n = 0;
+  for (int i = 0; i < OZ_S; ++i)
+    for (int j = 0; j < OZ_S; ++j) n += (i + j < OZ_NW) ? 1 : 0;
+  return n;
+}
 
 // Split operand: S digit planes [S][rows_p][kp] (int8, k contiguous, zero padded) and the row
 // exponents e[rows_p]; the tensor map views the planes as a 2D [S rows_p] x [kp] int8 matrix.
