@@ -263,16 +263,16 @@ template <int I>
 __device__ __forceinline__ void oz_stage_mmas(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
                                               bool first_kc) {
   const uint32_t odd = tile & 1;
+  // k step outer, digit pair inner: consecutive MMAs share the A (data) operand
 #pragma unroll
-  for (int j = 0; j < OZ_S && I + j < OZ_NW; ++j) {
-    const uint32_t td = tbase + (uint32_t)((odd ? OZ_NW - 1 - (I + j) : (I + j)) * OZ_BN);
-    const uint32_t idesc = oz_idesc(I == 0, j == 0);
-    const bool first_touch = first_kc && (j == 0 || I == OZ_S - 1);
+  for (int kk = 0; kk < OZ_BK / 32; ++kk)
 #pragma unroll
-    for (int kk = 0; kk < OZ_BK / 32; ++kk)
-      mma_i8(td, da + 2 * kk, db_kc + (uint64_t)(j * (OZ_BN * OZ_BK >> 4) + 2 * kk), idesc,
+    for (int j = 0; j < OZ_S && I + j < OZ_NW; ++j) {
+      const uint32_t td = tbase + (uint32_t)((odd ? OZ_NW - 1 - (I + j) : (I + j)) * OZ_BN);
+      const bool first_touch = first_kc && (j == 0 || I == OZ_S - 1);
+      mma_i8(td, da + 2 * kk, db_kc + (uint64_t)(j * (OZ_BN * OZ_BK >> 4) + 2 * kk), oz_idesc(I == 0, j == 0),
              (kk != 0 || !first_touch) ? 1u : 0u);
-  }
+    }
 }
 
 template <bool LAM>
