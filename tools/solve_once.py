@@ -25,6 +25,11 @@ P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
 b = torch.from_numpy(rhs(a.cfg, A.N)).cuda()
 x = torch.empty_like(b)
 solve = fd.gmres_solve if a.solver == "gmres" else fd.bicgstab_solve
-for _ in range(a.reps):
+for it in range(a.reps):
+    if it == a.reps - 1:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()  # ncu --profile-from-start off: the last solve only
     rep = solve(ctx, A, P, b, x, orth=a.orth) if a.solver == "gmres" else solve(ctx, A, P, b, x)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print(a, rep)
