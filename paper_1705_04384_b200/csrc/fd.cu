@@ -385,6 +385,7 @@ int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, 
   OzGemmArgs g{};
   g.X = &Xz;
   g.F = &Fz;
+  g.K = P->n[l];
   g.y = Y;
   g.skip = skip;
   if (Xz.rows == 0) return FDIGA_OK;

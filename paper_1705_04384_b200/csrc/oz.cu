@@ -220,9 +220,12 @@ __host__ __device__ constexpr uint32_t oz_idesc(bool a_signed, bool b_signed) {
   return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
          ((uint32_t)(OZ_BM >> 4) << 24);
 }
-template <int I>
+template <int I, int NKS>
 __device__ __forceinline__ void oz_stage_mmas(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
                                               bool first_kc);
+template <int I>
+__device__ __noinline__ void oz_stage_mmas_rt(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
+                                              bool first_kc, int nks);
 constexpr int OZ_STAGES = 6;
 constexpr int OZ_EW = 8;                    // epilogue warps: 4 lane quarters x 2 column halves
 constexpr int OZ_EC = OZ_BN / (OZ_EW / 4);  // columns per epilogue thread
@@ -234,6 +237,7 @@ struct OzKernelArgs {
   int64_t M, Nf;     // data rows, factor rows
   int64_t x_rows_p, f_rows_p;
   int KC;            // 128-wide k chunks
+  int ks_last;       // K-steps of 32 in the last chunk that reach below the contraction length (1..4)
   int mt, nt;        // tiles along M and Nf
   const int32_t* ex;
   const int32_t* ef;
@@ -259,13 +263,29 @@ __device__ __forceinline__ int oz_slot(int t, uint32_t tile) { return (tile & 1)
 // others unsigned: the instruction descriptor is chosen per pair.  In the first k chunk (descending digits)
 // pair (I, 0) is the first write of weight I, and for the first digit (S - 1) also pair (I, 1) of weight
 // I + 1 = NW - 1: those MMAs overwrite their slot.
-template <int I>
+template <int I, int NKS>
 __device__ __forceinline__ void oz_stage_mmas(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
                                               bool first_kc) {
   const uint32_t odd = tile & 1;
-  // k step outer, digit pair inner: consecutive MMAs share the A (data) operand
+  // k step outer, digit pair inner: consecutive MMAs share the A (data) operand.  NKS K-steps of 32: fewer
+  // than 4 in a last chunk that holds only padding zeros past the contraction length
 #pragma unroll
-  for (int kk = 0; kk < OZ_BK / 32; ++kk)
+  for (int kk = 0; kk < NKS; ++kk)
+#pragma unroll
+    for (int j = 0; j < OZ_S && I + j < OZ_NW; ++j) {
+      const uint32_t td = tbase + (uint32_t)((odd ? OZ_NW - 1 - (I + j) : (I + j)) * OZ_BN);
+      const bool first_touch = first_kc && (j == 0 || I == OZ_S - 1);
+      mma_i8(td, da + 2 * kk, db_kc + (uint64_t)(j * (OZ_BN * OZ_BK >> 4) + 2 * kk), oz_idesc(I == 0, j == 0),
+             (kk != 0 || !first_touch) ? 1u : 0u);
+    }
+}
+
+template <int I>
+__device__ __noinline__ void oz_stage_mmas_rt(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
+                                              bool first_kc, int nks) {
+  const uint32_t odd = tile & 1;
+#pragma unroll 1
+  for (int kk = 0; kk < nks; ++kk)
 #pragma unroll
     for (int j = 0; j < OZ_S && I + j < OZ_NW; ++j) {
       const uint32_t td = tbase + (uint32_t)((odd ? OZ_NW - 1 - (I + j) : (I + j)) * OZ_BN);
@@ -358,6 +378,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
         for (int kc = 0; kc < KC; ++kc) {
           const uint64_t dbk = db0 + (uint64_t)(kc * OZ_S * (OZ_FBYTES >> 4));
           const bool first = kc == 0, last = kc == KC - 1;
+          const int nks = last ? a.ks_last : OZ_BK / 32;  // K-steps of 32 carrying real contraction indices
           // one ring stage per data digit, its digit pairs fully unrolled (descriptor offsets are immediates)
 #define OZ_STAGE(I)                                                                                  \
   {                                                                                                  \
@@ -368,7 +389,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
       mbar_wait(&sempty[oz_slot(I, tl)], (tl - 1) & 1);                                              \
       tc_fence_after();                                                                              \
     }                                                                                                \
-    if (mma) oz_stage_mmas<I>(tbase, tl, da0 + (uint64_t)(st * (OZ_XBYTES >> 4)), dbk, first);      \
+    if (mma) {                                                                                       \
+      const uint64_t da_ = da0 + (uint64_t)(st * (OZ_XBYTES >> 4));                                  \
+      if (nks == OZ_BK / 32)                                                                         \
+        oz_stage_mmas<I, OZ_BK / 32>(tbase, tl, da_, dbk, first);                                    \
+      else /* short last chunk: a runtime K-step loop keeps the issue code small */                 \
+        oz_stage_mmas_rt<I>(tbase, tl, da_, dbk, first, nks);                                        \
+    }                                                                                                \
     tc_commit(&empty[st]); /* frees the ring slot when these MMAs have read it */                    \
     if (last && !first) { /* ascending: weight I complete (and the last weight after the last digit) */ \
       tc_commit(&sfull[oz_slot(I, tl)]);                                                             \
@@ -567,6 +594,8 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
 int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   const OzOperand& X = *g.X;
   const OzOperand& F = *g.F;
+  FDIGA_CHECK(g.K >= 1 && g.K <= X.kp, FDIGA_ERR_INVALID_ARG, "oz_gemm: contraction length %lld outside (0, %lld]",
+              (long long)g.K, (long long)X.kp);
   FDIGA_CHECK(X.kp == F.kp && X.box_rows == OZ_BM && F.box_rows == OZ_BN, FDIGA_ERR_INVALID_ARG,
               "oz_gemm: operand mismatch");
   if (X.rows == 0 || F.rows == 0) return FDIGA_OK;
@@ -576,6 +605,7 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   a.x_rows_p = X.rows_p;
   a.f_rows_p = F.rows_p;
   a.KC = (int)(X.kp / OZ_BK);
+  a.ks_last = (int)((g.K - (a.KC - 1) * OZ_BK + 31) / 32);  // g.K: the true contraction length
   a.mt = (int)(X.rows_p / OZ_BM);
   a.nt = (int)(F.rows_p / OZ_BN);
   a.ex = X.exps;

@@ -56,6 +56,7 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
 struct OzGemmArgs {
   const OzOperand* X;  // data (M rows)
   const OzOperand* F;  // factor (Nf rows)
+  int64_t K;           // contraction length (<= kp; the digits past it are zero)
   double* y;
   int64_t inner, bstride, mstride, fstride;
   const double* lamD;
