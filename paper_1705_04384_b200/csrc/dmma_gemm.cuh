@@ -93,7 +93,8 @@ struct TileCfg {
 };
 
 // VA / VB: doubles per cp.async chunk for A / B (2 needs 16-byte aligned rows, else 1).
-template <class T, BLayout BL, int VA, int VB>
+// RAG: K is not a multiple of BK (the last k-tile runs only the k-steps that reach below K)
+template <class T, BLayout BL, int VA, int VB, bool RAG>
 __global__ void __launch_bounds__(T::THREADS, T::MINB) dmma_gemm_kernel(GemmParams p) {
   // programmatic dependent launch: this grid may start while the previous kernel of the stream drains;
   // nothing it produced (the B/A operand, the skip flag) is read before its completion is awaited here
@@ -263,8 +264,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) dmma_gemm_kernel(GemmPara
 #pragma unroll
           for (int j = 0; j < T::NJ; ++j) dmma_8x8x4(acc[i][j], af[i][kk], bf[j][kk]);
     } else {
-#pragma unroll
-      for (int kk = 0; kk < T::BK / 4; ++kk) {
+      auto kstep = [&](int kk) {
         double af[T::MI], bf[T::NJ];
 #pragma unroll
         for (int i = 0; i < T::MI; ++i) af[i] = a_s[i * 8 * T::SA + kk * 4];
@@ -279,6 +279,16 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) dmma_gemm_kernel(GemmPara
         for (int i = 0; i < T::MI; ++i)
 #pragma unroll
           for (int j = 0; j < T::NJ; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+      };
+      // the last k-tile runs only the k-steps of 4 that reach below K (K = 131: 1 of 4); a separate,
+      // non-unrolled loop, so the hot unrolled loop stays free of predicates
+      const int ksteps = (RAG && kt == KT - 1) ? (K - kt * T::BK + 3) >> 2 : T::BK / 4;
+      if (!RAG || ksteps >= T::BK / 4) {
+#pragma unroll
+        for (int kk = 0; kk < T::BK / 4; ++kk) kstep(kk);
+      } else {
+#pragma unroll 1
+        for (int kk = 0; kk < ksteps; ++kk) kstep(kk);
       }
     }
   }

@@ -30,14 +30,16 @@ const bool g_pdl = [] {
 
 template <class T, BLayout BL, int VA, int VB>
 int launch_variant(fdiga_ctx* ctx, cudaStream_t stream, GemmParams p) {
-  auto kern = dmma_gemm_kernel<T, BL, VA, VB>;
+  auto kern = (p.K % T::BK) ? dmma_gemm_kernel<T, BL, VA, VB, true> : dmma_gemm_kernel<T, BL, VA, VB, false>;
   constexpr size_t smem = T::template smem_bytes<BL>();
   static bool attr_set = false;  // per instantiation (single device per process is assumed here)
   if (!attr_set) {
-    FDIGA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    // the whole unified L1/shared array as shared memory: several CTAs of 54-76 KB per SM
-    FDIGA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    (int)cudaSharedmemCarveoutMaxShared));
+    for (auto k : {dmma_gemm_kernel<T, BL, VA, VB, true>, dmma_gemm_kernel<T, BL, VA, VB, false>}) {
+      FDIGA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      // the whole unified L1/shared array as shared memory: several CTAs of 54-76 KB per SM
+      FDIGA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      (int)cudaSharedmemCarveoutMaxShared));
+    }
     attr_set = true;
   }
   p.tiles_m = (p.M + T::BM - 1) / T::BM;
