@@ -329,10 +329,10 @@ int broadcast_factors(fd_plan* P) {
 }
 
 // int8-split tensor-core mode products (oz.cu) for 3D real-spectrum plans (single-rank or slab-sharded) with
-// 192 <= n_l <= 256 -- where they beat the DMMA products on a B200 (n = 256: 1.38 vs 1.72 ms per apply;
-// at n = 128 / 131 the short contractions leave the tensor cores idle and DMMA wins).
-// FDIGA_FD_OZ=0 / 1 forces the choice (1: any n_l <= 256).  A static rule, so every run -- also under a
-// profiler -- takes the same kernels.
+// 192 <= n_l <= 512 -- where they beat the DMMA products on a B200 (n = 256: 1.43 vs 1.72 ms per apply,
+// n = 384: 6.2 vs 8.4 ms, n = 512: 18.4 vs 25.9 ms; at n = 128 / 131 the short contractions leave the tensor
+// cores idle and DMMA wins).  FDIGA_FD_OZ=0 / 1 forces the choice (1: any n_l <= 512).  A
+// static rule, so every run -- also under a profiler -- takes the same kernels.
 bool oz_eligible(const fd_plan* P) {
   if (P->d != 3 || P->has_pairs) return false;
   for (int l = 0; l < 3; ++l)

@@ -114,35 +114,40 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
 
 // inner > 1: the contracted index k is strided; rows m = b inner + i.  A block stages a K x 32 tile
 // (coalesced over i), takes the column maxima, and writes the digit rows k-contiguous (transposed).
+// CW columns i per block (32 for K <= 256; 16 for longer contractions, so a K x CW tile stays <= 64 KB and
+// three blocks fit an SM).  Lane l of a warp covers column l % CW of rows k = l / CW (mod 32 / CW).
+template <int CW>
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __restrict__ x, int64_t batch, int K,
                                                             int64_t inner, int8_t* __restrict__ digits,
                                                             int32_t* __restrict__ exps, int64_t rows_p, int kp,
                                                             const double* __restrict__ lam_row,
                                                             const double* __restrict__ lam_k, const int* skip) {
   if (skip && *skip) return;
-  // [K][32] tile, column i of row k stored at i ^ ((k / 8) mod 16): conflict-free both for the row-wise
+  constexpr int RPW = 32 / CW;  // rows per warp instruction
+  // [K][CW] tile, column i of row k stored at i ^ ((k / 8) mod CW): conflict-free both for the row-wise
   // staging (lanes = i) and for the digit pass (lanes = 8-row chunks c of one column i)
   extern __shared__ double tile[];
-  __shared__ double pmax[8][32];
-  __shared__ int es[32];
+  __shared__ double pmax[8 * RPW][CW];
+  __shared__ int es[CW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t tiles_i = (inner + 31) / 32;
+  const int col = lane % CW, rsub = lane / CW;
+  const int64_t tiles_i = (inner + CW - 1) / CW;
   const int64_t b = blockIdx.x / tiles_i;
-  const int64_t i0 = (blockIdx.x % tiles_i) * 32;
+  const int64_t i0 = (blockIdx.x % tiles_i) * CW;
   const double* xb = x + b * K * inner;
   double mx = 0.0;
-  const bool iv = i0 + lane < inner;
-  // the whole K x 32 tile in flight at once: 8-byte cp.async (zero-filled outside [0, inner)), no registers
-  for (int k = warp; k < K; k += 8)
-    cp_async8(smem_u32(&tile[k * 32 + (lane ^ ((k >> 3) & 15))]), iv ? xb + (int64_t)k * inner + i0 + lane : xb,
-              iv ? 8 : 0);
+  const bool iv = i0 + col < inner;
+  // the whole K x CW tile in flight at once: 8-byte cp.async (zero-filled outside [0, inner)), no registers
+  for (int k = warp * RPW + rsub; k < K; k += 8 * RPW)
+    cp_async8(smem_u32(&tile[k * CW + (col ^ ((k >> 3) & (CW - 1)))]),
+              iv ? xb + (int64_t)k * inner + i0 + col : xb, iv ? 8 : 0);
   cp_async_commit();
   cp_async_wait<0>();
   // each thread revisits only the elements it copied itself: no barrier needed before this pass
   // the eigenvalue-sum divide of the FD (eq:FD3D) when the split feeds the backward mode-d product
-  const double lr = (lam_row && iv) ? lam_row[b * inner + i0 + lane] : 0.0;
-  for (int k = warp; k < K; k += 8) {
-    double* tp = &tile[k * 32 + (lane ^ ((k >> 3) & 15))];
+  const double lr = (lam_row && iv) ? lam_row[b * inner + i0 + col] : 0.0;
+  for (int k = warp * RPW + rsub; k < K; k += 8 * RPW) {
+    double* tp = &tile[k * CW + (col ^ ((k >> 3) & (CW - 1)))];
     double val = *tp;
     if (lam_row) {  // val / (lr + lam_k[k]): float-seeded reciprocal, two Newton steps (< 1 ulp off)
       const double dn = lr + lam_k[k];
@@ -154,26 +159,26 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
     }
     mx = fmax(mx, fabs(val));
   }
-  pmax[warp][lane] = mx;
+  pmax[warp * RPW + rsub][col] = mx;
   __syncthreads();
-  if (warp == 0) {
-    double m2 = pmax[0][lane];
+  if (threadIdx.x < CW) {
+    double m2 = pmax[0][threadIdx.x];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) m2 = fmax(m2, pmax[w][lane]);
+    for (int w = 1; w < 8 * RPW; ++w) m2 = fmax(m2, pmax[w][threadIdx.x]);
     const int e = row_exponent(m2);
-    es[lane] = e;
-    if (i0 + lane < inner) exps[b * inner + i0 + lane] = e;
+    es[threadIdx.x] = e;
+    if (i0 + threadIdx.x < inner) exps[b * inner + i0 + threadIdx.x] = e;
   }
   __syncthreads();
   const int cpr = kp / 8;  // 8-byte chunks per digit row
-  for (int item = threadIdx.x; item < 32 * cpr; item += 256) {
+  for (int item = threadIdx.x; item < CW * cpr; item += 256) {
     const int i = item / cpr, c = item % cpr;
     if (i0 + i >= inner) continue;
     double v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int k = c * 8 + j;
-      v[j] = k < K ? tile[k * 32 + (i ^ ((k >> 3) & 15))] : 0.0;
+      v[j] = k < K ? tile[k * CW + (i ^ ((k >> 3) & (CW - 1)))] : 0.0;
     }
     uint64_t w[OZ_S];
     split8(v, es[i], w);
@@ -295,7 +300,9 @@ __device__ __noinline__ void oz_stage_mmas_rt(uint32_t tbase, uint32_t tile, uin
     }
 }
 
-template <bool LAM>
+// STREAM = false: the CTA's factor digits for all k chunks stay resident (K <= 256).  STREAM = true (K up to
+// 512): one k chunk of the factor digits (7 x 8 KB) at a time, double-buffered, reloaded for every tile.
+template <bool LAM, bool STREAM>
 __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap xmap,
                                                          const __grid_constant__ CUtensorMap fmap, OzKernelArgs a) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -303,12 +310,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
   extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
   const int KC = a.KC;
-  uint8_t* sF = smem;                                 // [KC][S] factor chunks (resident)
-  uint8_t* sX = smem + OZ_S * KC * OZ_FBYTES;         // data ring
+  uint8_t* sF = smem;  // [KC][S] factor chunks (resident) or [2][S] (streamed)
+  uint8_t* sX = smem + OZ_S * (STREAM ? 2 : KC) * OZ_FBYTES;  // data ring
   uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_STAGES * OZ_XBYTES);
   uint64_t* empty = full + OZ_STAGES;
-  uint64_t* fbar = empty + OZ_STAGES;
-  uint64_t* sfull = fbar + 1;      // [NW] accumulator slot complete (MMA -> epilogue)
+  uint64_t* fbar = empty + OZ_STAGES;  // resident: [1] factor landed; streamed: [2] full + [2] empty
+  uint64_t* sfull = fbar + 4;      // [NW] accumulator slot complete (MMA -> epilogue)
   uint64_t* sempty = sfull + OZ_NW;  // [NW] accumulator slot drained (epilogue -> MMA)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_NW);
   double* sLF = reinterpret_cast<double*>(sempty + OZ_NW + 1);  // eigenvalues of the CTA's factor rows
@@ -320,7 +327,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(fbar, 1);
+    for (int f = 0; f < 4; ++f) mbar_init(&fbar[f], 1);
     for (int t = 0; t < OZ_NW; ++t) {
       mbar_init(&sfull[t], 1);
       mbar_init(&sempty[t], OZ_EW);
@@ -344,16 +351,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
 
   if (warp == OZ_EW) {
     if (lane == 0) {
-      // resident factor digit planes of this column tile, [kc][digit] chunks
-      mbar_arrive_expect_tx(fbar, (uint32_t)(OZ_S * KC * OZ_FBYTES));
-      for (int s = 0; s < OZ_S; ++s)
-        for (int kc = 0; kc < KC; ++kc)
-          tma_load_2d(sF + (kc * OZ_S + s) * OZ_FBYTES, &fmap, kc * OZ_BK, (int)(s * a.f_rows_p + n0), fbar);
-      uint32_t st = 0, ph = 0;
+      if (!STREAM) {  // resident factor digit planes of this column tile, [kc][digit] chunks
+        mbar_arrive_expect_tx(fbar, (uint32_t)(OZ_S * KC * OZ_FBYTES));
+        for (int s = 0; s < OZ_S; ++s)
+          for (int kc = 0; kc < KC; ++kc)
+            tma_load_2d(sF + (kc * OZ_S + s) * OZ_FBYTES, &fmap, kc * OZ_BK, (int)(s * a.f_rows_p + n0), fbar);
+      }
+      uint32_t st = 0, ph = 0, fc = 0;
       bool wrapped = false;
       for (int mt = mt_first; mt < a.mt; mt += per_nt) {
         const int m0 = mt * OZ_BM;
-        for (int kc = 0; kc < KC; ++kc)
+        for (int kc = 0; kc < KC; ++kc) {
+          if (STREAM) {  // this k chunk's factor digits into factor slot fc % 2
+            const uint32_t fs = fc & 1;
+            if (fc >= 2) mbar_wait(&fbar[2 + fs], ((fc >> 1) - 1) & 1);
+            mbar_arrive_expect_tx(&fbar[fs], (uint32_t)(OZ_S * OZ_FBYTES));
+            for (int s = 0; s < OZ_S; ++s)
+              tma_load_2d(sF + (fs * OZ_S + s) * OZ_FBYTES, &fmap, kc * OZ_BK, (int)(s * a.f_rows_p + n0), &fbar[fs]);
+            ++fc;
+          }
           for (int pos = 0; pos < OZ_S; ++pos) {
             const int i = kc == 0 ? OZ_S - 1 - pos : pos;  // the MMA warp's digit order
             if (wrapped) mbar_wait(&empty[st], ph ^ 1);
@@ -365,18 +381,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
               wrapped = true;
             }
           }
+        }
       }
     }
   } else if (warp == OZ_EW + 1) {
     if (lane == 0) {
-      mbar_wait(fbar, 0);
+      if (!STREAM) mbar_wait(fbar, 0);
       tc_fence_after();
       const uint64_t da0 = sdesc_sw128(smem_u32(sX)), db0 = sdesc_sw128(smem_u32(sF));
-      uint32_t st = 0, ph = 0, tl = 0;
+      uint32_t st = 0, ph = 0, tl = 0, fc = 0;
       const bool mma = !(a.dbg & 2);
       for (int mt = mt_first; mt < a.mt; mt += per_nt, ++tl) {
         for (int kc = 0; kc < KC; ++kc) {
-          const uint64_t dbk = db0 + (uint64_t)(kc * OZ_S * (OZ_FBYTES >> 4));
+          uint64_t dbk = db0 + (uint64_t)(kc * OZ_S * (OZ_FBYTES >> 4));
+          if (STREAM) {
+            const uint32_t fs = fc & 1;
+            mbar_wait(&fbar[fs], (fc >> 1) & 1);
+            tc_fence_after();
+            dbk = db0 + (uint64_t)(fs * OZ_S * (OZ_FBYTES >> 4));
+          }
           const bool first = kc == 0, last = kc == KC - 1;
           const int nks = last ? a.ks_last : OZ_BK / 32;  // K-steps of 32 carrying real contraction indices
           // one ring stage per data digit, its digit pairs fully unrolled (descriptor offsets are immediates)
@@ -413,6 +436,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
             OZ_STAGE(0) OZ_STAGE(1) OZ_STAGE(2) OZ_STAGE(3) OZ_STAGE(4) OZ_STAGE(5) OZ_STAGE(6)
           }
 #undef OZ_STAGE
+          if (STREAM) {
+            tc_commit(&fbar[2 + (fc & 1)]);  // the factor slot is free when this chunk's MMAs have read it
+            ++fc;
+          }
           if (first && last)  // single k chunk (descending): every weight completes at its end
             for (int t = 0; t < OZ_NW; ++t) tc_commit(&sfull[oz_slot(t, tl)]);
         }
@@ -519,7 +546,8 @@ int get_encode(EncodeTiledFn* fn) {
 }
 
 constexpr size_t oz_smem_bytes(int KC) {
-  return 1024 + (size_t)OZ_S * KC * OZ_FBYTES + (size_t)OZ_STAGES * OZ_XBYTES + (2 * OZ_STAGES + 1 + 2 * OZ_NW + 1) * 8 +
+  return 1024 + (size_t)OZ_S * (KC > 2 ? 2 : KC) * OZ_FBYTES + (size_t)OZ_STAGES * OZ_XBYTES +
+         (2 * OZ_STAGES + 4 + 2 * OZ_NW + 1) * 8 +
          OZ_BN * 2 * sizeof(double);
 }
 
@@ -576,15 +604,21 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
     else
       oz_split_rows_kernel<2><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.rows_p, (int)op.kp, skip);
   } else {
-    const size_t smem = (size_t)K * 32 * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      FDIGA_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      FDIGA_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      FDIGA_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr = true;
     }
-    const int64_t tiles = batch * ((inner + 31) / 32);
-    oz_split_cols_kernel<<<(unsigned)tiles, 256, smem, stream>>>(x, batch, (int)K, inner, op.digits, op.exps,
-                                                                  op.rows_p, (int)op.kp, lam_row, lam_k, skip);
+    if (K <= 256) {
+      const int64_t tiles = batch * ((inner + 31) / 32);
+      oz_split_cols_kernel<32><<<(unsigned)tiles, 256, (size_t)K * 32 * sizeof(double), stream>>>(
+          x, batch, (int)K, inner, op.digits, op.exps, op.rows_p, (int)op.kp, lam_row, lam_k, skip);
+    } else {
+      const int64_t tiles = batch * ((inner + 15) / 16);
+      oz_split_cols_kernel<16><<<(unsigned)tiles, 256, (size_t)K * 16 * sizeof(double), stream>>>(
+          x, batch, (int)K, inner, op.digits, op.exps, op.rows_p, (int)op.kp, lam_row, lam_k, skip);
+    }
   }
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());
@@ -626,10 +660,10 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   const size_t smem = oz_smem_bytes(a.KC);
   static bool attr = false;
   if (!attr) {
-    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)oz_smem_bytes(OZ_MAXKP / OZ_BK)));
-    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)oz_smem_bytes(OZ_MAXKP / OZ_BK)));
+    for (auto k : {oz_gemm_kernel<false, false>, oz_gemm_kernel<true, false>})
+      FDIGA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz_smem_bytes(2)));
+    for (auto k : {oz_gemm_kernel<false, true>, oz_gemm_kernel<true, true>})
+      FDIGA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz_smem_bytes(4)));
     attr = true;
   }
   // persistent grid: a multiple of the column-tile count, at most one CTA per SM (TMEM: 512 columns)
@@ -645,12 +679,11 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   attr_pdl[0].val.programmaticStreamSerializationAllowed = 0;
   cfg.attrs = attr_pdl;
   cfg.numAttrs = 1;
-  if (a.lamD)
-    FDIGA_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<true>, *reinterpret_cast<const CUtensorMap*>(X.tmap),
-                                  *reinterpret_cast<const CUtensorMap*>(F.tmap), a));
-  else
-    FDIGA_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<false>, *reinterpret_cast<const CUtensorMap*>(X.tmap),
-                                  *reinterpret_cast<const CUtensorMap*>(F.tmap), a));
+  const bool stream_f = a.KC > 2;
+  auto kern = a.lamD ? (stream_f ? oz_gemm_kernel<true, true> : oz_gemm_kernel<true, false>)
+                     : (stream_f ? oz_gemm_kernel<false, true> : oz_gemm_kernel<false, false>);
+  FDIGA_CUDA(cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(X.tmap),
+                                *reinterpret_cast<const CUtensorMap*>(F.tmap), a));
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());
   return FDIGA_OK;

@@ -20,7 +20,7 @@ constexpr int OZ_WSHIFT = 14 + 8 * (OZ_NW - 1);  // 2^(e_x + e_f - WSHIFT) scale
 constexpr int OZ_BM = 128;   // data rows per tile (TMEM lanes)
 constexpr int OZ_BN = 64;    // factor rows per tile (TMEM columns per accumulator)
 constexpr int OZ_BK = 128;   // bytes (= k) per TMA box row (SWIZZLE_128B)
-constexpr int OZ_MAXKP = 256;  // resident factor slices: S x BN x Kp bytes of shared memory
+constexpr int OZ_MAXKP = 512;  // contraction lengths up to 512 (factor digits resident up to 256, streamed above)
 
 // digit pairs (i, j), i, j < S, i + j < NW: the MMAs per k step of a tile
 constexpr int oz_pairs() {

@@ -1,8 +1,9 @@
 """GPU parity of the int8-split tensor-core FD path (oz.cu: exact int8 digit splitting on
 tcgen05.mma.kind::i8) against the CPU oracle.
 
-The path is forced with FDIGA_FD_OZ=1 (read when a plan is set up) so that ragged, tiny and Poisson shapes
-go through it; the default rule (3D, real spectra, 192 <= n_l <= 256) is checked separately; the sharded
+The path is forced with FDIGA_FD_OZ=1 (read when a plan is set up) so that ragged, tiny, Poisson and long
+(K > 256: streamed factor digits) shapes go through it; the default rule (3D, real spectra,
+192 <= n_l <= 512) is checked separately; the sharded
 variants are in test_gpu_sharded.py.  Bar: the
 north_star's 1e-12 relative l2 for fd_apply, GMRES counts within +-1 of the oracle.
 """
@@ -59,7 +60,8 @@ def _random_factors(ns, seed):
 
 
 @pytest.mark.parametrize("ns", [(1, 1, 1), (2, 3, 5), (7, 9, 11), (16, 16, 16), (33, 17, 40), (65, 65, 65),
-                                (130, 3, 129), (131, 131, 131), (200, 256, 192)])
+                                (130, 3, 129), (131, 131, 131), (200, 256, 192), (300, 40, 36), (20, 300, 24),
+                                (24, 20, 400)])
 def test_int8_fd_apply_matches_oracle(ctx, forced, ns):
     f, rng = _random_factors(ns, 300 + sum(ns))
     plan = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
@@ -85,7 +87,8 @@ def test_int8_cfg4_n256_is_the_default_path(ctx):
 
 
 @pytest.mark.parametrize("ns,expect", [((128, 128, 128), "dmma"), ((131, 131, 131), "dmma"),
-                                       ((256, 256, 256), "int8_split"), ((512, 512, 512), "dmma"),
+                                       ((256, 256, 256), "int8_split"), ((512, 512, 512), "int8_split"),
+                                       ((256, 256, 512), "int8_split"), ((513, 256, 256), "dmma"),
                                        ((256, 256), "dmma")])
 def test_int8_default_rule(ctx, ns, expect):
     U = [np.eye(n) for n in ns]
