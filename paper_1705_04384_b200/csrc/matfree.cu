@@ -34,9 +34,29 @@ __device__ __forceinline__ const double* mf_plane(const MfArgs& A, int64_t g, in
 
 // Issue the x box of tile `tile` into xs with cp.async (8-byte LDGSTS): warp w takes the planes
 // j3 = w, w + 8, ...; its two half-warps take the rows j2 = 0, 1 (+2, ...), lanes the contiguous j1.
-__device__ __forceinline__ void mf_issue_box(const MfArgs& A, int64_t tile, double* xs, int* lo, int* bx) {
-  const int tl = (int)tile, t1 = (int)A.t1, t2 = (int)A.t2;
-  const int q1 = tl % t1, q2 = (tl / t1) % t2, q3 = tl / (t1 * t2);
+// tile coordinates along the three directions; the persistent CTA walks them by a fixed stride (gridDim.x)
+// with carry propagation instead of per-tile integer divisions
+struct MfTileQ {
+  int q1, q2, q3;
+};
+__device__ __forceinline__ MfTileQ mf_tile_q(int tl, int t1, int t2) { return {tl % t1, (tl / t1) % t2, tl / (t1 * t2)}; }
+__device__ __forceinline__ MfTileQ mf_advance(MfTileQ q, MfTileQ d, int t1, int t2) {
+  q.q1 += d.q1;
+  if (q.q1 >= t1) {
+    q.q1 -= t1;
+    ++q.q2;
+  }
+  q.q2 += d.q2;
+  if (q.q2 >= t2) {
+    q.q2 -= t2;
+    ++q.q3;
+  }
+  q.q3 += d.q3;
+  return q;
+}
+
+__device__ __forceinline__ void mf_issue_box(const MfArgs& A, MfTileQ q, double* xs, int* lo, int* bx) {
+  const int q1 = q.q1, q2 = q.q2, q3 = q.q3;
   const int l1 = __ldg(A.box1 + 2 * q1), b1 = __ldg(A.box1 + 2 * q1 + 1);
   const int l2 = __ldg(A.box2 + 2 * q2), b2 = __ldg(A.box2 + 2 * q2 + 1);
   const int l3 = __ldg(A.box3 + 2 * q3), b3 = __ldg(A.box3 + 2 * q3 + 1);
@@ -78,11 +98,14 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
   double* x12 = x1 + 3 * T * ps1;
   __shared__ int lo_s[2][3], bx_s[2][3];
   int buf = 0;
-  if (blockIdx.x < ntiles) mf_issue_box(A, blockIdx.x, xs, lo_s[0], bx_s[0]);
+  const int t1 = (int)A.t1, t2 = (int)A.t2;
+  const MfTileQ dq = mf_tile_q((int)gridDim.x, t1, t2);
+  MfTileQ cq = mf_tile_q((int)blockIdx.x, t1, t2);
+  if (blockIdx.x < ntiles) mf_issue_box(A, cq, xs, lo_s[0], bx_s[0]);
   const int64_t n12 = A.n1 * A.n2;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
-  const int tl = (int)tile, t1 = (int)A.t1, t2 = (int)A.t2;
-  const int q1 = tl % t1, q2 = (tl / t1) % t2, q3 = tl / (t1 * t2);
+  const int q1 = cq.q1, q2 = cq.q2, q3 = cq.q3;
+  const MfTileQ nq = mf_advance(cq, dq, t1, t2);
   const int a1 = q1 * T, a2 = q2 * T, a3 = (int)A.o + q3 * T;  // first row of the tile (global; 32-bit)
   const int n1i = (int)A.n1, n2i = (int)A.n2, n3i = (int)A.n3, Wt = A.W;
   const int m1 = (int)(A.n1 - a1 < T ? A.n1 - a1 : T), m2 = (int)(A.n2 - a2 < T ? A.n2 - a2 : T),
@@ -140,7 +163,7 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
     }
   }
   __syncthreads();  // xs is free: prefetch the next tile's box
-  if (tile + gridDim.x < ntiles) mf_issue_box(A, tile + gridDim.x, xs, lo_s[buf ^ 1], bx_s[buf ^ 1]);
+  if (tile + gridDim.x < ntiles) mf_issue_box(A, nq, xs, lo_s[buf ^ 1], bx_s[buf ^ 1]);
   // ---- stage 2: direction 2 (thread: fixed (i1, i2), loop over j3)
   {
     const int i1 = tid & (T - 1), i2 = (tid / T) & (T - 1), jg = tid / (T * T);
@@ -251,6 +274,7 @@ __global__ void __launch_bounds__(NT, 2) matfree_kernel(MfArgs A) {
       }
     }
   }
+  cq = nq;
   }  // tile loop
 }
 
