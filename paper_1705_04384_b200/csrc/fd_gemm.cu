@@ -114,11 +114,14 @@ using NK15 = TileCfg<128, 128, 16, 2, 4, 4, 1>; // NK0 with k-permuted fragments
 // 4 CTAs per SM (<= 128 registers, 3 stages of k-permuted 16-byte fragments: 54-55 KB of shared memory)
 using KN16 = TileCfg<64, 64, 16, 2, 2, 3, 1, 0, 4>;
 using NK16 = TileCfg<64, 64, 16, 2, 2, 3, 1, 0, 4>;
+// 8-warp versions of the n in (128, 144] tiles: 16 warps per SM at 2 CTAs (short-K, one-wave shapes, n = 131)
+using KN17 = TileCfg<144, 64, 16, 2, 4, 3, 0, 0, 2>;  // warp 72x16, <= 128 registers
+using NK17 = TileCfg<64, 144, 16, 4, 2, 3, 0, 0, 2>;  // warp 16x72, <= 128 registers
 const char* kKnNames[] = {"128x128", "144x128", "72x128", "88x128", "64x64", "72x64",
-                          "128x64", "128x128k32", "144x64", "72x32", "72x16", "64x64kv", "64x128kv", "64x128np", "64x128np4", "128x128np", "64x64kv3m4"};
+                          "128x64", "128x128k32", "144x64", "72x32", "72x16", "64x64kv", "64x128kv", "64x128np", "64x128np4", "128x128np", "64x64kv3m4", "144x64w8"};
 const char* kNkNames[] = {"128x128", "128x144", "128x72", "128x88", "64x64", "64x72",
-                          "64x128", "128x128k32", "64x144", "32x72", "16x72", "64x64kv", "64x128kv", "64x128kv4", "128x64kv", "128x128kv", "64x64kv3m4"};
-constexpr int kNumCfg = 17;
+                          "64x128", "128x128k32", "64x144", "32x72", "16x72", "64x64kv", "64x128kv", "64x128kv4", "128x64kv", "128x128kv", "64x64kv3m4", "64x144w8"};
+constexpr int kNumCfg = 18;
 
 }  // namespace
 
@@ -149,6 +152,7 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 14: return launch_cfg<KN14, BLayout::KN>(ctx, stream, p);
       case 15: return launch_cfg<KN15, BLayout::KN>(ctx, stream, p);
       case 16: return launch_cfg<KN16, BLayout::KN>(ctx, stream, p);
+      case 17: return launch_cfg<KN17, BLayout::KN>(ctx, stream, p);
     }
   } else {
     switch (cfg) {
@@ -169,6 +173,7 @@ int gemm_launch(fdiga_ctx* ctx, cudaStream_t stream, BLayout L, int cfg, GemmPar
       case 14: return launch_cfg<NK14, BLayout::NK>(ctx, stream, p);
       case 15: return launch_cfg<NK15, BLayout::NK>(ctx, stream, p);
       case 16: return launch_cfg<NK16, BLayout::NK>(ctx, stream, p);
+      case 17: return launch_cfg<NK17, BLayout::NK>(ctx, stream, p);
     }
   }
   set_error("bad GEMM configuration %d", cfg);

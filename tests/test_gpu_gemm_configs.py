@@ -30,7 +30,7 @@ print(worst)
 ''' % ROOT
 
 
-@pytest.mark.parametrize("cfg", list(range(17)))
+@pytest.mark.parametrize("cfg", list(range(18)))
 def test_forced_gemm_config_matches_oracle(cfg):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
