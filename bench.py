@@ -68,7 +68,7 @@ def roofline(path, kern, flops, int8_ops, achieved_fp64, fp64_pk, traffic, ws):
         return {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TOP/s (int8)", "frac": ach / pk,
                 "traffic": traffic.get("oz_gemm") if isinstance(traffic, dict) else None,
                 "kernel": f"oz_gemm_kernel (tcgen05.mma.kind::i8, {g['launches_per_apply']} launches per apply, "
-                          f"{100 * g['share']:.0f}% of the apply; the int8 digit splits are the rest)",
+                          f"{100 * g['share']:.0f}% of the apply; the other steps under 'kernels')",
                 "int8_ops_per_apply": int8_ops, "avg_launch_ms": g["avg_ms"], "peak_source": src,
                 "kernels": kern, "fp64_equivalent": fp64_eq}
     if kern and "dmma" in kern:
@@ -486,15 +486,14 @@ def main():
     path, int8_ops = plan.path()
     # per-kernel durations of the apply (CUDA events after every launch on the ctx stream, single rank):
     # the dominant kernel's roofline is its own algorithmic work / its own average launch time
-    kern = None
-    if ws == 1:
-        per = {}
-        for _ in range(3):
-            for kind, kms in fd.fd_apply_timed(plan, x, s):
-                per.setdefault(kind, []).append(kms)
-        tot = sum(sum(v) for v in per.values())
-        kern = {k: {"launches_per_apply": len(v) // 3, "avg_ms": float(np.mean(v)), "share": sum(v) / tot}
-                for k, v in per.items()}
+    # every rank (fd_apply_timed is collective on sharded plans); rank 0's durations are reported
+    per = {}
+    for _ in range(3):
+        for kind, kms in fd.fd_apply_timed(plan, x, s):
+            per.setdefault(kind, []).append(kms)
+    tot = sum(sum(v) for v in per.values())
+    kern = {k: {"launches_per_apply": len(v) // 3, "avg_ms": float(np.mean(v)), "share": sum(v) / tot}
+            for k, v in per.items()}
 
     # e2e: same metric through the C ABI with pinned host buffers (H2D + apply + D2H per step)
     xh = torch.from_numpy(np.random.default_rng(4001 + rank).standard_normal(plan.N)).pin_memory()

@@ -166,10 +166,11 @@ double fd_apply_flops(const fd_plan* plan);
  * operations one apply issues on that path (2 M N K per digit-pair MMA, padded shapes), else 0. */
 enum { FDIGA_PATH_DMMA = 0, FDIGA_PATH_INT8_SPLIT = 1 };
 int fd_plan_path(const fd_plan* plan, double* int8_ops);
-/* One fd_apply (single-rank plans) with a CUDA event recorded on the ctx stream after every kernel it
- * launches; synchronises.  kernel_ms[k] = duration of kernel k (event to event), kernel_kind[k] = 0 (DMMA mode
- * product), 1 (int8 digit split) or 2 (int8 tensor-core GEMM), for k < cap; *count = kernels launched.
- * Diagnostics for per-kernel rooflines (bench.py); the events serialise nothing that fd_apply overlaps. */
+/* One fd_apply with a CUDA event recorded on the ctx stream after every kernel (and, sharded, after every
+ * exchange) it issues; synchronises; collective like fd_apply.  kernel_ms[k] = duration of step k (event to
+ * event), kernel_kind[k] = 0 (DMMA mode product), 1 (int8 digit split), 2 (int8 tensor-core GEMM), 3 (slab
+ * pack) or 4 (NCCL / loopback exchange), for k < cap; *count = steps.  Diagnostics for per-kernel rooflines
+ * (bench.py); the events serialise nothing that fd_apply overlaps. */
 int fd_apply_timed(fd_plan* plan, const double* r, double* s, float* kernel_ms, int* kernel_kind, int cap,
                    int* count);
 int fd_plan_destroy(fd_plan* plan);

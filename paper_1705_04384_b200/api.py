@@ -289,14 +289,15 @@ def fd_apply(plan, r, s):
 
 
 def fd_apply_timed(plan, r, s):
-    """One apply with per-kernel CUDA-event durations: list of (kind, ms), kind in {'dmma', 'split', 'int8_gemm'}."""
+    """One apply with per-kernel CUDA-event durations: list of (kind, ms), kind in {'dmma', 'split', 'int8_gemm',
+    'slab_pack', 'exchange'} (collective on sharded plans)."""
     cap = 64
     ms = (C.c_float * cap)()
     kind = (C.c_int32 * cap)()
     cnt = C.c_int(0)
     check(plan.ctx._lib.fd_apply_timed(plan.handle, _devptr(r, plan.N), _devptr(s, plan.N), ms, kind, cap,
                                        C.byref(cnt)), "fd_apply_timed")
-    names = {0: "dmma", 1: "split", 2: "int8_gemm"}
+    names = {0: "dmma", 1: "split", 2: "int8_gemm", 3: "slab_pack", 4: "exchange"}
     return [(names[kind[k]], float(ms[k])) for k in range(min(cnt.value, cap))]
 
 

@@ -61,7 +61,7 @@ struct fd_plan {
   OzOperand ozW[3], ozU[3], ozX[3];
   // fd_apply_timed: an event recorded after every kernel of the apply (nullptr: off)
   std::vector<cudaEvent_t>* tev = nullptr;
-  std::vector<int>* tkind = nullptr;  // 0 = DMMA mode product, 1 = int8 split, 2 = int8 GEMM
+  std::vector<int>* tkind = nullptr;  // 0 DMMA mode product, 1 int8 split, 2 int8 GEMM, 3 slab pack, 4 exchange
 };
 
 namespace {
@@ -713,9 +713,11 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
     slab_pack_kernel<<<g, 256, 0, ctx->stream>>>(b, a, c, Nin, nr, 0, skip);
     count_launch(ctx);
     FDIGA_CUDA(cudaGetLastError());
+    FDIGA_TRY(mark(P, 3));
   }
   plan_msgs(a, b);
   FDIGA_TRY(comm_exchange(ctx, snd, rcv));  // b = T(n_d x len)
+  FDIGA_TRY(mark(P, 4));
   if (P->oz) {  // the Lambda divide rides in the split feeding the backward product (chunk offset q0)
     FDIGA_TRY(oz_mode(P, 2, P->ozW[2], b, a, skip));
     FDIGA_TRY(oz_mode(P, 2, P->ozU[2], a, b, skip, true));
@@ -725,10 +727,12 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
   }
   plan_msgs(a, b);
   FDIGA_TRY(comm_exchange(ctx, rcv, snd));  // reverse: rows of T back to their slab owners, into a
+  FDIGA_TRY(mark(P, 4));
   if (c > 0) {
     slab_pack_kernel<<<g, 256, 0, ctx->stream>>>(a, b, c, Nin, nr, 1, skip);
     count_launch(ctx);
     FDIGA_CUDA(cudaGetLastError());
+    FDIGA_TRY(mark(P, 3));
   }
   if (d == 3 && P->oz) {
     FDIGA_TRY(oz_mode(P, 1, P->ozU[1], b, a, skip));
@@ -1054,7 +1058,6 @@ int fd_apply_timed(fd_plan* P, const double* r, double* s, float* kernel_ms, int
                    int* count) {
   FDIGA_CHECK(P && count, FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_TRY(bind(P->ctx));
-  FDIGA_CHECK(!P->ctx->sharded, FDIGA_ERR_NOT_SUPPORTED, "fd_apply_timed: single-rank plans only");
   std::vector<cudaEvent_t> ev;
   std::vector<int> kind;
   cudaEvent_t e0;
