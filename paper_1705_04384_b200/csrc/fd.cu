@@ -172,27 +172,20 @@ int block_solve(fd_plan* P, double* x, const int* skip) {
 // Slab <-> transpose-chunk staging of the sharded mode-d pass.  Chunk s of the inner index J is
 // [q_s, q_s + len_s) (balanced split of Nin over nranks); the staging buffer holds, for each s in
 // order, the c x len_s block X[i][q_s .. q_s + len_s) (offset c q_s), i.e. what travels to / from s.
-__device__ __forceinline__ int64_t chunk_of(int64_t J, int64_t Nin, int nr, int64_t* qs, int64_t* ls) {
-  const int64_t q = Nin / nr, rr = Nin % nr, bnd = rr * (q + 1);
-  const int64_t s = J < bnd ? J / (q + 1) : rr + (J - bnd) / q;
-  *qs = s * q + (s < rr ? s : rr);
-  *ls = q + (s < rr ? 1 : 0);
-  return s;
-}
 
+// slab <-> staging copy: plane i's chunk q is the contiguous slab range x[i Nin + qs, + ls) and the contiguous
+// staging range stage[c qs + i ls, + ls): one segment per (i, q), bps blocks per segment, no per-element index
+// arithmetic beyond the segment offset
 __global__ void slab_pack_kernel(const double* __restrict__ x, double* __restrict__ stage, int64_t c, int64_t Nin,
-                                 int nr, int unpack, const int* skip) {
+                                 int nr, int unpack, int bps, const int* skip) {
   if (skip && *skip) return;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < c * Nin; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / Nin, J = t - i * Nin;
-    int64_t qs, ls;
-    chunk_of(J, Nin, nr, &qs, &ls);
-    const int64_t so = c * qs + i * ls + (J - qs);
-    if (unpack)
-      stage[t] = x[so];  // here x is the staging buffer and stage the slab
-    else
-      stage[so] = x[t];
-  }
+  const int64_t seg = blockIdx.x / bps, sub = blockIdx.x % bps;
+  const int64_t i = seg / nr, q = seg % nr;
+  const int64_t base = Nin / nr, rr = Nin % nr;
+  const int64_t qs = q * base + (q < rr ? q : rr), ls = base + (q < rr ? 1 : 0);
+  const double* src = unpack ? x + c * qs + i * ls : x + i * Nin + qs;
+  double* dst = unpack ? stage + i * Nin + qs : stage + c * qs + i * ls;
+  for (int64_t t = sub * blockDim.x + threadIdx.x; t < ls; t += (int64_t)bps * blockDim.x) dst[t] = src[t];
 }
 
 // mode 1 (contiguous axis): Y(R x n1) = X(R x n1) * F^T
@@ -697,7 +690,6 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
   } else {
     FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, b, c, skip));
   }
-  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((c * Nin + 255) / 256, 8 * ctx->sm_count));
   std::vector<int64_t> so(nr), sc(nr), to(nr), tc(nr);
   FDIGA_TRY(fdiga_transpose_plan(Nin, nd, nr, ctx->rank, so.data(), sc.data(), to.data(), tc.data()));
   std::vector<P2PMsg> snd, rcv;
@@ -709,8 +701,12 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
       rcv.push_back({q, tr_side + to[q], (size_t)tc[q] * 8});
     }
   };
+  const int64_t lmax = (Nin + nr - 1) / nr, nseg = std::max<int64_t>(1, c * nr);  // c = 0: a rank without planes
+  const int bps = (int)std::max<int64_t>(1, std::min<int64_t>((lmax + 1023) / 1024,
+                                                               (8 * ctx->sm_count + nseg - 1) / nseg));
+  const unsigned gsegs = (unsigned)(c * nr * bps);
   if (c > 0) {
-    slab_pack_kernel<<<g, 256, 0, ctx->stream>>>(b, a, c, Nin, nr, 0, skip);
+    slab_pack_kernel<<<gsegs, 256, 0, ctx->stream>>>(b, a, c, Nin, nr, 0, bps, skip);
     count_launch(ctx);
     FDIGA_CUDA(cudaGetLastError());
     FDIGA_TRY(mark(P, 3));
@@ -729,7 +725,7 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
   FDIGA_TRY(comm_exchange(ctx, rcv, snd));  // reverse: rows of T back to their slab owners, into a
   FDIGA_TRY(mark(P, 4));
   if (c > 0) {
-    slab_pack_kernel<<<g, 256, 0, ctx->stream>>>(a, b, c, Nin, nr, 1, skip);
+    slab_pack_kernel<<<gsegs, 256, 0, ctx->stream>>>(a, b, c, Nin, nr, 1, bps, skip);
     count_launch(ctx);
     FDIGA_CUDA(cudaGetLastError());
     FDIGA_TRY(mark(P, 3));
