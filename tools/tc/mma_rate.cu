@@ -9,13 +9,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t a) {
   return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) |
          ((uint64_t)2 << 61);
 }
-template <int N>
+template <int N, bool RANDOM>
 __global__ void __launch_bounds__(128, 1) k(int iters, int* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* s = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
-  for (int i = threadIdx.x; i < (128 + 256) * 128 / 4; i += blockDim.x) ((int*)s)[i] = 0;
+  for (int i = threadIdx.x; i < (128 + 256) * 128 / 4; i += blockDim.x) ((int*)s)[i] = RANDOM ? (int)(i * 2654435761u + 12345u) : 0;
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -50,32 +50,33 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int* out) {
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(t));
   if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = 1;
 }
-template <int N>
+template <int N, bool RANDOM>
 void run() {
   int* out;
   cudaMalloc(&out, 4);
   const int smem = 1024 + (128 + 256) * 128;
-  cudaFuncSetAttribute(k<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k<N, RANDOM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 4000;
-  k<N><<<148, 128, smem>>>(10, out);
+  k<N, RANDOM><<<148, 128, smem>>>(10, out);
   cudaDeviceSynchronize();
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k<N><<<148, 128, smem>>>(iters, out);
+  k<N, RANDOM><<<148, 128, smem>>>(iters, out);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
   const double ops = 2.0 * 148 * iters * 8 * 128.0 * N * 32;
-  printf("N=%3d: %.3f ms, %.0f TOPS, %.1f ns per MMA per SM (err %s)\n", N, ms, ops / ms / 1e9, ms * 1e6 / (iters * 8.0),
+  printf("N=%3d random=%d: %.3f ms, %.0f TOPS, %.1f ns per MMA per SM (err %s)\n", N, (int)RANDOM, ms, ops / ms / 1e9, ms * 1e6 / (iters * 8.0),
          cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
-  run<32>();
-  run<64>();
-  run<128>();
-  run<256>();
+  run<64, false>();
+  run<64, true>();
+  run<128, false>();
+  run<128, true>();
+  run<256, true>();
   return 0;
 }
