@@ -213,11 +213,20 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+// Issued by a whole, converged warp with warp-uniform operands: one elected lane executes the MMA.  (Issuing
+// from a single-lane branch made the compiler wrap every MMA in an ELECT / R2UR.BROADCAST loop to build its
+// uniform-register operands: ~13 instructions and 43 ns per N = 64 MMA instead of ~26 ns.)
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
-          tmem_d),
+      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 // instruction descriptor: D s32, A / B s8 (signed digit 0) or u8, K-major, N = 64, M = 128
@@ -385,7 +394,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
       }
     }
   } else if (warp == OZ_EW + 1) {
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop (uniform operands); one elected lane issues
       if (!STREAM) mbar_wait(fbar, 0);
       tc_fence_after();
       const uint64_t da0 = sdesc_sw128(smem_u32(sX)), db0 = sdesc_sw128(smem_u32(sF));
@@ -419,10 +428,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
       else /* short last chunk: a runtime K-step loop keeps the issue code small */                 \
         oz_stage_mmas_rt<I>(tbase, tl, da_, dbk, first, nks);                                        \
     }                                                                                                \
-    tc_commit(&empty[st]); /* frees the ring slot when these MMAs have read it */                    \
+    tc_commit_elect(&empty[st]); /* frees the ring slot when these MMAs have read it */                    \
     if (last && !first) { /* ascending: weight I complete (and the last weight after the last digit) */ \
-      tc_commit(&sfull[oz_slot(I, tl)]);                                                             \
-      if (I == OZ_S - 1) tc_commit(&sfull[oz_slot(OZ_NW - 1, tl)]);                                  \
+      tc_commit_elect(&sfull[oz_slot(I, tl)]);                                                             \
+      if (I == OZ_S - 1) tc_commit_elect(&sfull[oz_slot(OZ_NW - 1, tl)]);                                  \
     }                                                                                                \
     if (++st == OZ_STAGES) {                                                                         \
       st = 0;                                                                                        \
@@ -437,11 +446,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
           }
 #undef OZ_STAGE
           if (STREAM) {
-            tc_commit(&fbar[2 + (fc & 1)]);  // the factor slot is free when this chunk's MMAs have read it
+            tc_commit_elect(&fbar[2 + (fc & 1)]);  // the factor slot is free when this chunk's MMAs have read it
             ++fc;
           }
           if (first && last)  // single k chunk (descending): every weight completes at its end
-            for (int t = 0; t < OZ_NW; ++t) tc_commit(&sfull[oz_slot(t, tl)]);
+            for (int t = 0; t < OZ_NW; ++t) tc_commit_elect(&sfull[oz_slot(t, tl)]);
         }
       }
     }

@@ -4,6 +4,7 @@
 //   bit 2: the instruction descriptor alternates s8/u8 operand types
 //   bit 3: tcgen05.commit to an mbarrier after every 20 MMAs
 //   bit 4: tcgen05.fence::after_thread_sync before every 20 MMAs
+//   bit 6: A from a 6-stage ring of 16 KB tiles (a fresh A tile every 20 MMAs, as the GEMM's data ring)
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -19,7 +20,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int* out) {
   uint8_t* s = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar, bar2;
   __shared__ uint32_t slot;
-  for (int i = threadIdx.x; i < (16384 + 7 * 8192) / 4; i += blockDim.x) ((int*)s)[i] = (int)(i * 2654435761u);
+  for (int i = threadIdx.x; i < (6 * 16384 + 7 * 8192) / 4; i += blockDim.x) ((int*)s)[i] = (int)(i * 2654435761u);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar2)));
@@ -35,10 +36,11 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int* out) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t t = slot;
   if (threadIdx.x == 0) {
-    const uint64_t da = sdesc(su32(s)), db0 = sdesc(su32(s + 16384));
+    const uint64_t da0 = sdesc(su32(s)), db0 = sdesc(su32(s + 6 * 16384));
     int cnt = 0;
     for (int it = 0; it < iters; ++it) {
       if (MODE & 16) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t da = da0 + ((MODE & 64) ? (uint64_t)((it % 6) * 1024) : 0);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
@@ -69,7 +71,7 @@ template <int MODE>
 void run() {
   int* out;
   cudaMalloc(&out, 4);
-  const int smem = 1024 + 16384 + 7 * 8192;
+  const int smem = 1024 + 6 * 16384 + 7 * 8192;
   cudaFuncSetAttribute(k<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
   k<MODE><<<148, 128, smem>>>(10, out);
@@ -87,11 +89,8 @@ void run() {
 }
 int main() {
   run<0>();
-  run<1>();
-  run<2>();
-  run<4>();
-  run<8>();
-  run<16>();
   run<31>();
+  run<64>();
+  run<95>();
   return 0;
 }
