@@ -213,10 +213,14 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
 // from a single-lane branch made the compiler wrap every MMA in an ELECT / R2UR.BROADCAST loop to build its
 // uniform-register operands: ~13 instructions and 43 ns per N = 64 MMA instead of ~26 ns.)
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  // the two descriptors share their high words (SBO, version, swizzle); only the low words (start address,
+  // LBO) differ, and offsets added to them never carry (shared addresses < 2^18): 32-bit operands
+  const uint32_t alo = (uint32_t)da, blo = (uint32_t)db, hi = (uint32_t)(da >> 32);
   asm volatile(
-      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
-      " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      "{\n .reg .pred p, e;\n .reg .b64 a, b;\n elect.sync _|e, 0xffffffff;\n mov.b64 a, {%1, %3};\n"
+      " mov.b64 b, {%2, %3};\n setp.ne.b32 p, %5, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [%0], a, b, %4, p;\n}\n" ::"r"(tmem_d),
+      "r"(alo), "r"(blo), "r"(hi), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
   asm volatile(
