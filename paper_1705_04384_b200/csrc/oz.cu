@@ -222,6 +222,18 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db
       " @e tcgen05.mma.cta_group::1.kind::i8 [%0], a, b, %4, p;\n}\n" ::"r"(tmem_d),
       "r"(alo), "r"(blo), "r"(hi), "r"(idesc), "r"(acc));
 }
+// single-thread variant, for use inside a warp-converged `if (elect_one())` around a whole stage
+__device__ __forceinline__ void mma_i8_1(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e = 0;
+  asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(e));
+  return e != 0;
+}
 __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
@@ -282,16 +294,20 @@ __device__ __forceinline__ void oz_stage_mmas(uint32_t tbase, uint32_t tile, uin
                                               bool first_kc) {
   const uint32_t odd = tile & 1;
   // k step outer, digit pair inner: consecutive MMAs share the A (data) operand.  NKS K-steps of 32: fewer
-  // than 4 in a last chunk that holds only padding zeros past the contraction length
+  // than 4 in a last chunk that holds only padding zeros past the contraction length.  One elected lane
+  // issues the whole stage (operands computed by the converged warp before the branch).
+  if (elect_one()) {
 #pragma unroll
-  for (int kk = 0; kk < NKS; ++kk)
+    for (int kk = 0; kk < NKS; ++kk)
 #pragma unroll
-    for (int j = 0; j < OZ_S && I + j < OZ_NW; ++j) {
-      const uint32_t td = tbase + (uint32_t)((odd ? OZ_NW - 1 - (I + j) : (I + j)) * OZ_BN);
-      const bool first_touch = first_kc && (j == 0 || I == OZ_S - 1);
-      mma_i8(td, da + 2 * kk, db_kc + (uint64_t)(j * (OZ_BN * OZ_BK >> 4) + 2 * kk), oz_idesc(I == 0, j == 0),
-             (kk != 0 || !first_touch) ? 1u : 0u);
-    }
+      for (int j = 0; j < OZ_S && I + j < OZ_NW; ++j) {
+        const uint32_t td = tbase + (uint32_t)((odd ? OZ_NW - 1 - (I + j) : (I + j)) * OZ_BN);
+        const bool first_touch = first_kc && (j == 0 || I == OZ_S - 1);
+        mma_i8_1(td, da + 2 * kk, db_kc + (uint64_t)(j * (OZ_BN * OZ_BK >> 4) + 2 * kk), oz_idesc(I == 0, j == 0),
+                 (kk != 0 || !first_touch) ? 1u : 0u);
+      }
+  }
+  __syncwarp();
 }
 
 template <int I>
