@@ -45,6 +45,20 @@ def fp64_peak():
     return best
 
 
+# The paper's own numbers (context only, not a target): BiCGStab + FD iterations / CPU seconds including the
+# preconditioner setup, Matlab R2015a on one core of an Intel Xeon i7-5820K at 3.30 GHz.
+PAPER_CONTEXT = {
+    "hardware": "Matlab R2015a (GeoPDEs, Tensorlab 3.0), one core of an Intel Xeon i7-5820K at 3.30 GHz (P:499)",
+    "tolerance": "unstated (Matlab bicgstab default 1e-6, DESIGN.md reading 16); times include the FD setup (P:528)",
+    "table2_collocation_quarter_ring_2d": {"h^-1=256,p=3": {"bicgstab_iters": 13.5, "seconds": 0.25},
+                                           "h^-1=1024,p=3": {"bicgstab_iters": 13.5, "seconds": 10.18}},
+    "table4_collocation_revolved_ring_3d": {"h^-1=64,p=3": {"bicgstab_iters": 19.5, "seconds": 1.04},
+                                            "h^-1=64,p=5": {"bicgstab_iters": 22.5, "seconds": 3.12}},
+    "comparable_here": "gmres.cfg2 (2D quarter annulus, 256^2 elements, p = 3) and gmres.cfg5 (3D thick ring, "
+                       "128^3 elements, p = 5: 2.25M DOFs vs the paper's 3D h^-1 = 64), solved to 1e-8",
+}
+
+
 def int8_peak():
     """Dense int8 tensor-core peak: MEASURED_PEAKS.json's cuBLAS bf16 (burst) x the nominal int8/bf16 ratio
     (4.5 / 2.25 PFLOP/s, B200_PROFILING.md).  Our own tcgen05.mma.kind::i8 issue loop measured 4.55 POP/s
@@ -594,6 +608,7 @@ def main():
             "cpu_baseline": cpu,
             "gmres": gm,
             "weak_scaling": weak,
+            "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(rec), flush=True)
     for h in (plan,):
