@@ -160,3 +160,21 @@ def test_int8_poisson_pencils_match_oracle(ctx, forced):
     s = torch.empty(n ** 3, dtype=torch.float64, device=DEV)
     fd.fd_apply(P, gpu(b), s)
     assert rel(host(s), fastdiag.apply(f, b)) <= 1e-10
+
+
+def test_fd_apply_timed_reports_every_kernel(ctx, monkeypatch):
+    # fd_apply_timed: one event-timed step per launched kernel, kinds by path; same result as fd_apply
+    ns = (24, 20, 16)
+    f, rng = _random_factors(ns, 5)
+    r = gpu(rng.standard_normal(int(np.prod(ns))))
+    for force, kinds in (("1", ["split", "int8_gemm"] * 6), ("0", ["dmma"] * 6)):
+        monkeypatch.setenv("FDIGA_FD_OZ", force)
+        plan = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
+        s1 = torch.empty_like(r)
+        s2 = torch.empty_like(r)
+        steps = fd.fd_apply_timed(plan, r, s1)
+        fd.fd_apply(plan, r, s2)
+        assert [k for k, _ in steps] == kinds
+        assert all(ms > 0 for _, ms in steps)
+        assert torch.equal(s1, s2)
+        plan.close()
