@@ -1,12 +1,14 @@
 // FD mode products on tcgen05 int8 tensor cores with exact digit splitting (see oz.cuh).
 //
-//   oz_split_*_kernel : FP64 operand -> S int8 digit planes + per-row exponents (HBM-bound pass)
-//   oz_gemm_kernel    : persistent, warp-specialised tcgen05 GEMM.  Warp 4 streams the data digit planes
-//                       through a TMA (SWIZZLE_128B) ring; warp 5 issues tcgen05.mma.kind::i8 from one
-//                       thread into S int32 accumulators in TMEM (one per digit-pair weight t = i + j);
-//                       warps 0-3 read them back with tcgen05.ld, combine in FP64, scale by the row
-//                       exponents, optionally divide by the eigenvalue sums, and store.  The factor's
-//                       digit planes for the CTA's column tile stay resident in shared memory.
+//   oz_split_*_kernel : FP64 operand -> S = 7 int8 digit planes + per-row exponents (HBM-bound pass; the
+//                       strided modes are transposed so every GEMM operand is K-major)
+//   oz_gemm_kernel    : persistent, warp-specialised tcgen05 GEMM.  Warp 8 streams the data digit planes
+//                       through a TMA (SWIZZLE_128B) ring; warp 9 (converged, one elected lane per stage)
+//                       issues tcgen05.mma.kind::i8 into NW = 8 int32 accumulators in TMEM (one per
+//                       digit-pair weight t = i + j); warps 0-7 read them back with tcgen05.ld, combine in
+//                       FP64, scale by the row exponents, optionally divide by the eigenvalue sums, and
+//                       store.  The factor's digit planes for the CTA's column tile stay resident in shared
+//                       memory (K <= 256) or stream one k chunk at a time (K <= 512).
 #include <cuda.h>
 
 #include <cmath>
@@ -277,10 +279,10 @@ struct OzKernelArgs {
 
 
 // Accumulator hand-off between tiles.  Weight t (digit pairs i + j = t) of tile T lives in TMEM slot
-// p(t, T) = t (T even) or S - 1 - t (T odd).  The first k chunk of a tile takes the data digits in
+// p(t, T) = t (T even) or NW - 1 - t (T odd).  The first k chunk of a tile takes the data digits in
 // descending order (digit i first touches weight i), later chunks ascending, so in the last chunk weight t
 // completes right after digit t.  The epilogue drains weights in ascending order, i.e. slots in the order
-// 0, 1, .., S - 1 for either parity, which is exactly the order in which the next tile first writes them:
+// 0, 1, .., NW - 1 for either parity, which is exactly the order in which the next tile first writes them:
 // the epilogue of tile T runs under the MMAs of tile T + 1.
 __device__ __forceinline__ int oz_slot(int t, uint32_t tile) { return (tile & 1) ? OZ_NW - 1 - t : t; }
 
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
   uint64_t* sempty = sfull + OZ_NW;  // [NW] accumulator slot drained (epilogue -> MMA)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_NW);
   double* sLF = reinterpret_cast<double*>(sempty + OZ_NW + 1);  // eigenvalues of the CTA's factor rows
-  double* sSF = sLF + OZ_BN;                                    // 2^(e_f - 7 (S + 1)) of the CTA's factor rows
+  double* sSF = sLF + OZ_BN;                                    // 2^(e_f - WSHIFT) of the CTA's factor rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
