@@ -46,9 +46,35 @@ __device__ __forceinline__ int row_exponent(double mx) {
   return e;
 }
 
-// 8 consecutive values -> S packed 8-byte digit words.  |x| 2^(62 - e) < 2^62 is taken to a 62-bit integer
-// (truncated: bits below 2^-62 of the row scale are beyond digit S anyway); digit i of |x| is then bits
-// [62 - 7 i, 69 - 7 i) of it, with the sign of x -- the truncated base-128 expansion of x 2^-e.
+// 1 / d for a normal d on the FP64 pipe (MUFU.RCP and the F2F conversions a float seed needs run on the XU
+// pipe, which bounds the dividing split): the bit-pattern seed 0x7FDE623822FC16E6 - bits(|d|) is within
+// 12.5 % of 1 / |d|; Newton r <- r + r (1 - |d| r) squares the relative error, so five steps reach rounding
+// level (0.125 -> 1.6e-2 -> 2.4e-4 -> 6e-8 -> 3.6e-15 -> 1e-29).
+__device__ __forceinline__ double rcp_fp64(double d) {
+  const double a = fabs(d);
+  double r = __longlong_as_double(0x7FDE623822FC16E6LL - __double_as_longlong(a));
+#pragma unroll
+  for (int i = 0; i < 5; ++i) r = fma(r, fma(-a, r, 1.0), r);
+  return copysign(r, d);
+}
+
+// q = floor(v) for |v| < 2^62 as two 32-bit words, on the FP64 pipe (the F2I.S64.F64 conversion runs on
+// the XU pipe).  h = floor(v 2^-32): adding 1.5 2^52 with round-down leaves it in the low mantissa word
+// (two's complement, |h| <= 2^30); l = floor(v - h 2^32) in [0, 2^32) the same way with 2^52.  Every
+// operation rounds down, and floor(rd(t)) = floor(t) for any t (the integer floor(t) is representable and
+// rounding is monotone): the scaling may underflow for tiny v, and v - h 2^32 for a tiny negative v
+// (2^32 - |v|) is not representable -- rounded to nearest it would give 2^32 and l = 0 instead of 2^32 - 1.
+__device__ __forceinline__ void q_words(double v, uint32_t& h, uint32_t& l) {
+  constexpr double M = 6755399441055744.0;  // 1.5 * 2^52
+  const double a = __dadd_rd(__dmul_rd(v, 0x1p-32), M);
+  h = (uint32_t)__double2loint(a);
+  const double lo = __fma_rd(-(a - M), 4294967296.0, v);
+  l = (uint32_t)__double2loint(__dadd_rd(lo, 4503599627370496.0));
+}
+
+// 8 consecutive values -> S packed 8-byte digit words.  q = floor(x 2^(62 - e)) in [-2^62, 2^62) (bits
+// below 2^-62 of the row scale are beyond digit S anyway; the scaling rounds down so that an underflowing
+// negative x still floors to -1); digit 0 = q >> 55 (signed), digits 1..6 = the bytes of q at bits 47..7.
 __device__ __forceinline__ void split8(const double (&v)[8], int e, uint64_t (&w)[OZ_S]) {
   static_assert(OZ_S == 7, "digit extraction written for a signed 8-bit leading digit and 6 unsigned bytes");
   const double sc = pow2(62 - e);
@@ -59,8 +85,8 @@ __device__ __forceinline__ void split8(const double (&v)[8], int e, uint64_t (&w
   for (int j = 0; j < 8; ++j) {
     // q = floor(x 2^(62 - e)) in [-2^62, 2^62): digit 0 = q >> 55 (signed, [-128, 127]), digits 1..6 = the
     // unsigned bytes of q at bits 47, 39, .., 7 (two's complement makes the lower digits non-negative)
-    const long long q = __double2ll_rd(v[j] * sc);
-    const uint32_t h = (uint32_t)((unsigned long long)q >> 32), l = (uint32_t)q;
+    uint32_t h, l;
+    q_words(__dmul_rd(v[j], sc), h, l);
     uint32_t d[OZ_S];
     d[0] = (h >> 23) & 255u;
     d[1] = (h >> 15) & 255u;
@@ -151,12 +177,8 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
   for (int k = warp * RPW + rsub; k < K; k += 8 * RPW) {
     double* tp = &tile[k * CW + (col ^ ((k >> 3) & (CW - 1)))];
     double val = *tp;
-    if (lam_row) {  // val / (lr + lam_k[k]): float-seeded reciprocal, two Newton steps (< 1 ulp off)
-      const double dn = lr + lam_k[k];
-      double r = (double)__frcp_rn((float)dn);
-      r = fma(r, fma(-dn, r, 1.0), r);
-      r = fma(r, fma(-dn, r, 1.0), r);
-      val *= r;
+    if (lam_row) {  // val / (lr + lam_k[k]) (< 1 ulp off), all on the FP64 pipe
+      val *= rcp_fp64(lr + lam_k[k]);
       *tp = val;
     }
     mx = fmax(mx, fabs(val));
