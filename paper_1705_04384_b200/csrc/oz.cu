@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
 
 // inner > 1: the contracted index k is strided; rows m = b inner + i.  A block stages a K x 32 tile
 // (coalesced over i), takes the column maxima, and writes the digit rows k-contiguous (transposed).
-// CW columns i per block (32 for K <= 256; 16 for longer contractions, so a K x CW tile stays <= 64 KB and
-// three blocks fit an SM).  Lane l of a warp covers column l % CW of rows k = l / CW (mod 32 / CW).
+// CW = 16 columns i per block (a K x 16 tile: 32 KB at K = 256, six blocks per SM; the launch site records
+// the measured alternatives).  Lane l of a warp covers column l % CW of rows k = l / CW (mod 32 / CW).
 template <int CW>
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __restrict__ x, int64_t batch, int K,
                                                             int64_t inner, int8_t* __restrict__ digits,
@@ -655,19 +655,14 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
   } else {
     static bool attr = false;
     if (!attr) {
-      FDIGA_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       FDIGA_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr = true;
     }
-    if (K <= 256) {
-      const int64_t tiles = batch * ((inner + 31) / 32);
-      oz_split_cols_kernel<32><<<(unsigned)tiles, 256, (size_t)K * 32 * sizeof(double), stream>>>(
-          x, batch, (int)K, inner, op.digits, op.exps, op.rows_p, (int)op.kp, lam_row, lam_k, skip);
-    } else {
-      const int64_t tiles = batch * ((inner + 15) / 16);
-      oz_split_cols_kernel<16><<<(unsigned)tiles, 256, (size_t)K * 16 * sizeof(double), stream>>>(
-          x, batch, (int)K, inner, op.digits, op.exps, op.rows_p, (int)op.kp, lam_row, lam_k, skip);
-    }
+    // 16 columns per block for every K (<= 512): 32 KB tiles at K = 256, six blocks per SM; at n = 256 this
+    // beats 32 columns (three blocks per SM: 1.351 vs 1.336 ms per apply) and 8 (64-byte row segments: 1.368)
+    const int64_t tiles = batch * ((inner + 15) / 16);
+    oz_split_cols_kernel<16><<<(unsigned)tiles, 256, (size_t)K * 16 * sizeof(double), stream>>>(
+        x, batch, (int)K, inner, op.digits, op.exps, op.rows_p, (int)op.kp, lam_row, lam_k, skip);
   }
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());
