@@ -77,31 +77,28 @@ __device__ __forceinline__ void q_words(double v, uint32_t& h, uint32_t& l) {
 // negative x still floors to -1); digit 0 = q >> 55 (signed), digits 1..6 = the bytes of q at bits 47..7.
 __device__ __forceinline__ void split8(const double (&v)[8], int e, uint64_t (&w)[OZ_S]) {
   static_assert(OZ_S == 7, "digit extraction written for a signed 8-bit leading digit and 6 unsigned bytes");
-  const double sc = pow2(62 - e);
-  uint32_t lo[OZ_S], hi[OZ_S];  // bytes 0-3 / 4-7 of every digit word
+  // q = floor(x 2^(62 - e)) in [-2^62, 2^62): digit 0 = q >> 55 (signed, [-128, 127]), digits 1..6 = the
+  // unsigned bytes of q at bits 47, 39, .., 7 (two's complement makes the lower digits non-negative).  Taken
+  // as q' = floor(x 2^(55 - e)) = q >> 7, every digit is a whole byte of q' (digit s = byte 6 - s), and four
+  // values' digits pack into a word with three byte permutes
+  const double sc = pow2(55 - e);
+  uint32_t h[8], l[8];
 #pragma unroll
-  for (int s = 0; s < OZ_S; ++s) lo[s] = hi[s] = 0;
+  for (int j = 0; j < 8; ++j) q_words(__dmul_rd(v[j], sc), h[j], l[j]);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    // q = floor(x 2^(62 - e)) in [-2^62, 2^62): digit 0 = q >> 55 (signed, [-128, 127]), digits 1..6 = the
-    // unsigned bytes of q at bits 47, 39, .., 7 (two's complement makes the lower digits non-negative)
-    uint32_t h, l;
-    q_words(__dmul_rd(v[j], sc), h, l);
-    uint32_t d[OZ_S];
-    d[0] = (h >> 23) & 255u;
-    d[1] = (h >> 15) & 255u;
-    d[2] = (h >> 7) & 255u;
-    d[3] = __funnelshift_l(l, h, 1) & 255u;  // bits 31..38
-    d[4] = (l >> 23) & 255u;
-    d[5] = (l >> 15) & 255u;
-    d[6] = (l >> 7) & 255u;
+  for (int s = 0; s < OZ_S; ++s) {
+    const unsigned b = (unsigned)(6 - s) & 3u;  // byte within the word: s = 0..2 from h, 3..6 from l
+    const unsigned sel = b | ((b + 4u) << 4);
+    uint32_t half[2];
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s) {
-      if (j < 4) lo[s] |= d[s] << (8 * j); else hi[s] |= d[s] << (8 * (j - 4));
+    for (int g = 0; g < 2; ++g) {
+      const uint32_t* src = s < 3 ? h : l;
+      const uint32_t t01 = __byte_perm(src[4 * g], src[4 * g + 1], sel);
+      const uint32_t t23 = __byte_perm(src[4 * g + 2], src[4 * g + 3], sel);
+      half[g] = __byte_perm(t01, t23, 0x5410);
     }
+    w[s] = ((uint64_t)half[1] << 32) | half[0];
   }
-#pragma unroll
-  for (int s = 0; s < OZ_S; ++s) w[s] = ((uint64_t)hi[s] << 32) | lo[s];
 }
 
 // inner == 1: rows of K contiguous values.  One warp per row, 8 values per lane per 256-wide chunk.
