@@ -28,7 +28,8 @@ DEV = torch.device("cuda:0")
 
 
 def rel(a, b):
-    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    sc = float(np.max(np.abs(b))) or 1.0  # scaled: the 2^540 rows would overflow the squared norms
+    return float(np.linalg.norm((a - b) / sc) / np.linalg.norm(b / sc))
 
 
 @pytest.fixture(scope="module")
@@ -103,9 +104,12 @@ def test_int8_override_off(ctx, monkeypatch):
     assert plan.path() == ("dmma", 0.0)
 
 
-def test_int8_zero_and_scaled_rows(ctx, forced):
-    # zero rows (exponent 0, all digits 0) and rows 2^+-300 apart: the per-row exponents keep every row's
-    # relative accuracy (a shared scale would flush the small rows)
+@pytest.mark.parametrize("sc", [300, 540])
+def test_int8_zero_and_scaled_rows(ctx, forced, sc):
+    # zero rows (exponent 0, all digits 0) and rows 2^+-sc apart: the per-row exponents keep every row's
+    # relative accuracy (a shared scale would flush the small rows).  Mode-3 fibres span both scales; at
+    # sc = 540 the small values underflow when scaled by the fibre's exponent, and a negative one must still
+    # floor to -1 (the splits round the scaling down)
     ns = (48, 40, 36)
     f, rng = _random_factors(ns, 7)
     plan = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
@@ -113,8 +117,8 @@ def test_int8_zero_and_scaled_rows(ctx, forced):
     fd.fd_apply(plan, torch.zeros_like(s), s)
     assert not host(s).any()
     r = rng.standard_normal(ns[::-1])
-    r[::2] *= 2.0 ** 300
-    r[1::2] *= 2.0 ** -300
+    r[::2] *= 2.0 ** sc
+    r[1::2] *= 2.0 ** -sc
     r = r.ravel()
     fd.fd_apply(plan, gpu(r), s)
     expect = fastdiag.apply(f, r)
