@@ -158,14 +158,6 @@ class WQDiscretisation:
         return self.assemble_wq() @ x
 
 
-def galerkin_1d_exact(ne: int, p: int):
-    """Exact univariate Galerkin factors (eq:univariateWQ): M_ij = int B_i B_j, K_ij = int B'_i B'_j."""
-    xg, wg = gauss_rule(ne, p, p + 2)
-    B0 = interior_values(ne, p, xg, 0)
-    B1 = interior_values(ne, p, xg, 1)
-    return B0.T @ (wg[:, None] * B0), B1.T @ (wg[:, None] * B1)
-
-
 def e_h(disc: WQDiscretisation):
     """e_h = || H^{-1/2} (A_wq - A_G) H^{-1/2} ||_2 (Table 1), dense (small sizes only)."""
     E = (disc.assemble_wq() - disc.assemble_galerkin()).toarray()

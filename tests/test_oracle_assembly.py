@@ -212,3 +212,31 @@ def test_rotating_wind_is_angular_on_the_ring():
     F, J, _ = geo.thick_ring(xi)
     v = np.linalg.solve(J, geo.wind(geo.WIND_ROTATING, F, (3.0,))[..., None])[..., 0]
     np.testing.assert_allclose(v, np.tile([0.0, 6.0 / np.pi, 0.0], (20, 1)), atol=1e-12)
+
+
+@pytest.mark.parametrize("ns", [(2, 3), (3, 2), (2, 3, 4), (4, 3, 2), (3, 1, 2)])
+def test_kron_preconditioner_builders_match_entrywise_definition(ns):
+    # P = sum_k (x)_{l=d..1} (K_l if l == k else M_l) with i_1 fastest, written
+    # out entry by entry: P[i, j] = sum_k prod_l A^{(k)}_l[i_l, j_l].  Anisotropic sizes and distinct random
+    # factors per direction, so a swapped Kronecker order or a factor acting on the wrong index fails.
+    rng = np.random.default_rng(sum(ns) * 7 + len(ns))
+    d = len(ns)
+    Ms = [rng.standard_normal((n, n)) for n in ns]
+    Ks = [rng.standard_normal((n, n)) for n in ns]
+    N = int(np.prod(ns))
+
+    def multi(i):  # flat index -> (i_1, .., i_d), i_1 fastest
+        out = []
+        for n in ns:
+            out.append(i % n)
+            i //= n
+        return out
+
+    E = np.zeros((N, N))
+    for i in range(N):
+        ii = multi(i)
+        for j in range(N):
+            jj = multi(j)
+            E[i, j] = sum(np.prod([(Ks[l] if l == k else Ms[l])[ii[l], jj[l]] for l in range(d)]) for k in range(d))
+    np.testing.assert_allclose(assembly.kron_preconditioner_dense(Ms, Ks), E, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(assembly.kron_preconditioner_sparse(Ms, Ks).toarray(), E, rtol=1e-13, atol=1e-13)
