@@ -162,10 +162,18 @@ int fd_host_sync(fd_plan* plan);
 double fd_apply_flops(const fd_plan* plan);
 /* Kernel family of the mode products: FDIGA_PATH_DMMA (FP64 mma.sync DMMA tiles) or FDIGA_PATH_INT8_SPLIT
  * (exact int8 digit splitting on tcgen05.mma.kind::i8 with TMEM accumulators; 3D real-spectrum plans with
- * 192 <= n_l <= 256 by default, single-rank or sharded).  int8_ops (may be NULL) receives the int8 tensor-core
+ * 192 <= n_l <= 512 by default, single-rank or sharded).  int8_ops (may be NULL) receives the int8 tensor-core
  * operations one apply issues on that path (2 M N K per digit-pair MMA, padded shapes), else 0. */
 enum { FDIGA_PATH_DMMA = 0, FDIGA_PATH_INT8_SPLIT = 1 };
 int fd_plan_path(const fd_plan* plan, double* int8_ops);
+/* Select the kernel family of this plan's mode products (default: the rule above).  FDIGA_PATH_DMMA is IEEE
+ * FP64 (every output of a mode product is an FP64 dot product; always allowed).  FDIGA_PATH_INT8_SPLIT
+ * needs d = 3, a real spectrum and n_l <= 512 (else NOT_SUPPORTED, plan unchanged); its accuracy contract
+ * (DESIGN.md §5.1): per mode product y = F x, |y^ - y| <= 8u|y| + 2^-51.9 K max_k|x_k| max_k|F_ik| for every
+ * output (u = 2^-53, K the contraction length) -- FP64-level relative to the fibre and factor-row maxima,
+ * not componentwise -- and fibres / factor rows holding NaN/Inf, a nonzero |x| below 2^-24 of the row's
+ * scale, or exponents below -900 are computed as IEEE FP64 dot products instead.  Synchronous. */
+int fd_plan_set_path(fd_plan* plan, int path);
 /* One fd_apply with a CUDA event recorded on the ctx stream after every kernel (and, sharded, after every
  * exchange) it issues; synchronises; collective like fd_apply.  kernel_ms[k] = duration of step k (event to
  * event), kernel_kind[k] = 0 (DMMA mode product), 1 (int8 digit split), 2 (int8 tensor-core GEMM), 3 (slab

@@ -68,6 +68,7 @@ SIGNATURES = {
     "fd_host_sync": (C.c_int, [C.c_void_p]),
     "fd_apply_flops": (C.c_double, [C.c_void_p]),
     "fd_plan_path": (C.c_int, [C.c_void_p, c_double_p]),
+    "fd_plan_set_path": (C.c_int, [C.c_void_p, C.c_int]),
     "fd_apply_timed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_float), c_int32_p, C.c_int,
                                  C.POINTER(C.c_int)]),
     "fd_plan_destroy": (C.c_int, [C.c_void_p]),

@@ -166,6 +166,11 @@ class FDPlan:
             check(k, "fd_plan_path")
         return ("int8_split" if k == 1 else "dmma"), float(ops.value)
 
+    def set_path(self, path):
+        """Select the mode-product kernels: 'dmma' (IEEE FP64) or 'int8_split' (fd_plan_set_path)."""
+        code = {"dmma": 0, "int8_split": 1}[path]
+        check(self.ctx._lib.fd_plan_set_path(self.handle, code), "fd_plan_set_path")
+
     def close(self):
         if self.handle:
             if self.ctx.handle:  # a closed context already destroyed its children

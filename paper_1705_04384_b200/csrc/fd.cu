@@ -326,10 +326,14 @@ int broadcast_factors(fd_plan* P) {
 // n = 384: 6.2 vs 8.4 ms, n = 512: 18.4 vs 25.9 ms; at n = 128 / 131 the short contractions leave the tensor
 // cores idle and DMMA wins).  FDIGA_FD_OZ=0 / 1 forces the choice (1: any n_l <= 512).  A
 // static rule, so every run -- also under a profiler -- takes the same kernels.
-bool oz_eligible(const fd_plan* P) {
+bool oz_supported(const fd_plan* P) {  // shapes and spectra the int8 kernels handle at all
   if (P->d != 3 || P->has_pairs) return false;
   for (int l = 0; l < 3; ++l)
     if (P->n[l] > OZ_MAXKP) return false;
+  return true;
+}
+bool oz_eligible(const fd_plan* P) {  // the default rule
+  if (!oz_supported(P)) return false;
   const char* e = getenv("FDIGA_FD_OZ");
   if (e && e[0] == '0') return false;
   if (e && e[0] == '1') return true;
@@ -348,8 +352,8 @@ OzShapes oz_shapes(const fd_plan* P) {
   return {{P->n[1] * c, P->n[0] * c, P->len}};
 }
 
-int oz_setup(fd_plan* P) {
-  if (!oz_eligible(P)) return FDIGA_OK;
+int oz_setup(fd_plan* P, bool force = false) {
+  if (!(force ? oz_supported(P) : oz_eligible(P))) return FDIGA_OK;
   cudaStream_t st = P->ctx->stream;
   const OzShapes sh = oz_shapes(P);
   for (int l = 0; l < 3; ++l) {
@@ -369,7 +373,7 @@ int oz_setup(fd_plan* P) {
 //   l = 1: slab, data rows (i3, i1), k = i2 (the split transposes)
 //   l = 2: chunk T[i3][q] (q over len inner indices), data rows q, k = i3; divide_input: X / (lam_inner[q0 + q] +
 //          lam_3[i3]) first (the Lambda divide of eq:FD3D, applied as the data enters the backward product)
-int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, const int* skip,
+int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* Fs, const double* X, double* Y, const int* skip,
             bool divide_input = false) {
   const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
   const int64_t c = P->e - P->o, len = P->len;
@@ -381,6 +385,9 @@ int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, 
   g.K = P->n[l];
   g.y = Y;
   g.skip = skip;
+  g.xs = X;  // the FP64 operands, for the outputs of wide rows (oz.cuh: guard)
+  g.fs = Fs;
+  g.ldf = P->ld[l];
   if (Xz.rows == 0) return FDIGA_OK;
   if (l == 0) {
     FDIGA_TRY(oz_split(P->ctx, st, X, n2 * c, n1, 1, n1, Xz, skip));
@@ -388,19 +395,25 @@ int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, 
     g.bstride = 0;
     g.mstride = n1;
     g.fstride = 1;
+    g.xs_b = 0, g.xs_i = n1, g.xs_k = 1;
   } else if (l == 1) {
     FDIGA_TRY(oz_split(P->ctx, st, X, c, n2, n1, 0, Xz, skip));
     g.inner = n1;
     g.bstride = n1 * n2;
     g.mstride = 1;
     g.fstride = n1;
+    g.xs_b = n1 * n2, g.xs_i = 1, g.xs_k = n1;
   } else {
-    FDIGA_TRY(oz_split(P->ctx, st, X, 1, n3, len, 0, Xz, skip, divide_input ? P->lam_inner + P->q0 : nullptr,
-                       divide_input ? P->lam[2] : nullptr));
+    const double* lr = divide_input ? P->lam_inner + P->q0 : nullptr;
+    const double* lk = divide_input ? P->lam[2] : nullptr;
+    FDIGA_TRY(oz_split(P->ctx, st, X, 1, n3, len, 0, Xz, skip, lr, lk));
     g.inner = len;
     g.bstride = 0;
     g.mstride = 1;
     g.fstride = len;
+    g.xs_b = 0, g.xs_i = 1, g.xs_k = len;
+    g.lam_row = lr;
+    g.lam_k = lk;
   }
   FDIGA_TRY(mark(P, 1));
   FDIGA_TRY(oz_gemm(P->ctx, st, g));
@@ -410,13 +423,13 @@ int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* X, double* Y, 
 int fd_apply_oz(fd_plan* P, const double* r, double* s, const int* skip) {
   double* a = P->t0.p;
   double* b = P->t1.p;
-  FDIGA_TRY(oz_mode(P, 0, P->ozW[0], r, a, skip));
-  FDIGA_TRY(oz_mode(P, 1, P->ozW[1], a, b, skip));
+  FDIGA_TRY(oz_mode(P, 0, P->ozW[0], P->W[0], r, a, skip));
+  FDIGA_TRY(oz_mode(P, 1, P->ozW[1], P->W[1], a, b, skip));
   // the Lambda divide rides in the split that feeds the backward mode-3 product
-  FDIGA_TRY(oz_mode(P, 2, P->ozW[2], b, a, skip));
-  FDIGA_TRY(oz_mode(P, 2, P->ozU[2], a, b, skip, true));
-  FDIGA_TRY(oz_mode(P, 1, P->ozU[1], b, a, skip));
-  return oz_mode(P, 0, P->ozU[0], a, s, skip);
+  FDIGA_TRY(oz_mode(P, 2, P->ozW[2], P->W[2], b, a, skip));
+  FDIGA_TRY(oz_mode(P, 2, P->ozU[2], P->U[2], a, b, skip, true));
+  FDIGA_TRY(oz_mode(P, 1, P->ozU[1], P->U[1], b, a, skip));
+  return oz_mode(P, 0, P->ozU[0], P->U[0], a, s, skip);
 }
 
 int finish_plan(fd_plan* P) {
@@ -682,8 +695,8 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
   const int64_t c = P->e - P->o, Nin = P->Nin, len = P->len;
   // forward modes 1..d-1 -> b (slab layout)
   if (d == 3 && P->oz) {
-    FDIGA_TRY(oz_mode(P, 0, P->ozW[0], r, a, skip));
-    FDIGA_TRY(oz_mode(P, 1, P->ozW[1], a, b, skip));
+    FDIGA_TRY(oz_mode(P, 0, P->ozW[0], P->W[0], r, a, skip));
+    FDIGA_TRY(oz_mode(P, 1, P->ozW[1], P->W[1], a, b, skip));
   } else if (d == 3) {
     FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2 * c, skip));
     FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, c, nullptr, nullptr, skip));
@@ -715,8 +728,8 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
   FDIGA_TRY(comm_exchange(ctx, snd, rcv));  // b = T(n_d x len)
   FDIGA_TRY(mark(P, 4));
   if (P->oz) {  // the Lambda divide rides in the split feeding the backward product (chunk offset q0)
-    FDIGA_TRY(oz_mode(P, 2, P->ozW[2], b, a, skip));
-    FDIGA_TRY(oz_mode(P, 2, P->ozU[2], a, b, skip, true));
+    FDIGA_TRY(oz_mode(P, 2, P->ozW[2], P->W[2], b, a, skip));
+    FDIGA_TRY(oz_mode(P, 2, P->ozU[2], P->U[2], a, b, skip, true));
   } else {
     FDIGA_TRY(model(P, d - 1, P->W[d - 1], P->ld[d - 1], b, a, len, 1, P->lam[d - 1], P->lam_inner + P->q0, skip));
     FDIGA_TRY(model(P, d - 1, P->U[d - 1], P->ld[d - 1], a, b, len, 1, nullptr, nullptr, skip));
@@ -731,8 +744,8 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
     FDIGA_TRY(mark(P, 3));
   }
   if (d == 3 && P->oz) {
-    FDIGA_TRY(oz_mode(P, 1, P->ozU[1], b, a, skip));
-    FDIGA_TRY(oz_mode(P, 0, P->ozU[0], a, s, skip));
+    FDIGA_TRY(oz_mode(P, 1, P->ozU[1], P->U[1], b, a, skip));
+    FDIGA_TRY(oz_mode(P, 0, P->ozU[0], P->U[0], a, s, skip));
   } else if (d == 3) {
     FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, c, nullptr, nullptr, skip));
     FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2 * c, skip));
@@ -1094,6 +1107,21 @@ int fd_plan_path(const fd_plan* P, double* int8_ops) {
     *int8_ops = ops;
   }
   return P->oz ? FDIGA_PATH_INT8_SPLIT : FDIGA_PATH_DMMA;
+}
+
+int fd_plan_set_path(fd_plan* P, int path) {
+  FDIGA_CHECK(P, FDIGA_ERR_INVALID_ARG, "NULL plan");
+  FDIGA_CHECK(path == FDIGA_PATH_DMMA || path == FDIGA_PATH_INT8_SPLIT, FDIGA_ERR_INVALID_ARG, "unknown path %d", path);
+  FDIGA_TRY(bind(P->ctx));
+  if (path == FDIGA_PATH_DMMA) {
+    P->oz = false;  // the digit buffers stay allocated: switching back costs nothing
+    return FDIGA_OK;
+  }
+  FDIGA_CHECK(oz_supported(P), FDIGA_ERR_NOT_SUPPORTED,
+              "int8-split path: needs d = 3, a real spectrum and n_l <= %d", OZ_MAXKP);
+  if (!P->ozW[0].digits) FDIGA_TRY(oz_setup(P, true));
+  P->oz = true;
+  return FDIGA_OK;
 }
 
 int fd_plan_destroy(fd_plan* P) {

@@ -6,13 +6,15 @@
 //                       through a TMA (SWIZZLE_128B) ring; warp 9 (converged, one elected lane per stage)
 //                       issues tcgen05.mma.kind::i8 into NW = 8 int32 accumulators in TMEM (one per
 //                       digit-pair weight t = i + j); warps 0-7 read them back with tcgen05.ld, combine in
-//                       FP64, scale by the row exponents, optionally divide by the eigenvalue sums, and
-//                       store.  The factor's digit planes for the CTA's column tile stay resident in shared
-//                       memory (K <= 256) or stream one k chunk at a time (K <= 512).
+//                       FP64, scale by the row exponents and store; outputs of "wide" rows (oz.cuh: guard)
+//                       are computed instead as IEEE FP64 dot products from the FP64 operands.  The factor's
+//                       digit planes for the CTA's column tile stay resident in shared memory (K <= 256) or
+//                       stream one k chunk at a time (K <= 512).
 #include <cuda.h>
 
 #include <cmath>
 #include <cstdlib>
+#include <atomic>
 #include <mutex>
 
 #include "oz.cuh"
@@ -45,6 +47,26 @@ __device__ __forceinline__ int row_exponent(double mx) {
   if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): every |x| <= mx < 2^e
   return e;
 }
+
+// running guard state of a row: max |x|, min nonzero |x|, any non-finite value
+struct RowStat {
+  double mx = 0.0, mn = INFINITY;
+  bool nf = false;
+  __device__ __forceinline__ void add(double v) {
+    const double a = fabs(v);
+    mx = fmax(mx, a);
+    mn = fmin(mn, a == 0.0 ? INFINITY : a);
+    nf |= !(a <= 1.7976931348623157e308);  // NaN or Inf
+  }
+};
+
+// stored exponent of a row: e, or e + OZ_WIDE when the row goes to the FP64 fallback (oz.cuh)
+__device__ __forceinline__ int row_code(const RowStat& r, int e) {
+  const bool wide = r.nf || (r.mx > 0.0 && (e < OZ_EMIN || r.mn < pow2(e - OZ_SPREAD)));
+  return wide ? e + OZ_WIDE : e;
+}
+__device__ __forceinline__ bool code_wide(int c) { return c >= OZ_WIDE / 2; }
+__device__ __forceinline__ int code_exp(int c) { return code_wide(c) ? c - OZ_WIDE : c; }
 
 // 1 / d for a normal d on the FP64 pipe (MUFU.RCP and the F2F conversions a float seed needs run on the XU
 // pipe, which bounds the dividing split): the bit-pattern seed 0x7FDE623822FC16E6 - bits(|d|) is within
@@ -112,19 +134,23 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
   if (m >= rows) return;
   const double* xr = x + m * ldx;
   double v[NCH][8];
-  double mx = 0.0;
+  RowStat st;
 #pragma unroll
   for (int c = 0; c < NCH; ++c)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int k = c * 256 + lane * 8 + j;
       v[c][j] = k < K ? xr[k] : 0.0;
-      mx = fmax(mx, fabs(v[c][j]));
+      st.add(v[c][j]);
     }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  const int e = row_exponent(mx);
-  if (lane == 0) exps[m] = e;
+  for (int o = 16; o > 0; o >>= 1) {
+    st.mx = fmax(st.mx, __shfl_xor_sync(0xffffffffu, st.mx, o));
+    st.mn = fmin(st.mn, __shfl_xor_sync(0xffffffffu, st.mn, o));
+  }
+  st.nf = __any_sync(0xffffffffu, st.nf);
+  const int e = row_exponent(st.mx);
+  if (lane == 0) exps[m] = row_code(st, e);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int k0 = c * 256 + lane * 8;
@@ -152,7 +178,8 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
   // [K][CW] tile, column i of row k stored at i ^ ((k / 8) mod CW): conflict-free both for the row-wise
   // staging (lanes = i) and for the digit pass (lanes = 8-row chunks c of one column i)
   extern __shared__ double tile[];
-  __shared__ double pmax[8 * RPW][CW];
+  __shared__ double pmax[8 * RPW][CW], pmin[8 * RPW][CW];
+  __shared__ int pnf[CW];
   __shared__ int es[CW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int col = lane % CW, rsub = lane / CW;
@@ -160,8 +187,9 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
   const int64_t b = blockIdx.x / tiles_i;
   const int64_t i0 = (blockIdx.x % tiles_i) * CW;
   const double* xb = x + b * K * inner;
-  double mx = 0.0;
+  RowStat st;
   const bool iv = i0 + col < inner;
+  if (threadIdx.x < CW) pnf[threadIdx.x] = 0;
   // the whole K x CW tile in flight at once: 8-byte cp.async (zero-filled outside [0, inner)), no registers
   for (int k = warp * RPW + rsub; k < K; k += 8 * RPW)
     cp_async8(smem_u32(&tile[k * CW + (col ^ ((k >> 3) & (CW - 1)))]),
@@ -178,17 +206,24 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
       val *= rcp_fp64(lr + lam_k[k]);
       *tp = val;
     }
-    mx = fmax(mx, fabs(val));
+    st.add(val);
   }
-  pmax[warp * RPW + rsub][col] = mx;
+  pmax[warp * RPW + rsub][col] = st.mx;
+  pmin[warp * RPW + rsub][col] = st.mn;
+  __syncthreads();  // (also orders the pnf reset above before the flags below)
+  if (st.nf) atomicOr(&pnf[col], 1);
   __syncthreads();
   if (threadIdx.x < CW) {
-    double m2 = pmax[0][threadIdx.x];
+    RowStat r;
+    r.nf = pnf[threadIdx.x] != 0;
 #pragma unroll
-    for (int w = 1; w < 8 * RPW; ++w) m2 = fmax(m2, pmax[w][threadIdx.x]);
-    const int e = row_exponent(m2);
+    for (int w = 0; w < 8 * RPW; ++w) {
+      r.mx = fmax(r.mx, pmax[w][threadIdx.x]);
+      r.mn = fmin(r.mn, pmin[w][threadIdx.x]);
+    }
+    const int e = row_exponent(r.mx);
     es[threadIdx.x] = e;
-    if (i0 + threadIdx.x < inner) exps[b * inner + i0 + threadIdx.x] = e;
+    if (i0 + threadIdx.x < inner) exps[b * inner + i0 + threadIdx.x] = row_code(r, e);
   }
   __syncthreads();
   const int cpr = kp / 8;  // 8-byte chunks per digit row
@@ -286,15 +321,56 @@ struct OzKernelArgs {
   int KC;            // 128-wide k chunks
   int ks_last;       // K-steps of 32 in the last chunk that reach below the contraction length (1..4)
   int mt, nt;        // tiles along M and Nf
+  int K;             // contraction length
   const int32_t* ex;
   const int32_t* ef;
   double* y;
   int64_t inner, bstride, mstride, fstride;
-  const double* lamD;
-  const double* lamF;
+  bool yvec;         // y 16-byte aligned (double2 stores of column pairs when fstride == 1)
+  // FP64 operands for the wide-row fallback (oz.cuh: OzGemmArgs)
+  const double* xs;
+  int64_t xs_b, xs_i, xs_k;
+  const double* lam_row;
+  const double* lam_k;
+  const double* fs;
+  int64_t ldf;
   const int* skip;
-  int dbg;  // experiments (FDIGA_OZ_DBG): bit 0 = no epilogue work, bit 1 = no MMAs
 };
+
+// IEEE FP64 dot product sum_k F[f][k] X[m][k] from the FP64 operands (wide rows, oz.cuh), k ascending
+__device__ __forceinline__ double oz_fp64_dot(const OzKernelArgs& a, int64_t m, int64_t f) {
+  const double* xr = a.xs + (m / a.inner) * a.xs_b + (m % a.inner) * a.xs_i;
+  const double* fr = a.fs + f * a.ldf;
+  const double lr = a.lam_row ? a.lam_row[m] : 0.0;
+  double acc = 0.0;
+  for (int k = 0; k < a.K; ++k) {
+    double xv = xr[k * a.xs_k];
+    if (a.lam_row) xv = xv / (lr + a.lam_k[k]);
+    acc = fma(fr[k], xv, acc);
+  }
+  return acc;
+}
+__device__ __forceinline__ int64_t oz_out_off(const OzKernelArgs& a, int64_t m) {
+  return (m / a.inner) * a.bstride + (m % a.inner) * a.mstride;
+}
+// The outputs of one epilogue warp's 32 rows (row0 + lane) x 32 columns (f0 + j) that belong to a wide data
+// row (bit r of rowmask) or a wide factor row (bit j of colmask): computed here in FP64 and stored (the int8
+// results of those outputs are not stored).  Wide rows: lane j computes column f0 + j; wide columns: lane r
+// computes row row0 + r.
+__device__ __forceinline__ void oz_wide_outputs(const OzKernelArgs& a, int64_t row0, int64_t f0, uint32_t rowmask,
+                                             uint32_t colmask, int lane) {
+  for (uint32_t rm = rowmask; rm; rm &= rm - 1) {
+    const int64_t m = row0 + __ffs(rm) - 1;
+    const int64_t f = f0 + lane;
+    if (f < a.Nf) a.y[oz_out_off(a, m) + f * a.fstride] = oz_fp64_dot(a, m, f);
+  }
+  const int64_t m = row0 + lane;
+  const bool mine = m < a.M && !((rowmask >> lane) & 1u);
+  for (uint32_t cm = colmask; cm; cm &= cm - 1) {
+    const int64_t f = f0 + __ffs(cm) - 1;
+    if (mine && f < a.Nf) a.y[oz_out_off(a, m) + f * a.fstride] = oz_fp64_dot(a, m, f);
+  }
+}
 
 
 // Accumulator hand-off between tiles.  Weight t (digit pairs i + j = t) of tile T lives in TMEM slot
@@ -348,9 +424,10 @@ __device__ __noinline__ void oz_stage_mmas_rt(uint32_t tbase, uint32_t tile, uin
 
 // STREAM = false: the CTA's factor digits for all k chunks stay resident (K <= 256).  STREAM = true (K up to
 // 512): one k chunk of the factor digits (7 x 8 KB) at a time, double-buffered, reloaded for every tile.
-template <bool LAM, bool STREAM>
+template <bool STREAM>
 __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap xmap,
-                                                         const __grid_constant__ CUtensorMap fmap, OzKernelArgs a) {
+                                                         const __grid_constant__ CUtensorMap fmap,
+                                                         const __grid_constant__ OzKernelArgs a) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
@@ -364,8 +441,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
   uint64_t* sfull = fbar + 4;      // [NW] accumulator slot complete (MMA -> epilogue)
   uint64_t* sempty = sfull + OZ_NW;  // [NW] accumulator slot drained (epilogue -> MMA)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_NW);
-  double* sLF = reinterpret_cast<double*>(sempty + OZ_NW + 1);  // eigenvalues of the CTA's factor rows
-  double* sSF = sLF + OZ_BN;                                    // 2^(e_f - WSHIFT) of the CTA's factor rows
+  uint32_t* swide = tslot + 1;                                  // [2] wide factor rows of the CTA's 64 columns
+  double* sSF = reinterpret_cast<double*>(sempty + OZ_NW + 2);  // 2^(e_f - WSHIFT) of the CTA's factor rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -436,7 +513,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
       tc_fence_after();
       const uint64_t da0 = sdesc_sw128(smem_u32(sX)), db0 = sdesc_sw128(smem_u32(sF));
       uint32_t st = 0, ph = 0, tl = 0, fc = 0;
-      const bool mma = !(a.dbg & 2);
       for (int mt = mt_first; mt < a.mt; mt += per_nt, ++tl) {
         for (int kc = 0; kc < KC; ++kc) {
           uint64_t dbk = db0 + (uint64_t)(kc * OZ_S * (OZ_FBYTES >> 4));
@@ -458,7 +534,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
       mbar_wait(&sempty[oz_slot(I, tl)], (tl - 1) & 1);                                              \
       tc_fence_after();                                                                              \
     }                                                                                                \
-    if (mma) {                                                                                       \
+    {                                                                                                \
       const uint64_t da_ = da0 + (uint64_t)(st * (OZ_XBYTES >> 4));                                  \
       if (nks == OZ_BK / 32)                                                                         \
         oz_stage_mmas<I, OZ_BK / 32>(tbase, tl, da_, dbk, first);                                    \
@@ -495,21 +571,27 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
     // epilogue: warp w owns TMEM lanes 32w..32w+31 = data rows m0 + 32w + lane
     if (threadIdx.x < OZ_BN) {
       const int64_t f = n0 + threadIdx.x;
-      sSF[threadIdx.x] = pow2(f < a.Nf ? a.ef[f] - OZ_WSHIFT : 0);
-      sLF[threadIdx.x] = (LAM && f < a.Nf) ? a.lamF[f] : 0.0;
+      const int code = f < a.Nf ? a.ef[f] : 0;
+      sSF[threadIdx.x] = pow2(code_exp(code) - OZ_WSHIFT);
+      const uint32_t wm = __ballot_sync(0xffffffffu, code_wide(code));
+      if (lane == 0) swide[threadIdx.x >> 5] = wm;
     }
     asm volatile("bar.sync 1, %0;\n" ::"n"(OZ_EW * 32) : "memory");  // epilogue warps only
     uint32_t tl = 0;
     // warp w: TMEM lanes 32 (w % 4).. (data rows), columns [32 (w / 4), +32) of every weight slot
     const int quarter = warp & 3, c0 = (warp >> 2) * OZ_EC;
+    static_assert(OZ_EC == 32, "one 32-bit wide-column mask per epilogue warp");
+    const uint32_t colmask = swide[c0 >> 5];
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     for (int mt = mt_first; mt < a.mt; mt += per_nt, ++tl) {
-      const int64_t m = (int64_t)mt * OZ_BM + quarter * 32 + lane;
+      const int64_t row0 = (int64_t)mt * OZ_BM + quarter * 32;
+      const int64_t m = row0 + lane;
       const bool mv = m < a.M;
       const int64_t mm = mv ? m : 0;
-      const int64_t row_off = (mm / a.inner) * a.bstride + (mm % a.inner) * a.mstride;
-      const double sx = pow2(mv ? a.ex[mm] : 0);
-      const double lamd = (LAM && mv) ? a.lamD[mm] : 0.0;
+      const int64_t row_off = oz_out_off(a, mm);
+      const int code = mv ? a.ex[mm] : 0;
+      const double sx = pow2(code_exp(code));
+      const uint32_t rowmask = __ballot_sync(0xffffffffu, mv && code_wide(code));
       // sum_t 2^{8 (NW - 1 - t)} C_t over the weights as they complete (largest weight first)
       double acc[OZ_EC];
 #pragma unroll
@@ -520,48 +602,44 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
         mbar_wait(&sfull[p], tl & 1);
         tc_fence_after();
         const double w = (double)(1ll << (8 * (OZ_NW - 1 - t)));
-        if (!(a.dbg & 1)) {
 #pragma unroll
-          for (int c = 0; c < OZ_EC; c += 16) {
-            uint32_t v[16];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                : "r"(tbase + lane_off + (uint32_t)(p * OZ_BN + c0 + c)));
-            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        for (int c = 0; c < OZ_EC; c += 16) {
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(tbase + lane_off + (uint32_t)(p * OZ_BN + c0 + c)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-            // int32 -> double without I2F: the bits 0x43300000:(v ^ 2^31) are 2^52 + 2^31 + v exactly, and
-            // subtracting 2^52 + 2^31 is exact
-            for (int q = 0; q < 16; ++q)
-              acc[c + q] = fma(__hiloint2double(0x43300000, (int)(v[q] ^ 0x80000000u)) - 4503601774854144.0, w,
-                               acc[c + q]);
-          }
+          // int32 -> double without I2F: the bits 0x43300000:(v ^ 2^31) are 2^52 + 2^31 + v exactly, and
+          // subtracting 2^52 + 2^31 is exact
+          for (int q = 0; q < 16; ++q)
+            acc[c + q] = fma(__hiloint2double(0x43300000, (int)(v[q] ^ 0x80000000u)) - 4503601774854144.0, w,
+                             acc[c + q]);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[p]);
       }
-      if (mv && !(a.dbg & 1)) {
-        const bool vec = a.fstride == 1 && ((row_off + n0 + c0) & 1) == 0;
+      if (mv && !((rowmask >> lane) & 1u)) {
+        const bool vec = a.yvec && a.fstride == 1 && ((row_off + n0 + c0) & 1) == 0;
 #pragma unroll
         for (int c = 0; c < OZ_EC; c += 2) {
           const int64_t f = n0 + c0 + c;
           // two exact power-of-two scalings: the factor row's (with the digit weight) and the data row's
-          double y0 = (acc[c] * sSF[c0 + c]) * sx;
-          double y1 = (acc[c + 1] * sSF[c0 + c + 1]) * sx;
-          if (LAM) {
-            y0 = y0 / (lamd + sLF[c0 + c]);
-            y1 = y1 / (lamd + sLF[c0 + c + 1]);
-          }
-          if (vec && f + 1 < a.Nf) {  // contiguous factor index (mode 1): one 16-byte store per pair
+          const double y0 = (acc[c] * sSF[c0 + c]) * sx;
+          const double y1 = (acc[c + 1] * sSF[c0 + c + 1]) * sx;
+          const uint32_t wide2 = (colmask >> c) & 3u;  // outputs of wide factor rows are stored below
+          if (vec && f + 1 < a.Nf && !wide2) {  // contiguous factor index (mode 1): one 16-byte store per pair
             *reinterpret_cast<double2*>(a.y + row_off + f) = make_double2(y0, y1);
           } else {
-            if (f < a.Nf) a.y[row_off + f * a.fstride] = y0;
-            if (f + 1 < a.Nf) a.y[row_off + (f + 1) * a.fstride] = y1;
+            if (f < a.Nf && !(wide2 & 1u)) a.y[row_off + f * a.fstride] = y0;
+            if (f + 1 < a.Nf && !(wide2 & 2u)) a.y[row_off + (f + 1) * a.fstride] = y1;
           }
         }
       }
+      if (rowmask | colmask) oz_wide_outputs(a, row0, n0 + c0, rowmask, colmask, lane);
     }
   }
   tc_fence_before();
@@ -593,8 +671,14 @@ int get_encode(EncodeTiledFn* fn) {
 
 constexpr size_t oz_smem_bytes(int KC) {
   return 1024 + (size_t)OZ_S * (KC > 2 ? 2 : KC) * OZ_FBYTES + (size_t)OZ_STAGES * OZ_XBYTES +
-         (2 * OZ_STAGES + 4 + 2 * OZ_NW + 1) * 8 +
-         OZ_BN * 2 * sizeof(double);
+         (2 * OZ_STAGES + 4 + 2 * OZ_NW + 2) * 8 +
+         OZ_BN * sizeof(double);
+}
+
+// cudaFuncSetAttribute is per device: one flag bit per device ordinal
+bool attr_once(std::atomic<uint64_t>& done, int device) {
+  const uint64_t bit = 1ull << (device & 63);
+  return !(done.fetch_or(bit) & bit);
 }
 
 }  // namespace
@@ -650,11 +734,9 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
     else
       oz_split_rows_kernel<2><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.rows_p, (int)op.kp, skip);
   } else {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (attr_once(attr, ctx->device))
       FDIGA_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
     // 16 columns per block for every K (<= 512): 32 KB tiles at K = 256, six blocks per SM; at n = 256 this
     // beats 32 columns (three blocks per SM: 1.351 vs 1.336 ms per apply) and 8 (64-byte row segments: 1.368)
     const int64_t tiles = batch * ((inner + 15) / 16);
@@ -683,6 +765,7 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   a.ks_last = (int)((g.K - (a.KC - 1) * OZ_BK + 31) / 32);  // g.K: the true contraction length
   a.mt = (int)(X.rows_p / OZ_BM);
   a.nt = (int)(F.rows_p / OZ_BN);
+  a.K = (int)g.K;
   a.ex = X.exps;
   a.ef = F.exps;
   a.y = g.y;
@@ -690,22 +773,25 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   a.bstride = g.bstride;
   a.mstride = g.mstride;
   a.fstride = g.fstride;
-  a.lamD = g.lamD;
-  a.lamF = g.lamF;
+  a.yvec = (reinterpret_cast<uintptr_t>(g.y) & 15) == 0;
+  a.xs = g.xs;
+  a.xs_b = g.xs_b;
+  a.xs_i = g.xs_i;
+  a.xs_k = g.xs_k;
+  a.lam_row = g.lam_row;
+  a.lam_k = g.lam_k;
+  a.fs = g.fs;
+  a.ldf = g.ldf;
   a.skip = g.skip;
-  {
-    static const int dbg = getenv("FDIGA_OZ_DBG") ? atoi(getenv("FDIGA_OZ_DBG")) : 0;
-    a.dbg = dbg;
-  }
+  FDIGA_CHECK(g.xs && g.fs, FDIGA_ERR_INVALID_ARG, "oz_gemm: FP64 operands for the wide-row fallback missing");
   FDIGA_CHECK(a.nt <= ctx->sm_count, FDIGA_ERR_NOT_SUPPORTED, "oz_gemm: too many column tiles");
   const size_t smem = oz_smem_bytes(a.KC);
-  static bool attr = false;
-  if (!attr) {
-    for (auto k : {oz_gemm_kernel<false, false>, oz_gemm_kernel<true, false>})
-      FDIGA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz_smem_bytes(2)));
-    for (auto k : {oz_gemm_kernel<false, true>, oz_gemm_kernel<true, true>})
-      FDIGA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz_smem_bytes(4)));
-    attr = true;
+  static std::atomic<uint64_t> attr{0};
+  if (attr_once(attr, ctx->device)) {
+    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)oz_smem_bytes(2)));
+    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)oz_smem_bytes(4)));
   }
   // persistent grid: a multiple of the column-tile count, at most one CTA per SM (TMEM: 512 columns)
   int64_t grid = (int64_t)(ctx->sm_count / a.nt) * a.nt;
@@ -721,8 +807,7 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   cfg.attrs = attr_pdl;
   cfg.numAttrs = 1;
   const bool stream_f = a.KC > 2;
-  auto kern = a.lamD ? (stream_f ? oz_gemm_kernel<true, true> : oz_gemm_kernel<true, false>)
-                     : (stream_f ? oz_gemm_kernel<false, true> : oz_gemm_kernel<false, false>);
+  auto kern = stream_f ? oz_gemm_kernel<true> : oz_gemm_kernel<false>;
   FDIGA_CUDA(cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(X.tmap),
                                 *reinterpret_cast<const CUtensorMap*>(F.tmap), a));
   count_launch(ctx);

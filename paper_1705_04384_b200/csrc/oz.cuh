@@ -21,6 +21,14 @@ constexpr int OZ_BM = 128;   // data rows per tile (TMEM lanes)
 constexpr int OZ_BN = 64;    // factor rows per tile (TMEM columns per accumulator)
 constexpr int OZ_BK = 128;   // bytes (= k) per TMA box row (SWIZZLE_128B)
 constexpr int OZ_MAXKP = 512;  // contraction lengths up to 512 (factor digits resident up to 256, streamed above)
+// Guard ("accuracy contract"): a row (data fibre or factor row) is "wide" when it holds a
+// non-finite value, a nonzero |x| < 2^(e - OZ_SPREAD) (its digits would keep fewer than 55 - OZ_SPREAD = 31
+// significant bits of that value), or its exponent is below OZ_EMIN (the digit scaling 2^(55 - e) would leave
+// the double range).  The split marks it by adding OZ_WIDE to the stored exponent; the GEMM epilogue computes
+// every output of a wide data row or a wide factor row as an IEEE FP64 dot product from the FP64 operands.
+constexpr int OZ_SPREAD = 24;
+constexpr int OZ_EMIN = -900;
+constexpr int OZ_WIDE = 1 << 20;
 
 // digit pairs (i, j), i, j < S, i + j < NW: the MMAs per k step of a tile
 constexpr int oz_pairs() {
@@ -31,7 +39,8 @@ constexpr int oz_pairs() {
 }
 
 // Split operand: S digit planes [S][rows_p][kp] (int8, k contiguous, zero padded) and the row
-// exponents e[rows_p]; the tensor map views the planes as a 2D [S rows_p] x [kp] int8 matrix.
+// exponents e[rows_p] (+ OZ_WIDE for a wide row); the tensor map views the planes as a 2D [S rows_p] x [kp]
+// int8 matrix.
 struct OzOperand {
   int8_t* digits = nullptr;
   int32_t* exps = nullptr;
@@ -51,16 +60,23 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
              int64_t ldx, OzOperand& op, const int* skip, const double* lam_row = nullptr,
              const double* lam_k = nullptr);
 
-// y[off(m, f)] = sum_k F[f][k] X[m][k]  (/ (lamD[m] + lamF[f]) when lamD != nullptr), for data rows m < M
-// and factor rows f < Nf, off(m, f) = (m / inner) bstride + (m % inner) mstride + f fstride.
+// y[off(m, f)] = sum_k F[f][k] X[m][k] for data rows m < M and factor rows f < Nf,
+// off(m, f) = (m / inner) bstride + (m % inner) mstride + f fstride.
+// The FP64 operands the digits were split from (for the wide-row fallback): X[m][k] =
+// xs[(m / inner) xs_b + (m % inner) xs_i + k xs_k] (divided by lam_row[m] + lam_k[k] when lam_row is set, as the
+// split did), F[f][k] = fs[f ldf + k].
 struct OzGemmArgs {
   const OzOperand* X;  // data (M rows)
   const OzOperand* F;  // factor (Nf rows)
   int64_t K;           // contraction length (<= kp; the digits past it are zero)
   double* y;
   int64_t inner, bstride, mstride, fstride;
-  const double* lamD;
-  const double* lamF;
+  const double* xs;
+  int64_t xs_b, xs_i, xs_k;
+  const double* lam_row;
+  const double* lam_k;
+  const double* fs;
+  int64_t ldf;
   const int* skip;
 };
 int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& a);

@@ -66,13 +66,17 @@ def test_fd_apply_matches_oracle_shared_factors(ctx, ns):
     assert rel(host(s), expect) <= 1e-12
 
 
-@pytest.mark.parametrize("n", [128, 256, 512])
-def test_fd_apply_cfg4_full_size(ctx, n):
-    # BASELINE.json configs[3]: U ~ N(0,1), lam ~ U(1,100), x ~ N(0,1); W = U^{-1} from the oracle
+@pytest.mark.parametrize("n,path", [(128, None), (256, None), (512, None), (256, "dmma"), (512, "dmma")])
+def test_fd_apply_cfg4_full_size(ctx, n, path):
+    # BASELINE.json configs[3]: U ~ N(0,1), lam ~ U(1,100), x ~ N(0,1); W = U^{-1} from the oracle.  path None:
+    # the default rule (int8-split at 256 / 512); "dmma": the IEEE FP64 DMMA products at the headline sizes
     rng, U, lam = fd_sweep_factors(n)
     f = fastdiag.factors_from_eig(U, lam)
     x = fd_sweep_vector(rng, n ** 3)
     plan = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
+    if path:
+        plan.set_path(path)
+        assert plan.path()[0] == path
     s = torch.empty(n ** 3, dtype=torch.float64, device=DEV)
     fd.fd_apply(plan, gpu(x), s)
     assert rel(host(s), fastdiag.apply(f, x)) <= 1e-12
