@@ -361,6 +361,8 @@ int oz_setup(fd_plan* P, bool force = false) {
     FDIGA_TRY(oz_operand_alloc(P->ozU[l], P->n[l], P->n[l], OZ_BN));
     FDIGA_TRY(oz_split(P->ctx, st, P->W[l], P->n[l], P->n[l], 1, P->ld[l], P->ozW[l], nullptr));
     FDIGA_TRY(oz_split(P->ctx, st, P->U[l], P->n[l], P->n[l], 1, P->ld[l], P->ozU[l], nullptr));
+    FDIGA_TRY(oz_operand_set_ft(P->ozW[l], P->hW[l].data(), P->n[l]));
+    FDIGA_TRY(oz_operand_set_ft(P->ozU[l], P->hU[l].data(), P->n[l]));
     FDIGA_TRY(oz_operand_alloc(P->ozX[l], sh.rows[l], P->n[l], OZ_BM));
   }
   FDIGA_CUDA(cudaStreamSynchronize(st));

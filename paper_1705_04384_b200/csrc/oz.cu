@@ -6,16 +6,18 @@
 //                       through a TMA (SWIZZLE_128B) ring; warp 9 (converged, one elected lane per stage)
 //                       issues tcgen05.mma.kind::i8 into NW = 8 int32 accumulators in TMEM (one per
 //                       digit-pair weight t = i + j); warps 0-7 read them back with tcgen05.ld, combine in
-//                       FP64, scale by the row exponents and store; outputs of "wide" rows (oz.cuh: guard)
-//                       are computed instead as IEEE FP64 dot products from the FP64 operands.  The factor's
-//                       digit planes for the CTA's column tile stay resident in shared memory (K <= 256) or
-//                       stream one k chunk at a time (K <= 512).
+//                       FP64, scale by the row exponents and store.  The factor's digit planes for the CTA's
+//                       column tile stay resident in shared memory (K <= 256) or stream one k chunk at a time
+//                       (K <= 512).
+//                       Outputs of "wide" rows (oz.cuh: guard) are then recomputed by the CTA that owns them
+//                       as IEEE FP64 dot products of the FP64 operands (oz_cta_fixup).
 #include <cuda.h>
 
 #include <cmath>
 #include <cstdlib>
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "oz.cuh"
 #include "ptx.cuh"
@@ -25,8 +27,12 @@ namespace fdiga {
 void OzOperand::release() {
   if (digits) cudaFree(digits);
   if (exps) cudaFree(exps);
+  if (wide) cudaFree(wide);
+  if (ft) cudaFree(ft);
+  ft = nullptr;
   digits = nullptr;
   exps = nullptr;
+  wide = nullptr;
   rows = rows_p = kp = 0;
 }
 
@@ -127,7 +133,8 @@ __device__ __forceinline__ void split8(const double (&v)[8], int e, uint64_t (&w
 template <int NCH>
 __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __restrict__ x, int64_t rows, int K, int64_t ldx,
                                                             int8_t* __restrict__ digits, int32_t* __restrict__ exps,
-                                                            int64_t rows_p, int kp, const int* skip) {
+                                                            int32_t* __restrict__ wide, int64_t rows_p, int kp,
+                                                            const int* skip) {
   if (skip && *skip) return;
   const int lane = threadIdx.x & 31;
   const int64_t m = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -150,7 +157,11 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
   }
   st.nf = __any_sync(0xffffffffu, st.nf);
   const int e = row_exponent(st.mx);
-  if (lane == 0) exps[m] = row_code(st, e);
+  if (lane == 0) {
+    const int code = row_code(st, e);
+    exps[m] = code;
+    if (code_wide(code)) wide[2 + atomicAdd(wide, 1)] = (int32_t)m;
+  }
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int k0 = c * 256 + lane * 8;
@@ -170,7 +181,8 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
 template <int CW>
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __restrict__ x, int64_t batch, int K,
                                                             int64_t inner, int8_t* __restrict__ digits,
-                                                            int32_t* __restrict__ exps, int64_t rows_p, int kp,
+                                                            int32_t* __restrict__ exps, int32_t* __restrict__ wide,
+                                                            int64_t rows_p, int kp,
                                                             const double* __restrict__ lam_row,
                                                             const double* __restrict__ lam_k, const int* skip) {
   if (skip && *skip) return;
@@ -223,7 +235,11 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
     }
     const int e = row_exponent(r.mx);
     es[threadIdx.x] = e;
-    if (i0 + threadIdx.x < inner) exps[b * inner + i0 + threadIdx.x] = row_code(r, e);
+    if (i0 + threadIdx.x < inner) {
+      const int code = row_code(r, e);
+      exps[b * inner + i0 + threadIdx.x] = code;
+      if (code_wide(code)) wide[2 + atomicAdd(wide, 1)] = (int32_t)(b * inner + i0 + threadIdx.x);
+    }
   }
   __syncthreads();
   const int cpr = kp / 8;  // 8-byte chunks per digit row
@@ -334,41 +350,84 @@ struct OzKernelArgs {
   const double* lam_k;
   const double* fs;
   int64_t ldf;
+  const double* ft;  // F^T [k][f]
+  int32_t* xw;       // wide lists (oz.cuh: OzOperand::wide) of the data and the factor
+  const int32_t* fw;
   const int* skip;
 };
 
-// IEEE FP64 dot product sum_k F[f][k] X[m][k] from the FP64 operands (wide rows, oz.cuh), k ascending
-__device__ __forceinline__ double oz_fp64_dot(const OzKernelArgs& a, int64_t m, int64_t f) {
-  const double* xr = a.xs + (m / a.inner) * a.xs_b + (m % a.inner) * a.xs_i;
-  const double* fr = a.fs + f * a.ldf;
-  const double lr = a.lam_row ? a.lam_row[m] : 0.0;
-  double acc = 0.0;
-  for (int k = 0; k < a.K; ++k) {
-    double xv = xr[k * a.xs_k];
-    if (a.lam_row) xv = xv / (lr + a.lam_k[k]);
-    acc = fma(fr[k], xv, acc);
-  }
-  return acc;
-}
 __device__ __forceinline__ int64_t oz_out_off(const OzKernelArgs& a, int64_t m) {
   return (m / a.inner) * a.bstride + (m % a.inner) * a.mstride;
 }
-// The outputs of one epilogue warp's 32 rows (row0 + lane) x 32 columns (f0 + j) that belong to a wide data
-// row (bit r of rowmask) or a wide factor row (bit j of colmask): computed here in FP64 and stored (the int8
-// results of those outputs are not stored).  Wide rows: lane j computes column f0 + j; wide columns: lane r
-// computes row row0 + r.
-__device__ __forceinline__ void oz_wide_outputs(const OzKernelArgs& a, int64_t row0, int64_t f0, uint32_t rowmask,
-                                             uint32_t colmask, int lane) {
-  for (uint32_t rm = rowmask; rm; rm &= rm - 1) {
-    const int64_t m = row0 + __ffs(rm) - 1;
-    const int64_t f = f0 + lane;
-    if (f < a.Nf) a.y[oz_out_off(a, m) + f * a.fstride] = oz_fp64_dot(a, m, f);
+// X[m][k] of the FP64 data operand (divided by the eigenvalue sum when the split did so)
+__device__ __forceinline__ double oz_x(const OzKernelArgs& a, const double* xr, double lr, int k) {
+  const double xv = xr[k * a.xs_k];
+  return a.lam_row ? xv / (lr + a.lam_k[k]) : xv;
+}
+// The guard's fallback (oz.cuh), run by the epilogue warps of every GEMM CTA after its last tile: the outputs
+// of the CTA's tiles (its row tiles x its column tile) that belong to a wide data row (X's list) or a wide
+// factor row (F's list) are recomputed as IEEE FP64 dot products of the FP64 operands and stored over the
+// int8 results (each output has one owner CTA, so no grid-wide ordering is needed).  Items of 32 outputs:
+// the item's shared operand row (K values) is staged in shared memory; thread (c, s) of the 8 epilogue warps
+// sums k = s, s + 8, .. for output c (loads of F^T / of the data coalesced over c, 16 in flight), and the 8
+// partial sums per output are added in a fixed order.  The last CTA to finish resets X's list for the next
+// split.  No wide row: two loads and one atomic per CTA.
+__device__ __forceinline__ void oz_bar_epi() { asm volatile("bar.sync 1, %0;\n" ::"n"(256) : "memory"); }
+__device__ __forceinline__ void oz_fix_item(const OzKernelArgs& a, int64_t m, int64_t f, bool wide_row, double* sv,
+                                            double* part, int c, int sl) {
+  // sv holds the item's shared row; this thread's output is (m, f)
+  double acc = 0.0;
+  if (wide_row) {
+    const int64_t fc = min(f, a.Nf - 1);
+#pragma unroll 16
+    for (int k = sl; k < a.K; k += 8) acc = fma(a.ft[k * a.Nf + fc], sv[k], acc);
+  } else {
+    const int64_t mc = min(m, a.M - 1);
+    const double* xr = a.xs + (mc / a.inner) * a.xs_b + (mc % a.inner) * a.xs_i;
+    const double lr = a.lam_row ? a.lam_row[mc] : 0.0;
+#pragma unroll 16
+    for (int k = sl; k < a.K; k += 8) acc = fma(sv[k], oz_x(a, xr, lr, k), acc);
   }
-  const int64_t m = row0 + lane;
-  const bool mine = m < a.M && !((rowmask >> lane) & 1u);
-  for (uint32_t cm = colmask; cm; cm &= cm - 1) {
-    const int64_t f = f0 + __ffs(cm) - 1;
-    if (mine && f < a.Nf) a.y[oz_out_off(a, m) + f * a.fstride] = oz_fp64_dot(a, m, f);
+  part[sl * 32 + c] = acc;
+  oz_bar_epi();
+  if (sl == 0 && m < a.M && f < a.Nf) {
+    double t = part[c];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += part[q * 32 + c];
+    a.y[oz_out_off(a, m) + f * a.fstride] = t;
+  }
+  oz_bar_epi();
+}
+// mt_first / per_nt: the CTA's row tiles; [n0, n0 + BN) its factor rows.  Called by the 256 epilogue threads.
+__device__ void oz_cta_fixup(const OzKernelArgs& a, int32_t* xw, const int32_t* fw, int mt_first, int per_nt,
+                             int n0, double* sv, double* part) {
+  const int c = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int nx = *(volatile int32_t*)xw, nf = *(volatile const int32_t*)fw;
+  for (int i = 0; i < nx; ++i) {
+    const int64_t m = xw[2 + i];
+    const int mt = (int)(m / OZ_BM);
+    if (mt < mt_first || (mt - mt_first) % per_nt) continue;
+    const double* xr = a.xs + (m / a.inner) * a.xs_b + (m % a.inner) * a.xs_i;
+    const double lr = a.lam_row ? a.lam_row[m] : 0.0;
+    for (int k = threadIdx.x; k < a.K; k += 256) sv[k] = oz_x(a, xr, lr, k);
+    oz_bar_epi();
+    for (int h = 0; h < OZ_BN; h += 32) oz_fix_item(a, m, n0 + h + c, true, sv, part, c, sl);
+  }
+  for (int i = 0; i < nf; ++i) {
+    const int64_t f = fw[2 + i];
+    if (f < n0 || f >= n0 + OZ_BN) continue;
+    for (int k = threadIdx.x; k < a.K; k += 256) sv[k] = a.fs[f * a.ldf + k];
+    oz_bar_epi();
+    for (int mt = mt_first; mt < a.mt; mt += per_nt)
+      for (int r = 0; r < OZ_BM; r += 32) oz_fix_item(a, (int64_t)mt * OZ_BM + r + c, f, false, sv, part, c, sl);
+  }
+  // reset X's list once every CTA has read its count
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&xw[1], 1) == (int)gridDim.x - 1) {
+      xw[0] = 0;
+      xw[1] = 0;
+    }
   }
 }
 
@@ -441,8 +500,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
   uint64_t* sfull = fbar + 4;      // [NW] accumulator slot complete (MMA -> epilogue)
   uint64_t* sempty = sfull + OZ_NW;  // [NW] accumulator slot drained (epilogue -> MMA)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_NW);
-  uint32_t* swide = tslot + 1;                                  // [2] wide factor rows of the CTA's 64 columns
   double* sSF = reinterpret_cast<double*>(sempty + OZ_NW + 2);  // 2^(e_f - WSHIFT) of the CTA's factor rows
+  double* sFix = sSF + OZ_BN;                                   // fixup: [OZ_MAXKP] row + [8][32] partial sums
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -571,27 +630,19 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
     // epilogue: warp w owns TMEM lanes 32w..32w+31 = data rows m0 + 32w + lane
     if (threadIdx.x < OZ_BN) {
       const int64_t f = n0 + threadIdx.x;
-      const int code = f < a.Nf ? a.ef[f] : 0;
-      sSF[threadIdx.x] = pow2(code_exp(code) - OZ_WSHIFT);
-      const uint32_t wm = __ballot_sync(0xffffffffu, code_wide(code));
-      if (lane == 0) swide[threadIdx.x >> 5] = wm;
+      sSF[threadIdx.x] = pow2(code_exp(f < a.Nf ? a.ef[f] : 0) - OZ_WSHIFT);
     }
     asm volatile("bar.sync 1, %0;\n" ::"n"(OZ_EW * 32) : "memory");  // epilogue warps only
     uint32_t tl = 0;
     // warp w: TMEM lanes 32 (w % 4).. (data rows), columns [32 (w / 4), +32) of every weight slot
     const int quarter = warp & 3, c0 = (warp >> 2) * OZ_EC;
-    static_assert(OZ_EC == 32, "one 32-bit wide-column mask per epilogue warp");
-    const uint32_t colmask = swide[c0 >> 5];
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     for (int mt = mt_first; mt < a.mt; mt += per_nt, ++tl) {
-      const int64_t row0 = (int64_t)mt * OZ_BM + quarter * 32;
-      const int64_t m = row0 + lane;
+      const int64_t m = (int64_t)mt * OZ_BM + quarter * 32 + lane;
       const bool mv = m < a.M;
       const int64_t mm = mv ? m : 0;
       const int64_t row_off = oz_out_off(a, mm);
-      const int code = mv ? a.ex[mm] : 0;
-      const double sx = pow2(code_exp(code));
-      const uint32_t rowmask = __ballot_sync(0xffffffffu, mv && code_wide(code));
+      const double sx = pow2(code_exp(mv ? a.ex[mm] : 0));  // (outputs of wide rows: replaced by oz_fixup)
       // sum_t 2^{8 (NW - 1 - t)} C_t over the weights as they complete (largest weight first)
       double acc[OZ_EC];
 #pragma unroll
@@ -622,7 +673,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[p]);
       }
-      if (mv && !((rowmask >> lane) & 1u)) {
+      if (mv) {  // (outputs of wide rows: replaced by oz_cta_fixup after the last tile)
         const bool vec = a.yvec && a.fstride == 1 && ((row_off + n0 + c0) & 1) == 0;
 #pragma unroll
         for (int c = 0; c < OZ_EC; c += 2) {
@@ -630,17 +681,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
           // two exact power-of-two scalings: the factor row's (with the digit weight) and the data row's
           const double y0 = (acc[c] * sSF[c0 + c]) * sx;
           const double y1 = (acc[c + 1] * sSF[c0 + c + 1]) * sx;
-          const uint32_t wide2 = (colmask >> c) & 3u;  // outputs of wide factor rows are stored below
-          if (vec && f + 1 < a.Nf && !wide2) {  // contiguous factor index (mode 1): one 16-byte store per pair
+          if (vec && f + 1 < a.Nf) {  // contiguous factor index (mode 1): one 16-byte store per pair
             *reinterpret_cast<double2*>(a.y + row_off + f) = make_double2(y0, y1);
           } else {
-            if (f < a.Nf && !(wide2 & 1u)) a.y[row_off + f * a.fstride] = y0;
-            if (f + 1 < a.Nf && !(wide2 & 2u)) a.y[row_off + (f + 1) * a.fstride] = y1;
+            if (f < a.Nf) a.y[row_off + f * a.fstride] = y0;
+            if (f + 1 < a.Nf) a.y[row_off + (f + 1) * a.fstride] = y1;
           }
         }
       }
-      if (rowmask | colmask) oz_wide_outputs(a, row0, n0 + c0, rowmask, colmask, lane);
     }
+    oz_cta_fixup(a, a.xw, a.fw, mt_first, per_nt, n0, sFix, sFix + OZ_MAXKP);
   }
   tc_fence_before();
   __syncthreads();
@@ -672,7 +722,7 @@ int get_encode(EncodeTiledFn* fn) {
 constexpr size_t oz_smem_bytes(int KC) {
   return 1024 + (size_t)OZ_S * (KC > 2 ? 2 : KC) * OZ_FBYTES + (size_t)OZ_STAGES * OZ_XBYTES +
          (2 * OZ_STAGES + 4 + 2 * OZ_NW + 2) * 8 +
-         OZ_BN * sizeof(double);
+         (OZ_BN + OZ_MAXKP + 8 * 32) * sizeof(double);
 }
 
 // cudaFuncSetAttribute is per device: one flag bit per device ordinal
@@ -696,6 +746,7 @@ int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows) {
   }
   if (op.digits && op.rows_p == rows_p && op.kp == kp && op.box_rows == box_rows) {
     op.rows = rows;
+    FDIGA_CUDA(cudaMemset(op.wide, 0, 2 * sizeof(int32_t)));
     return FDIGA_OK;
   }
   op.release();
@@ -703,6 +754,8 @@ int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows) {
   FDIGA_CUDA(cudaMemset(op.digits, 0, (size_t)OZ_S * rows_p * kp));
   FDIGA_CUDA(cudaMalloc(&op.exps, (size_t)rows_p * sizeof(int32_t)));
   FDIGA_CUDA(cudaMemset(op.exps, 0, (size_t)rows_p * sizeof(int32_t)));
+  FDIGA_CUDA(cudaMalloc(&op.wide, (size_t)(rows_p + 2) * sizeof(int32_t)));
+  FDIGA_CUDA(cudaMemset(op.wide, 0, 2 * sizeof(int32_t)));
   op.rows = rows;
   op.rows_p = rows_p;
   op.kp = kp;
@@ -721,6 +774,17 @@ int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows) {
   return FDIGA_OK;
 }
 
+int oz_operand_set_ft(OzOperand& op, const double* F_host, int64_t n) {
+  std::vector<double> t((size_t)(n * n));
+  for (int64_t f = 0; f < n; ++f)
+    for (int64_t k = 0; k < n; ++k) t[(size_t)(k * n + f)] = F_host[f * n + k];
+  if (op.ft) cudaFree(op.ft);
+  op.ft = nullptr;
+  FDIGA_CUDA(cudaMalloc(&op.ft, t.size() * sizeof(double)));
+  FDIGA_CUDA(cudaMemcpy(op.ft, t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return FDIGA_OK;
+}
+
 int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch, int64_t K, int64_t inner,
              int64_t ldx, OzOperand& op, const int* skip, const double* lam_row, const double* lam_k) {
 
@@ -730,9 +794,11 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
   if (inner == 1 && !lam_row) {  // (the divide is done by the strided kernel, which handles inner == 1 too)
     const unsigned grid = (unsigned)((rows + 7) / 8);
     if (op.kp <= 256)
-      oz_split_rows_kernel<1><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.rows_p, (int)op.kp, skip);
+      oz_split_rows_kernel<1><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.wide, op.rows_p,
+                                                        (int)op.kp, skip);
     else
-      oz_split_rows_kernel<2><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.rows_p, (int)op.kp, skip);
+      oz_split_rows_kernel<2><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.wide, op.rows_p,
+                                                        (int)op.kp, skip);
   } else {
     static std::atomic<uint64_t> attr{0};
     if (attr_once(attr, ctx->device))
@@ -741,7 +807,7 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
     // beats 32 columns (three blocks per SM: 1.351 vs 1.336 ms per apply) and 8 (64-byte row segments: 1.368)
     const int64_t tiles = batch * ((inner + 15) / 16);
     oz_split_cols_kernel<16><<<(unsigned)tiles, 256, (size_t)K * 16 * sizeof(double), stream>>>(
-        x, batch, (int)K, inner, op.digits, op.exps, op.rows_p, (int)op.kp, lam_row, lam_k, skip);
+        x, batch, (int)K, inner, op.digits, op.exps, op.wide, op.rows_p, (int)op.kp, lam_row, lam_k, skip);
   }
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());
@@ -782,8 +848,11 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   a.lam_k = g.lam_k;
   a.fs = g.fs;
   a.ldf = g.ldf;
+  a.ft = F.ft;
+  a.xw = X.wide;
+  a.fw = F.wide;
   a.skip = g.skip;
-  FDIGA_CHECK(g.xs && g.fs, FDIGA_ERR_INVALID_ARG, "oz_gemm: FP64 operands for the wide-row fallback missing");
+  FDIGA_CHECK(g.xs && g.fs && F.ft, FDIGA_ERR_INVALID_ARG, "oz_gemm: FP64 operands for the wide-row fallback missing");
   FDIGA_CHECK(a.nt <= ctx->sm_count, FDIGA_ERR_NOT_SUPPORTED, "oz_gemm: too many column tiles");
   const size_t smem = oz_smem_bytes(a.KC);
   static std::atomic<uint64_t> attr{0};

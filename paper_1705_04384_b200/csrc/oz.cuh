@@ -24,9 +24,13 @@ constexpr int OZ_MAXKP = 512;  // contraction lengths up to 512 (factor digits r
 // Guard ("accuracy contract"): a row (data fibre or factor row) is "wide" when it holds a
 // non-finite value, a nonzero |x| < 2^(e - OZ_SPREAD) (its digits would keep fewer than 55 - OZ_SPREAD = 31
 // significant bits of that value), or its exponent is below OZ_EMIN (the digit scaling 2^(55 - e) would leave
-// the double range).  The split marks it by adding OZ_WIDE to the stored exponent; the GEMM epilogue computes
-// every output of a wide data row or a wide factor row as an IEEE FP64 dot product from the FP64 operands.
-constexpr int OZ_SPREAD = 24;
+// the double range).  The split marks it by adding OZ_WIDE to the stored exponent and appends the row to the
+// operand's wide list; after its last tile, every GEMM CTA recomputes its outputs of wide data rows and wide
+// factor rows as IEEE FP64 dot products of the FP64 operands (over the int8 results).
+#ifndef FDIGA_OZ_SPREAD
+#define FDIGA_OZ_SPREAD 24
+#endif
+constexpr int OZ_SPREAD = FDIGA_OZ_SPREAD;
 constexpr int OZ_EMIN = -900;
 constexpr int OZ_WIDE = 1 << 20;
 
@@ -40,10 +44,13 @@ constexpr int oz_pairs() {
 
 // Split operand: S digit planes [S][rows_p][kp] (int8, k contiguous, zero padded) and the row
 // exponents e[rows_p] (+ OZ_WIDE for a wide row); the tensor map views the planes as a 2D [S rows_p] x [kp]
-// int8 matrix.
+// int8 matrix.  wide: [0] count, [1] ticket (the GEMM's last-CTA reset), [2 ..] the wide rows (at most
+// rows_p), appended by the split in no particular order.
 struct OzOperand {
   int8_t* digits = nullptr;
   int32_t* exps = nullptr;
+  int32_t* wide = nullptr;
+  double* ft = nullptr;  // factor operands: the FP64 factor transposed, [k][row] (oz_fixup's coalesced reads)
   int64_t rows = 0, rows_p = 0, kp = 0;
   int box_rows = 0;
   alignas(64) unsigned char tmap[128];  // CUtensorMap
@@ -52,6 +59,8 @@ struct OzOperand {
 
 // Allocate (or grow) an operand for `rows` rows of k values; box_rows = OZ_BM (data) or OZ_BN (factor).
 int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows);
+// Factor operands: keep F^T ([k][row], n x n) for the fixup; F row-major n x n on the host.
+int oz_operand_set_ft(OzOperand& op, const double* F_host, int64_t n);
 // Split x (element (b, k, i) at x[b K inner + k inner + i]; for inner == 1 row b at x[b ldx]) into op,
 // row m = b inner + i, on `stream`.
 // lam_row / lam_k (may be NULL): divide element (b, k, i) by lam_row[b inner + i] + lam_k[k]
@@ -79,6 +88,8 @@ struct OzGemmArgs {
   int64_t ldf;
   const int* skip;
 };
+// oz_gemm: the int8 GEMM, including the outputs of wide data rows (X's list, reset afterwards for the next
+// split) and of wide factor rows (F's list, kept: the factor is split once at setup).
 int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& a);
 
 }  // namespace fdiga
