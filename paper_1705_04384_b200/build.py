@@ -7,8 +7,9 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-CSRC = os.path.join(PKG, "csrc")
-LIBDIR = os.path.join(PKG, "lib")
+# FDIGA_CSRC / FDIGA_LIBDIR: experiment builds of a copied source tree into another directory
+CSRC = os.environ.get("FDIGA_CSRC") or os.path.join(PKG, "csrc")
+LIBDIR = os.environ.get("FDIGA_LIBDIR") or os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libfdiga.so")
 SOURCES = ["ctx.cu", "comm.cu", "fd_gemm.cu", "fd.cu", "stencil.cu", "krylov.cu", "bicgstab.cu", "matfree.cu", "wq.cu", "oz.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -47,7 +48,7 @@ def build(force=False, verbose=False):
     nvcc = nvcc_path()
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
                      "-I", nccl_include()]
-    build_dir = os.path.join(PKG, "build")
+    build_dir = os.path.join(LIBDIR, "build") if os.environ.get("FDIGA_LIBDIR") else os.path.join(PKG, "build")
     os.makedirs(build_dir, exist_ok=True)
     cmds = []
     for src in SOURCES:

@@ -357,8 +357,8 @@ int oz_setup(fd_plan* P, bool force = false) {
   cudaStream_t st = P->ctx->stream;
   const OzShapes sh = oz_shapes(P);
   for (int l = 0; l < 3; ++l) {
-    FDIGA_TRY(oz_operand_alloc(P->ozW[l], P->n[l], P->n[l], OZ_BN));
-    FDIGA_TRY(oz_operand_alloc(P->ozU[l], P->n[l], P->n[l], OZ_BN));
+    FDIGA_TRY(oz_operand_alloc(P->ozW[l], P->n[l], P->n[l], OZ_BNH));
+    FDIGA_TRY(oz_operand_alloc(P->ozU[l], P->n[l], P->n[l], OZ_BNH));
     FDIGA_TRY(oz_split(P->ctx, st, P->W[l], P->n[l], P->n[l], 1, P->ld[l], P->ozW[l], nullptr));
     FDIGA_TRY(oz_split(P->ctx, st, P->U[l], P->n[l], P->n[l], 1, P->ld[l], P->ozU[l], nullptr));
     FDIGA_TRY(oz_operand_set_ft(P->ozW[l], P->hW[l].data(), P->n[l]));

@@ -262,16 +262,33 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
 }
 
 // ---------------------------------------------------------------------------------------------
-// tcgen05 GEMM
+// tcgen05 GEMM (CTA pairs, cta_group::2)
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const void* map, int x, int y, uint64_t* bar) {
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// shared::cluster address of `p`'s counterpart in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// remote arrive (CTA-scope release: the arriving warp's tcgen05.ld are complete, and it orders no global
+// stores for the peer -- a cluster-scope release would wait for the warp's outstanding y stores)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster) : "memory");
+}
+// pair TMA: the bytes land in this CTA's shared memory, completion is signalled on the leader's mbarrier
+__device__ __forceinline__ void tma_load_2sm(void* dst, const void* map, int x, int y, uint32_t bar_leader) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_leader)
       : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -281,23 +298,12 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-// Issued by a whole, converged warp with warp-uniform operands: one elected lane executes the MMA.  (Issuing
-// from a single-lane branch made the compiler wrap every MMA in an ELECT / R2UR.BROADCAST loop to build its
-// uniform-register operands: ~13 instructions and 43 ns per N = 64 MMA instead of ~26 ns.)
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  // the two descriptors share their high words (SBO, version, swizzle); only the low words (start address,
-  // LBO) differ, and offsets added to them never carry (shared addresses < 2^18): 32-bit operands
-  const uint32_t alo = (uint32_t)da, blo = (uint32_t)db, hi = (uint32_t)(da >> 32);
+// single-thread MMA of the pair (issued by the leader CTA inside a warp-converged `if (elect_one())` around a
+// whole stage): D (128 lanes x N columns in each CTA's TMEM) += A (128 rows from each CTA) B^T (N / 2 rows
+// from each CTA), both operands at the same shared-memory offsets in the two CTAs
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n .reg .pred p, e;\n .reg .b64 a, b;\n elect.sync _|e, 0xffffffff;\n mov.b64 a, {%1, %3};\n"
-      " mov.b64 b, {%2, %3};\n setp.ne.b32 p, %5, 0;\n"
-      " @e tcgen05.mma.cta_group::1.kind::i8 [%0], a, b, %4, p;\n}\n" ::"r"(tmem_d),
-      "r"(alo), "r"(blo), "r"(hi), "r"(idesc), "r"(acc));
-}
-// single-thread variant, for use inside a warp-converged `if (elect_one())` around a whole stage
-__device__ __forceinline__ void mma_i8_1(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
           tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
@@ -306,37 +312,36 @@ __device__ __forceinline__ bool elect_one() {
   asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(e));
   return e != 0;
 }
-__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+// arrive on the mbarrier at `bar`'s offset in both CTAs of the pair once the MMAs issued so far complete
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
   asm volatile(
       "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
-      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
       : "memory");
 }
 
-// instruction descriptor: D s32, A / B s8 (signed digit 0) or u8, K-major, N = 64, M = 128
+// instruction descriptor: D s32, A / B s8 (signed digit 0) or u8, K-major, N = 128, M = 256 (the pair)
 __host__ __device__ constexpr uint32_t oz_idesc(bool a_signed, bool b_signed) {
   return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
-         ((uint32_t)(OZ_BM >> 4) << 24);
+         ((uint32_t)(OZ_PM >> 4) << 24);
 }
-template <int I, int NKS>
-__device__ __forceinline__ void oz_stage_mmas(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
-                                              bool first_kc);
-template <int I>
-__device__ __noinline__ void oz_stage_mmas_rt(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
-                                              bool first_kc, int nks);
-constexpr int OZ_STAGES = 6;
-constexpr int OZ_EW = 8;                    // epilogue warps: 4 lane quarters x 2 column halves
-constexpr int OZ_EC = OZ_BN / (OZ_EW / 4);  // columns per epilogue thread
+constexpr int OZ_NSLOT = 4;                 // TMEM accumulator slots of OZ_BN columns (4 x 128 = 512)
+constexpr int OZ_EW = 16;                   // epilogue warps: 4 lane quarters x 4 column groups of 32
+constexpr int OZ_EC = 32;                   // columns per epilogue thread
 constexpr int OZ_THREADS = (OZ_EW + 2) * 32;  // + TMA producer warp + MMA warp
-constexpr int OZ_XBYTES = OZ_BM * OZ_BK;  // one data digit plane chunk: 128 rows x 128 B
-constexpr int OZ_FBYTES = OZ_BN * OZ_BK;  // one factor digit plane chunk: 64 rows x 128 B
+constexpr int OZ_XBYTES = OZ_BM * OZ_BK;    // one data digit plane chunk per CTA: 128 rows x 128 B
+constexpr int OZ_FBYTES = OZ_BNH * OZ_BK;   // one factor digit plane chunk per CTA: 64 rows x 128 B
+constexpr int OZ_NST = 6;                   // data ring stages
+static_assert(OZ_EC * (OZ_EW / 4) == OZ_BN, "epilogue column groups cover the tile");
 
 struct OzKernelArgs {
   int64_t M, Nf;     // data rows, factor rows
   int64_t x_rows_p, f_rows_p;
   int KC;            // 128-wide k chunks
   int ks_last;       // K-steps of 32 in the last chunk that reach below the contraction length (1..4)
-  int mt, nt;        // tiles along M and Nf
+  int mt, nt;        // pair tiles along M (256 rows) and Nf (128 rows)
   int K;             // contraction length
   const int32_t* ex;
   const int32_t* ef;
@@ -364,316 +369,341 @@ __device__ __forceinline__ double oz_x(const OzKernelArgs& a, const double* xr, 
   const double xv = xr[k * a.xs_k];
   return a.lam_row ? xv / (lr + a.lam_k[k]) : xv;
 }
+
 // The guard's fallback (oz.cuh), run by the epilogue warps of every GEMM CTA after its last tile: the outputs
-// of the CTA's tiles (its row tiles x its column tile) that belong to a wide data row (X's list) or a wide
-// factor row (F's list) are recomputed as IEEE FP64 dot products of the FP64 operands and stored over the
-// int8 results (each output has one owner CTA, so no grid-wide ordering is needed).  Items of 32 outputs:
-// the item's shared operand row (K values) is staged in shared memory; thread (c, s) of the 8 epilogue warps
-// sums k = s, s + 8, .. for output c (loads of F^T / of the data coalesced over c, 16 in flight), and the 8
-// partial sums per output are added in a fixed order.  The last CTA to finish resets X's list for the next
-// split.  No wide row: two loads and one atomic per CTA.
-__device__ __forceinline__ void oz_bar_epi() { asm volatile("bar.sync 1, %0;\n" ::"n"(256) : "memory"); }
+// of the CTA's 128-row halves of its pair tiles (x the pair's factor rows) that belong to a wide data row
+// (X's list) or a wide factor row (F's list) are recomputed as IEEE FP64 dot products of the FP64 operands and
+// stored over the int8 results (each output has one owner CTA, so no grid-wide ordering is needed).  Items of
+// 32 outputs: the item's shared operand row (K values) is staged in shared memory; thread (c, s) of the
+// OZ_EW epilogue warps sums k = s, s + OZ_EW, .. for output c (loads of F^T / of the data coalesced over c),
+// and the partial sums per output are added in a fixed order.  The last CTA to finish resets X's list for the
+// next split.  No wide row: two loads and one atomic per CTA.
+__device__ __forceinline__ void oz_bar_epi() { asm volatile("bar.sync 1, %0;\n" ::"n"(OZ_EW * 32) : "memory"); }
 __device__ __forceinline__ void oz_fix_item(const OzKernelArgs& a, int64_t m, int64_t f, bool wide_row, double* sv,
                                             double* part, int c, int sl) {
   // sv holds the item's shared row; this thread's output is (m, f)
   double acc = 0.0;
   if (wide_row) {
     const int64_t fc = min(f, a.Nf - 1);
-#pragma unroll 16
-    for (int k = sl; k < a.K; k += 8) acc = fma(a.ft[k * a.Nf + fc], sv[k], acc);
+#pragma unroll 8
+    for (int k = sl; k < a.K; k += OZ_EW) acc = fma(a.ft[k * a.Nf + fc], sv[k], acc);
   } else {
     const int64_t mc = min(m, a.M - 1);
     const double* xr = a.xs + (mc / a.inner) * a.xs_b + (mc % a.inner) * a.xs_i;
     const double lr = a.lam_row ? a.lam_row[mc] : 0.0;
-#pragma unroll 16
-    for (int k = sl; k < a.K; k += 8) acc = fma(sv[k], oz_x(a, xr, lr, k), acc);
+#pragma unroll 8
+    for (int k = sl; k < a.K; k += OZ_EW) acc = fma(sv[k], oz_x(a, xr, lr, k), acc);
   }
   part[sl * 32 + c] = acc;
   oz_bar_epi();
   if (sl == 0 && m < a.M && f < a.Nf) {
     double t = part[c];
 #pragma unroll
-    for (int q = 1; q < 8; ++q) t += part[q * 32 + c];
+    for (int q = 1; q < OZ_EW; ++q) t += part[q * 32 + c];
     a.y[oz_out_off(a, m) + f * a.fstride] = t;
   }
   oz_bar_epi();
 }
-// mt_first / per_nt: the CTA's row tiles; [n0, n0 + BN) its factor rows.  Called by the 256 epilogue threads.
-__device__ void oz_cta_fixup(const OzKernelArgs& a, int32_t* xw, const int32_t* fw, int mt_first, int per_nt,
-                             int n0, double* sv, double* part) {
+// The CTA's rows: [mt OZ_PM + rank OZ_BM, + OZ_BM) for mt = mt_first, mt_first + per_nt, ..; its factor rows
+// [n0, n0 + OZ_BN).  Called by the OZ_EW epilogue warps.
+__device__ void oz_cta_fixup(const OzKernelArgs& a, int mt_first, int per_nt, uint32_t rank, int n0, double* sv,
+                             double* part) {
   const int c = threadIdx.x & 31, sl = threadIdx.x >> 5;
-  const int nx = *(volatile int32_t*)xw, nf = *(volatile const int32_t*)fw;
+  const int nx = *(volatile int32_t*)a.xw, nf = *(volatile const int32_t*)a.fw;
   for (int i = 0; i < nx; ++i) {
-    const int64_t m = xw[2 + i];
-    const int mt = (int)(m / OZ_BM);
-    if (mt < mt_first || (mt - mt_first) % per_nt) continue;
+    const int64_t m = a.xw[2 + i];
+    const int mt = (int)(m / OZ_PM);
+    if (mt < mt_first || (mt - mt_first) % per_nt || (uint32_t)((m % OZ_PM) / OZ_BM) != rank) continue;
     const double* xr = a.xs + (m / a.inner) * a.xs_b + (m % a.inner) * a.xs_i;
     const double lr = a.lam_row ? a.lam_row[m] : 0.0;
-    for (int k = threadIdx.x; k < a.K; k += 256) sv[k] = oz_x(a, xr, lr, k);
+    for (int k = threadIdx.x; k < a.K; k += OZ_EW * 32) sv[k] = oz_x(a, xr, lr, k);
     oz_bar_epi();
     for (int h = 0; h < OZ_BN; h += 32) oz_fix_item(a, m, n0 + h + c, true, sv, part, c, sl);
   }
   for (int i = 0; i < nf; ++i) {
-    const int64_t f = fw[2 + i];
+    const int64_t f = a.fw[2 + i];
     if (f < n0 || f >= n0 + OZ_BN) continue;
-    for (int k = threadIdx.x; k < a.K; k += 256) sv[k] = a.fs[f * a.ldf + k];
+    for (int k = threadIdx.x; k < a.K; k += OZ_EW * 32) sv[k] = a.fs[f * a.ldf + k];
     oz_bar_epi();
     for (int mt = mt_first; mt < a.mt; mt += per_nt)
-      for (int r = 0; r < OZ_BM; r += 32) oz_fix_item(a, (int64_t)mt * OZ_BM + r + c, f, false, sv, part, c, sl);
+      for (int r = 0; r < OZ_BM; r += 32)
+        oz_fix_item(a, (int64_t)mt * OZ_PM + rank * OZ_BM + r + c, f, false, sv, part, c, sl);
   }
   // reset X's list once every CTA has read its count
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(&xw[1], 1) == (int)gridDim.x - 1) {
-      xw[0] = 0;
-      xw[1] = 0;
+    if (atomicAdd(&a.xw[1], 1) == (int)gridDim.x - 1) {
+      a.xw[0] = 0;
+      a.xw[1] = 0;
     }
   }
 }
 
+// Two passes per tile over the contraction: pass 0 accumulates the weights t = 0..3 (10 digit pairs, data and
+// factor digits 0..3), pass 1 the weights 4..7 (24 pairs, digits 0..6), four int32 accumulators of 128 columns
+// each (all 512 TMEM columns).  Phase q = 2 tile + pass.  Within a phase the first k chunk takes the data
+// digits in descending order and later chunks ascending, so the weights are first written in the order
+// 3, 2, 1, 0 (pass 0) / {6, 7}, 5, 4 (pass 1) and complete in the order 0, 1, 2, 3 / 4, 5, {6, 7}.  The
+// epilogue drains every phase in ascending weight order.  The slot of a weight is chosen so that the next
+// phase first writes its slots in exactly the order the epilogue drains them (the assignment repeats every
+// two tiles):
+//   q % 4 = 0: w0..w3 -> slots 3 2 1 0     q % 4 = 1: w4..w7 -> 0 1 3 2
+//   q % 4 = 2: w0..w3 -> slots 2 3 1 0     q % 4 = 3: w4..w7 -> 0 1 2 3
+__host__ __device__ constexpr int oz_slot(int q4, int t) {
+  // the table above, 2 bits per entry, entry (q4, t) at bit 2 (4 q4 + t)
+  constexpr uint32_t T = (3u << 0) | (2u << 2) | (1u << 4) | (0u << 6) | (0u << 8) | (1u << 10) | (3u << 12) |
+                         (2u << 14) | (2u << 16) | (3u << 18) | (1u << 20) | (0u << 22) | (0u << 24) | (1u << 26) |
+                         (2u << 28) | (3u << 30);
+  return (int)((T >> (2 * (4 * q4 + (t & 3)))) & 3u);
+}
+// digit pairs (I, j) of pass P: i + j in [4P, 4P + 3], i, j <= 6
+__host__ __device__ constexpr int oz_jlo(int P, int I) { return P == 0 ? 0 : (4 - I > 0 ? 4 - I : 0); }
+__host__ __device__ constexpr int oz_jhi(int P, int I) { return P == 0 ? 3 - I : (7 - I < 6 ? 7 - I : 6); }
+// does stage I of the first chunk write weight I + j first (descending digit order)?
+__host__ __device__ constexpr bool oz_first_touch(int P, int I, int j) {
+  return P == 0 ? j == 0 : ((I == 6 && j <= 1) || ((I == 5 || I == 4) && j == 0));
+}
 
-// Accumulator hand-off between tiles.  Weight t (digit pairs i + j = t) of tile T lives in TMEM slot
-// p(t, T) = t (T even) or NW - 1 - t (T odd).  The first k chunk of a tile takes the data digits in
-// descending order (digit i first touches weight i), later chunks ascending, so in the last chunk weight t
-// completes right after digit t.  The epilogue drains weights in ascending order, i.e. slots in the order
-// 0, 1, .., NW - 1 for either parity, which is exactly the order in which the next tile first writes them:
-// the epilogue of tile T runs under the MMAs of tile T + 1.
-__device__ __forceinline__ int oz_slot(int t, uint32_t tile) { return (tile & 1) ? OZ_NW - 1 - t : t; }
-
-// the MMAs of data digit I: pairs (I, j), j = 0..min(S - 1, NW - 1 - I), into weight I + j; 4 K-steps of 32.
+// the MMAs of data digit I in pass P: pairs (I, j) into weight I + j, NKS K-steps of 32 (k step outer, pair
+// inner: consecutive MMAs share the A operand).  so[w & 3]: the TMEM column of weight w's slot in this phase.
 // db_kc: descriptor of factor digit 0 of this k chunk (digit j is j chunks further).  Digit 0 is signed, the
-// others unsigned: the instruction descriptor is chosen per pair.  In the first k chunk (descending digits)
-// pair (I, 0) is the first write of weight I, and for the first digit (S - 1) also pair (I, 1) of weight
-// I + 1 = NW - 1: those MMAs overwrite their slot.
-template <int I, int NKS>
-__device__ __forceinline__ void oz_stage_mmas(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
-                                              bool first_kc) {
-  const uint32_t odd = tile & 1;
-  // k step outer, digit pair inner: consecutive MMAs share the A (data) operand.  NKS K-steps of 32: fewer
-  // than 4 in a last chunk that holds only padding zeros past the contraction length.  One elected lane
-  // issues the whole stage (operands computed by the converged warp before the branch).
+// others unsigned: the instruction descriptor is chosen per pair.  One elected lane issues the whole stage.
+template <int P, int I>
+__device__ __forceinline__ void oz_stage_mmas(const uint32_t (&so)[4], uint64_t da, uint64_t db_kc, bool first_kc,
+                                              int nks) {
   if (elect_one()) {
+    if (nks == OZ_BK / 32) {
 #pragma unroll
-    for (int kk = 0; kk < NKS; ++kk)
+      for (int kk = 0; kk < OZ_BK / 32; ++kk)
 #pragma unroll
-      for (int j = 0; j < OZ_S && I + j < OZ_NW; ++j) {
-        const uint32_t td = tbase + (uint32_t)((odd ? OZ_NW - 1 - (I + j) : (I + j)) * OZ_BN);
-        const bool first_touch = first_kc && (j == 0 || I == OZ_S - 1);
-        mma_i8_1(td, da + 2 * kk, db_kc + (uint64_t)(j * (OZ_BN * OZ_BK >> 4) + 2 * kk), oz_idesc(I == 0, j == 0),
-                 (kk != 0 || !first_touch) ? 1u : 0u);
-      }
+        for (int j = oz_jlo(P, I); j <= oz_jhi(P, I); ++j)
+          mma_i8_pair(so[(I + j) & 3], da + 2 * kk, db_kc + (uint64_t)(j * (OZ_FBYTES >> 4) + 2 * kk),
+                      oz_idesc(I == 0, j == 0), (kk != 0 || !(first_kc && oz_first_touch(P, I, j))) ? 1u : 0u);
+    } else {  // short last chunk: only the K-steps that reach below the contraction length
+#pragma unroll 1
+      for (int kk = 0; kk < nks; ++kk)
+#pragma unroll
+        for (int j = oz_jlo(P, I); j <= oz_jhi(P, I); ++j)
+          mma_i8_pair(so[(I + j) & 3], da + 2 * kk, db_kc + (uint64_t)(j * (OZ_FBYTES >> 4) + 2 * kk),
+                      oz_idesc(I == 0, j == 0), (kk != 0 || !(first_kc && oz_first_touch(P, I, j))) ? 1u : 0u);
+    }
   }
   __syncwarp();
 }
 
-template <int I>
-__device__ __noinline__ void oz_stage_mmas_rt(uint32_t tbase, uint32_t tile, uint64_t da, uint64_t db_kc,
-                                              bool first_kc, int nks) {
-  const uint32_t odd = tile & 1;
-#pragma unroll 1
-  for (int kk = 0; kk < nks; ++kk)
-#pragma unroll
-    for (int j = 0; j < OZ_S && I + j < OZ_NW; ++j) {
-      const uint32_t td = tbase + (uint32_t)((odd ? OZ_NW - 1 - (I + j) : (I + j)) * OZ_BN);
-      const bool first_touch = first_kc && (j == 0 || I == OZ_S - 1);
-      mma_i8(td, da + 2 * kk, db_kc + (uint64_t)(j * (OZ_BN * OZ_BK >> 4) + 2 * kk), oz_idesc(I == 0, j == 0),
-             (kk != 0 || !first_touch) ? 1u : 0u);
-    }
-}
-
-// STREAM = false: the CTA's factor digits for all k chunks stay resident (K <= 256).  STREAM = true (K up to
-// 512): one k chunk of the factor digits (7 x 8 KB) at a time, double-buffered, reloaded for every tile.
-template <bool STREAM>
-__global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_constant__ CUtensorMap xmap,
-                                                         const __grid_constant__ CUtensorMap fmap,
-                                                         const __grid_constant__ OzKernelArgs a) {
+// One CTA pair (cluster of 2, the SMs of a TPC) per pair tile: 256 data rows (128 per CTA = the TMEM lanes of
+// each CTA) x 128 factor rows (64 per CTA), four accumulator slots of 128 columns in each CTA's TMEM.  The
+// leader (rank 0) issues every MMA (M = 256, N = 128, K = 32); both CTAs stream their own data rows and their
+// half of the factor rows (one k chunk of factor digits at a time, double-buffered) by TMA, completion
+// counted on the leader's barriers, and drain their own accumulators.
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap fmap,
+                   const __grid_constant__ OzKernelArgs a) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  if (a.skip && *a.skip) return;
+  if (a.skip && *a.skip) return;  // (both CTAs of a pair read the same flag)
   extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
   const int KC = a.KC;
-  uint8_t* sF = smem;  // [KC][S] factor chunks (resident) or [2][S] (streamed)
-  uint8_t* sX = smem + OZ_S * (STREAM ? 2 : KC) * OZ_FBYTES;  // data ring
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_STAGES * OZ_XBYTES);
-  uint64_t* empty = full + OZ_STAGES;
-  uint64_t* fbar = empty + OZ_STAGES;  // resident: [1] factor landed; streamed: [2] full + [2] empty
-  uint64_t* sfull = fbar + 4;      // [NW] accumulator slot complete (MMA -> epilogue)
-  uint64_t* sempty = sfull + OZ_NW;  // [NW] accumulator slot drained (epilogue -> MMA)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_NW);
-  double* sSF = reinterpret_cast<double*>(sempty + OZ_NW + 2);  // 2^(e_f - WSHIFT) of the CTA's factor rows
-  double* sFix = sSF + OZ_BN;                                   // fixup: [OZ_MAXKP] row + [8][32] partial sums
+  uint8_t* sF = smem;                                  // [2][S] factor chunks of this CTA's 64 rows
+  uint8_t* sX = smem + 2 * OZ_S * OZ_FBYTES;           // data ring [NST]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_NST * OZ_XBYTES);  // [NST] (leader: both CTAs' bytes)
+  uint64_t* empty = full + OZ_NST;                                        // [NST] (each CTA, multicast commit)
+  uint64_t* ffull = empty + OZ_NST;   // [2] factor chunk landed (leader)
+  uint64_t* fempty = ffull + 2;       // [2] factor chunk consumed (each CTA)
+  uint64_t* sfull = fempty + 2;       // [4] accumulator slot complete (MMA -> epilogues of both CTAs)
+  uint64_t* sempty = sfull + OZ_NSLOT;  // [4] accumulator slot drained by both CTAs (leader)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_NSLOT);
+  double* sSF = reinterpret_cast<double*>(sempty + OZ_NSLOT + 2);  // 2^(e_f - WSHIFT) of the pair's factor rows
+  double* sFix = sSF + OZ_BN;  // fixup: [OZ_MAXKP] row + [OZ_EW][32] partial sums
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < OZ_STAGES; ++s) {
+    for (int s = 0; s < OZ_NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int f = 0; f < 4; ++f) mbar_init(&fbar[f], 1);
-    for (int t = 0; t < OZ_NW; ++t) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&ffull[s], 1);
+      mbar_init(&fempty[s], 1);
+    }
+    for (int t = 0; t < OZ_NSLOT; ++t) {
       mbar_init(&sfull[t], 1);
-      mbar_init(&sempty[t], OZ_EW);
+      mbar_init(&sempty[t], 2 * OZ_EW);
     }
     fence_barrier_init();
   }
-  if (warp == OZ_EW + 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tslot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  if (warp == OZ_EW + 1) {  // the same warp in both CTAs allocates the pair's TMEM
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
-  // tile sequence of this CTA: column tile nt0 fixed, row tiles strided
-  const int per_nt = gridDim.x / a.nt;
-  const int nt0 = blockIdx.x % a.nt;
-  const int mt_first = blockIdx.x / a.nt;
+  // tile sequence of this pair: column tile nt0 fixed, row tiles strided
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int per_nt = npairs / a.nt;
+  const int nt0 = pair % a.nt;
+  const int mt_first = pair / a.nt;
   const int n0 = nt0 * OZ_BN;
 
   if (warp == OZ_EW) {
     if (lane == 0) {
-      if (!STREAM) {  // resident factor digit planes of this column tile, [kc][digit] chunks
-        mbar_arrive_expect_tx(fbar, (uint32_t)(OZ_S * KC * OZ_FBYTES));
-        for (int s = 0; s < OZ_S; ++s)
-          for (int kc = 0; kc < KC; ++kc)
-            tma_load_2d(sF + (kc * OZ_S + s) * OZ_FBYTES, &fmap, kc * OZ_BK, (int)(s * a.f_rows_p + n0), fbar);
-      }
       uint32_t st = 0, ph = 0, fc = 0;
       bool wrapped = false;
       for (int mt = mt_first; mt < a.mt; mt += per_nt) {
-        const int m0 = mt * OZ_BM;
-        for (int kc = 0; kc < KC; ++kc) {
-          if (STREAM) {  // this k chunk's factor digits into factor slot fc % 2
-            const uint32_t fs = fc & 1;
-            if (fc >= 2) mbar_wait(&fbar[2 + fs], ((fc >> 1) - 1) & 1);
-            mbar_arrive_expect_tx(&fbar[fs], (uint32_t)(OZ_S * OZ_FBYTES));
-            for (int s = 0; s < OZ_S; ++s)
-              tma_load_2d(sF + (fs * OZ_S + s) * OZ_FBYTES, &fmap, kc * OZ_BK, (int)(s * a.f_rows_p + n0), &fbar[fs]);
-            ++fc;
-          }
-          for (int pos = 0; pos < OZ_S; ++pos) {
-            const int i = kc == 0 ? OZ_S - 1 - pos : pos;  // the MMA warp's digit order
-            if (wrapped) mbar_wait(&empty[st], ph ^ 1);
-            mbar_arrive_expect_tx(&full[st], OZ_XBYTES);
-            tma_load_2d(sX + st * OZ_XBYTES, &xmap, kc * OZ_BK, (int)(i * a.x_rows_p + m0), &full[st]);
-            if (++st == OZ_STAGES) {
-              st = 0;
-              ph ^= 1;
-              wrapped = true;
+        const int m0 = mt * OZ_PM + (int)rank * OZ_BM;
+        for (int pass = 0; pass < 2; ++pass) {
+          const int nd = pass == 0 ? 4 : OZ_S;  // digits of this pass (factor and data)
+          for (int kc = 0; kc < KC; ++kc) {
+            {  // this chunk's factor digits (this CTA's 64 rows) into factor slot fc % 2
+              const uint32_t fs = fc & 1;
+              if (fc >= 2) mbar_wait(&fempty[fs], ((fc >> 1) - 1) & 1);
+              if (leader) mbar_arrive_expect_tx(&ffull[fs], (uint32_t)(2 * nd * OZ_FBYTES));
+              const uint32_t bar = mapa(&ffull[fs], 0);
+              for (int s = 0; s < nd; ++s)
+                tma_load_2sm(sF + (fs * OZ_S + s) * OZ_FBYTES, &fmap, kc * OZ_BK,
+                             (int)(s * a.f_rows_p + n0 + rank * OZ_BNH), bar);
+              ++fc;
+            }
+            for (int pos = 0; pos < nd; ++pos) {
+              const int i = kc == 0 ? nd - 1 - pos : pos;  // the MMA warp's digit order
+              if (wrapped) mbar_wait(&empty[st], ph ^ 1);
+              if (leader) mbar_arrive_expect_tx(&full[st], 2 * OZ_XBYTES);
+              tma_load_2sm(sX + st * OZ_XBYTES, &xmap, kc * OZ_BK, (int)(i * a.x_rows_p + m0), mapa(&full[st], 0));
+              if (++st == OZ_NST) {
+                st = 0;
+                ph ^= 1;
+                wrapped = true;
+              }
             }
           }
         }
       }
     }
   } else if (warp == OZ_EW + 1) {
-    {  // the whole warp runs the issue loop (uniform operands); one elected lane issues
-      if (!STREAM) mbar_wait(fbar, 0);
-      tc_fence_after();
+    if (leader) {  // the whole warp runs the issue loop (uniform operands); one elected lane issues
       const uint64_t da0 = sdesc_sw128(smem_u32(sX)), db0 = sdesc_sw128(smem_u32(sF));
-      uint32_t st = 0, ph = 0, tl = 0, fc = 0;
-      for (int mt = mt_first; mt < a.mt; mt += per_nt, ++tl) {
-        for (int kc = 0; kc < KC; ++kc) {
-          uint64_t dbk = db0 + (uint64_t)(kc * OZ_S * (OZ_FBYTES >> 4));
-          if (STREAM) {
+      uint32_t st = 0, ph = 0, fc = 0, q = 0;
+      for (int mt = mt_first; mt < a.mt; mt += per_nt) {
+        for (int pass = 0; pass < 2; ++pass, ++q) {
+          uint32_t so[4];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) so[w] = tbase + (uint32_t)(oz_slot((int)(q & 3), w) * OZ_BN);
+          for (int kc = 0; kc < KC; ++kc) {
             const uint32_t fs = fc & 1;
-            mbar_wait(&fbar[fs], (fc >> 1) & 1);
+            mbar_wait(&ffull[fs], (fc >> 1) & 1);
             tc_fence_after();
-            dbk = db0 + (uint64_t)(fs * OZ_S * (OZ_FBYTES >> 4));
-          }
-          const bool first = kc == 0, last = kc == KC - 1;
-          const int nks = last ? a.ks_last : OZ_BK / 32;  // K-steps of 32 carrying real contraction indices
-          // one ring stage per data digit, its digit pairs fully unrolled (descriptor offsets are immediates)
-#define OZ_STAGE(I)                                                                                  \
-  {                                                                                                  \
-    mbar_wait(&full[st], ph);                                                                        \
-    tc_fence_after();                                                                                \
-    if (first && tl > 0) { /* weights first written by this stage: their slots must be drained */  \
-      if (I == OZ_S - 1) mbar_wait(&sempty[oz_slot(OZ_NW - 1, tl)], (tl - 1) & 1);                  \
-      mbar_wait(&sempty[oz_slot(I, tl)], (tl - 1) & 1);                                              \
-      tc_fence_after();                                                                              \
-    }                                                                                                \
-    {                                                                                                \
-      const uint64_t da_ = da0 + (uint64_t)(st * (OZ_XBYTES >> 4));                                  \
-      if (nks == OZ_BK / 32)                                                                         \
-        oz_stage_mmas<I, OZ_BK / 32>(tbase, tl, da_, dbk, first);                                    \
-      else /* short last chunk: a runtime K-step loop keeps the issue code small */                 \
-        oz_stage_mmas_rt<I>(tbase, tl, da_, dbk, first, nks);                                        \
-    }                                                                                                \
-    tc_commit_elect(&empty[st]); /* frees the ring slot when these MMAs have read it */                    \
-    if (last && !first) { /* ascending: weight I complete (and the last weight after the last digit) */ \
-      tc_commit_elect(&sfull[oz_slot(I, tl)]);                                                             \
-      if (I == OZ_S - 1) tc_commit_elect(&sfull[oz_slot(OZ_NW - 1, tl)]);                                  \
-    }                                                                                                \
-    if (++st == OZ_STAGES) {                                                                         \
-      st = 0;                                                                                        \
-      ph ^= 1;                                                                                       \
-    }                                                                                                \
+            const uint64_t dbk = db0 + (uint64_t)(fs * OZ_S * (OZ_FBYTES >> 4));
+            const bool first = kc == 0, last = kc == KC - 1;
+            const int nks = last ? a.ks_last : OZ_BK / 32;  // K-steps of 32 carrying real contraction indices
+#define OZ_WAIT_SLOT(w) mbar_wait(&sempty[oz_slot((int)(q & 3), (w))], (q - 1) & 1)
+#define OZ_STAGE(P, I)                                                                                 \
+  {                                                                                                    \
+    mbar_wait(&full[st], ph);                                                                          \
+    tc_fence_after();                                                                                  \
+    if (first && q > 0) { /* weights first written by this stage: their slots must be drained */      \
+      if (P == 0) OZ_WAIT_SLOT(I);                                                                     \
+      if (P == 1 && I >= 4) OZ_WAIT_SLOT(I);                                                           \
+      if (P == 1 && I == 6) OZ_WAIT_SLOT(7);                                                           \
+      tc_fence_after();                                                                                \
+    }                                                                                                  \
+    oz_stage_mmas<P, I>(so, da0 + (uint64_t)(st * (OZ_XBYTES >> 4)), dbk, first, nks);                 \
+    tc_commit_pair(&empty[st]); /* frees the ring slot in both CTAs when these MMAs have read it */     \
+    if (last && !first) { /* ascending: weights complete after their last digit */                     \
+      if (P == 0) tc_commit_pair(&sfull[oz_slot((int)(q & 3), I)]);                                    \
+      if (P == 1 && I >= 4) tc_commit_pair(&sfull[oz_slot((int)(q & 3), I)]);                          \
+      if (P == 1 && I == 6) tc_commit_pair(&sfull[oz_slot((int)(q & 3), 7)]);                          \
+    }                                                                                                  \
+    if (++st == OZ_NST) {                                                                              \
+      st = 0;                                                                                          \
+      ph ^= 1;                                                                                         \
+    }                                                                                                  \
   }
-          if (first) {
             static_assert(OZ_S == 7 && OZ_NW == 8, "stage sequences written for 7 digits, 8 weights");
-            OZ_STAGE(6) OZ_STAGE(5) OZ_STAGE(4) OZ_STAGE(3) OZ_STAGE(2) OZ_STAGE(1) OZ_STAGE(0)
-          } else {
-            OZ_STAGE(0) OZ_STAGE(1) OZ_STAGE(2) OZ_STAGE(3) OZ_STAGE(4) OZ_STAGE(5) OZ_STAGE(6)
-          }
+            if (pass == 0) {
+              if (first) {
+                OZ_STAGE(0, 3) OZ_STAGE(0, 2) OZ_STAGE(0, 1) OZ_STAGE(0, 0)
+              } else {
+                OZ_STAGE(0, 0) OZ_STAGE(0, 1) OZ_STAGE(0, 2) OZ_STAGE(0, 3)
+              }
+            } else {
+              if (first) {
+                OZ_STAGE(1, 6) OZ_STAGE(1, 5) OZ_STAGE(1, 4) OZ_STAGE(1, 3) OZ_STAGE(1, 2) OZ_STAGE(1, 1)
+                OZ_STAGE(1, 0)
+              } else {
+                OZ_STAGE(1, 0) OZ_STAGE(1, 1) OZ_STAGE(1, 2) OZ_STAGE(1, 3) OZ_STAGE(1, 4) OZ_STAGE(1, 5)
+                OZ_STAGE(1, 6)
+              }
+            }
 #undef OZ_STAGE
-          if (STREAM) {
-            tc_commit_elect(&fbar[2 + (fc & 1)]);  // the factor slot is free when this chunk's MMAs have read it
+#undef OZ_WAIT_SLOT
+            tc_commit_pair(&fempty[fs]);  // the factor slot is free when this chunk's MMAs have read it
             ++fc;
+            if (first && last)  // single k chunk (descending): every weight of the pass completes at its end
+              for (int w = 0; w < 4; ++w) tc_commit_pair(&sfull[oz_slot((int)(q & 3), w)]);
           }
-          if (first && last)  // single k chunk (descending): every weight completes at its end
-            for (int t = 0; t < OZ_NW; ++t) tc_commit_elect(&sfull[oz_slot(t, tl)]);
         }
       }
     }
   } else {
-    // epilogue: warp w owns TMEM lanes 32w..32w+31 = data rows m0 + 32w + lane
+    // epilogue (both CTAs): warp w owns TMEM lanes 32 (w % 4).. = this CTA's data rows, columns
+    // [32 (w / 4), +32) of every slot
     if (threadIdx.x < OZ_BN) {
       const int64_t f = n0 + threadIdx.x;
       sSF[threadIdx.x] = pow2(code_exp(f < a.Nf ? a.ef[f] : 0) - OZ_WSHIFT);
     }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(OZ_EW * 32) : "memory");  // epilogue warps only
-    uint32_t tl = 0;
-    // warp w: TMEM lanes 32 (w % 4).. (data rows), columns [32 (w / 4), +32) of every weight slot
+    oz_bar_epi();
+    uint32_t q = 0;
     const int quarter = warp & 3, c0 = (warp >> 2) * OZ_EC;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    for (int mt = mt_first; mt < a.mt; mt += per_nt, ++tl) {
-      const int64_t m = (int64_t)mt * OZ_BM + quarter * 32 + lane;
+    for (int mt = mt_first; mt < a.mt; mt += per_nt) {
+      const int64_t m = (int64_t)mt * OZ_PM + rank * OZ_BM + quarter * 32 + lane;
       const bool mv = m < a.M;
       const int64_t mm = mv ? m : 0;
       const int64_t row_off = oz_out_off(a, mm);
-      const double sx = pow2(code_exp(mv ? a.ex[mm] : 0));  // (outputs of wide rows: replaced by oz_fixup)
+      const double sx = pow2(code_exp(mv ? a.ex[mm] : 0));  // (outputs of wide rows: replaced by oz_cta_fixup)
       // sum_t 2^{8 (NW - 1 - t)} C_t over the weights as they complete (largest weight first)
       double acc[OZ_EC];
 #pragma unroll
       for (int c = 0; c < OZ_EC; ++c) acc[c] = 0.0;
 #pragma unroll 1
-      for (int t = 0; t < OZ_NW; ++t) {
-        const int p = oz_slot(t, tl);
-        mbar_wait(&sfull[p], tl & 1);
-        tc_fence_after();
-        const double w = (double)(1ll << (8 * (OZ_NW - 1 - t)));
+      for (int pass = 0; pass < 2; ++pass, ++q) {
+#pragma unroll 1
+        for (int w = 0; w < 4; ++w) {
+          const int t = 4 * pass + w;
+          const int p = oz_slot((int)(q & 3), w);
+          mbar_wait(&sfull[p], q & 1);
+          tc_fence_after();
+          const double wt = (double)(1ll << (8 * (OZ_NW - 1 - t)));
 #pragma unroll
-        for (int c = 0; c < OZ_EC; c += 16) {
-          uint32_t v[16];
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-              : "r"(tbase + lane_off + (uint32_t)(p * OZ_BN + c0 + c)));
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-          // int32 -> double without I2F: the bits 0x43300000:(v ^ 2^31) are 2^52 + 2^31 + v exactly, and
-          // subtracting 2^52 + 2^31 is exact
-          for (int q = 0; q < 16; ++q)
-            acc[c + q] = fma(__hiloint2double(0x43300000, (int)(v[q] ^ 0x80000000u)) - 4503601774854144.0, w,
-                             acc[c + q]);
+          for (int c = 0; c < OZ_EC; c += 16) {
+            uint32_t v[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                "[%16];\n"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15])
+                : "r"(tbase + lane_off + (uint32_t)(p * OZ_BN + c0 + c)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            // int32 -> double without I2F: the bits 0x43300000:(v ^ 2^31) are 2^52 + 2^31 + v exactly, and
+            // subtracting 2^52 + 2^31 is exact
+#pragma unroll
+            for (int r = 0; r < 16; ++r)
+              acc[c + r] = fma(__hiloint2double(0x43300000, (int)(v[r] ^ 0x80000000u)) - 4503601774854144.0, wt,
+                               acc[c + r]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa(&sempty[p], 0));
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sempty[p]);
       }
-      if (mv) {  // (outputs of wide rows: replaced by oz_cta_fixup after the last tile)
+      if (mv) {
         const bool vec = a.yvec && a.fstride == 1 && ((row_off + n0 + c0) & 1) == 0;
 #pragma unroll
         for (int c = 0; c < OZ_EC; c += 2) {
@@ -690,11 +720,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const __grid_con
         }
       }
     }
-    oz_cta_fixup(a, a.xw, a.fw, mt_first, per_nt, n0, sFix, sFix + OZ_MAXKP);
+    oz_cta_fixup(a, mt_first, per_nt, rank, n0, sFix, sFix + OZ_MAXKP);
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == OZ_EW + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+  cluster_sync();  // every MMA done and every remote arrive delivered before the pair's TMEM is released
+  tc_fence_after();
+  if (warp == OZ_EW + 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -719,11 +750,11 @@ int get_encode(EncodeTiledFn* fn) {
   return FDIGA_OK;
 }
 
-constexpr size_t oz_smem_bytes(int KC) {
-  return 1024 + (size_t)OZ_S * (KC > 2 ? 2 : KC) * OZ_FBYTES + (size_t)OZ_STAGES * OZ_XBYTES +
-         (2 * OZ_STAGES + 4 + 2 * OZ_NW + 2) * 8 +
-         (OZ_BN + OZ_MAXKP + 8 * 32) * sizeof(double);
+constexpr size_t oz_smem_bytes() {
+  return 1024 + (size_t)2 * OZ_S * OZ_FBYTES + (size_t)OZ_NST * OZ_XBYTES + (2 * OZ_NST + 4 + 2 * OZ_NSLOT + 2) * 8 +
+         (OZ_BN + OZ_MAXKP + OZ_EW * 32) * sizeof(double);
 }
+static_assert(oz_smem_bytes() <= 227 * 1024, "shared memory per CTA");
 
 // cudaFuncSetAttribute is per device: one flag bit per device ordinal
 bool attr_once(std::atomic<uint64_t>& done, int device) {
@@ -735,7 +766,9 @@ bool attr_once(std::atomic<uint64_t>& done, int device) {
 
 int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows) {
   const int64_t kp = (k + OZ_BK - 1) / OZ_BK * OZ_BK;
-  const int64_t rows_p = (rows + box_rows - 1) / box_rows * box_rows;
+  // rows padded to the pair tile (data: 256 = two 128-row boxes; factor: 64 = two 32-row halves)
+  const int64_t pad = 2 * box_rows;
+  const int64_t rows_p = (rows + pad - 1) / pad * pad;
   FDIGA_CHECK(kp <= OZ_MAXKP, FDIGA_ERR_NOT_SUPPORTED, "int8-split FD: contraction length %lld > %d",
               (long long)k, OZ_MAXKP);
   if (rows == 0) {  // a rank without planes / chunk: nothing to split or multiply
@@ -819,7 +852,7 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   const OzOperand& F = *g.F;
   FDIGA_CHECK(g.K >= 1 && g.K <= X.kp, FDIGA_ERR_INVALID_ARG, "oz_gemm: contraction length %lld outside (0, %lld]",
               (long long)g.K, (long long)X.kp);
-  FDIGA_CHECK(X.kp == F.kp && X.box_rows == OZ_BM && F.box_rows == OZ_BN, FDIGA_ERR_INVALID_ARG,
+  FDIGA_CHECK(X.kp == F.kp && X.box_rows == OZ_BM && F.box_rows == OZ_BNH, FDIGA_ERR_INVALID_ARG,
               "oz_gemm: operand mismatch");
   if (X.rows == 0 || F.rows == 0) return FDIGA_OK;
   OzKernelArgs a{};
@@ -829,7 +862,7 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   a.f_rows_p = F.rows_p;
   a.KC = (int)(X.kp / OZ_BK);
   a.ks_last = (int)((g.K - (a.KC - 1) * OZ_BK + 31) / 32);  // g.K: the true contraction length
-  a.mt = (int)(X.rows_p / OZ_BM);
+  a.mt = (int)(X.rows_p / OZ_PM);
   a.nt = (int)(F.rows_p / OZ_BN);
   a.K = (int)g.K;
   a.ex = X.exps;
@@ -853,32 +886,34 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   a.fw = F.wide;
   a.skip = g.skip;
   FDIGA_CHECK(g.xs && g.fs && F.ft, FDIGA_ERR_INVALID_ARG, "oz_gemm: FP64 operands for the wide-row fallback missing");
-  FDIGA_CHECK(a.nt <= ctx->sm_count, FDIGA_ERR_NOT_SUPPORTED, "oz_gemm: too many column tiles");
-  const size_t smem = oz_smem_bytes(a.KC);
+  const int npairs_max = ctx->sm_count / 2;
+  FDIGA_CHECK(a.nt <= npairs_max, FDIGA_ERR_NOT_SUPPORTED, "oz_gemm: too many column tiles");
   static std::atomic<uint64_t> attr{0};
-  if (attr_once(attr, ctx->device)) {
-    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)oz_smem_bytes(2)));
-    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)oz_smem_bytes(4)));
-  }
-  // persistent grid: a multiple of the column-tile count, at most one CTA per SM (TMEM: 512 columns)
-  int64_t grid = (int64_t)(ctx->sm_count / a.nt) * a.nt;
-  grid = std::min<int64_t>(grid, (int64_t)a.mt * a.nt);
+  if (attr_once(attr, ctx->device))
+    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz_smem_bytes()));
+  // persistent grid of CTA pairs (clusters of 2): a multiple of the column-tile count, one CTA per SM
+  int64_t npairs = (int64_t)(npairs_max / a.nt) * a.nt;
+  npairs = std::min<int64_t>(npairs, (int64_t)a.mt * a.nt);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)grid);
+  cfg.gridDim = dim3((unsigned)(2 * npairs));
   cfg.blockDim = dim3(OZ_THREADS);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = oz_smem_bytes();
   cfg.stream = stream;
-  cudaLaunchAttribute attr_pdl[1];
-  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr_pdl[0].val.programmaticStreamSerializationAllowed = 0;
-  cfg.attrs = attr_pdl;
-  cfg.numAttrs = 1;
-  const bool stream_f = a.KC > 2;
-  auto kern = stream_f ? oz_gemm_kernel<true> : oz_gemm_kernel<false>;
-  FDIGA_CUDA(cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(X.tmap),
-                                *reinterpret_cast<const CUtensorMap*>(F.tmap), a));
+  cfg.attrs = nullptr;
+  cfg.numAttrs = 0;
+  auto kern = oz_gemm_kernel;
+  {
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(X.tmap),
+                                             *reinterpret_cast<const CUtensorMap*>(F.tmap), a);
+    if (e != cudaSuccess) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, oz_gemm_kernel);
+      FDIGA_CHECK(false, FDIGA_ERR_CUDA, "oz_gemm launch: %s (grid %u, block %u, smem %zu; kernel: %d regs, max %d threads, "
+                  "static smem %zu, max dyn smem %d)", cudaGetErrorString(e), cfg.gridDim.x, cfg.blockDim.x,
+                  cfg.dynamicSmemBytes, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
+                  fa.maxDynamicSharedSizeBytes);
+    }
+  }
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());
   return FDIGA_OK;

@@ -17,8 +17,10 @@ namespace fdiga {
 constexpr int OZ_S = 7;      // digit planes per operand (digit 0 signed, 1..6 unsigned)
 constexpr int OZ_NW = 8;     // digit-pair weights t = i + j = 0..7 (= int32 accumulators in TMEM)
 constexpr int OZ_WSHIFT = 14 + 8 * (OZ_NW - 1);  // 2^(e_x + e_f - WSHIFT) scales sum_t 2^(8 (NW - 1 - t)) C_t
-constexpr int OZ_BM = 128;   // data rows per tile (TMEM lanes)
-constexpr int OZ_BN = 64;    // factor rows per tile (TMEM columns per accumulator)
+constexpr int OZ_BM = 128;   // data rows per CTA (TMEM lanes); a CTA pair (cta_group::2) covers OZ_PM
+constexpr int OZ_PM = 256;   // data rows per pair tile (MMA M)
+constexpr int OZ_BN = 128;   // factor rows per pair tile (MMA N = TMEM columns per accumulator)
+constexpr int OZ_BNH = 64;   // factor rows per CTA (each CTA of the pair holds half of B)
 constexpr int OZ_BK = 128;   // bytes (= k) per TMA box row (SWIZZLE_128B)
 constexpr int OZ_MAXKP = 512;  // contraction lengths up to 512 (factor digits resident up to 256, streamed above)
 // Guard ("accuracy contract"): a row (data fibre or factor row) is "wide" when it holds a
@@ -57,7 +59,8 @@ struct OzOperand {
   void release();
 };
 
-// Allocate (or grow) an operand for `rows` rows of k values; box_rows = OZ_BM (data) or OZ_BN (factor).
+// Allocate (or grow) an operand for `rows` rows of k values; box_rows = OZ_BM (data) or OZ_BNH (factor); rows
+// are padded to 2 box_rows (the pair tile).
 int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows);
 // Factor operands: keep F^T ([k][row], n x n) for the fixup; F row-major n x n on the host.
 int oz_operand_set_ft(OzOperand& op, const double* F_host, int64_t n);
