@@ -293,11 +293,6 @@ __device__ __forceinline__ void tma_load_2sm(void* dst, const void* map, int x, 
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-// K-major operand tile of 128-byte rows written by TMA with SWIZZLE_128B: 8-row atoms 1024 B apart
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
 // single-thread MMA of the pair (issued by the leader CTA inside a warp-converged `if (elect_one())` around a
 // whole stage): D (128 lanes x N columns in each CTA's TMEM) += A (128 rows from each CTA) B^T (N / 2 rows
 // from each CTA), both operands at the same shared-memory offsets in the two CTAs
@@ -327,22 +322,32 @@ __host__ __device__ constexpr uint32_t oz_idesc(bool a_signed, bool b_signed) {
   return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
          ((uint32_t)(OZ_PM >> 4) << 24);
 }
+// K-major operand tile of 64-byte rows written by TMA with SWIZZLE_64B: 8-row atoms 512 B apart
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
 constexpr int OZ_NSLOT = 4;                 // TMEM accumulator slots of OZ_BN columns (4 x 128 = 512)
 constexpr int OZ_EW = 16;                   // epilogue warps: 4 lane quarters x 4 column groups of 32
 constexpr int OZ_EC = 32;                   // columns per epilogue thread
-constexpr int OZ_THREADS = (OZ_EW + 2) * 32;  // + TMA producer warp + MMA warp
-constexpr int OZ_XBYTES = OZ_BM * OZ_BK;    // one data digit plane chunk per CTA: 128 rows x 128 B
-constexpr int OZ_FBYTES = OZ_BNH * OZ_BK;   // one factor digit plane chunk per CTA: 64 rows x 128 B
-constexpr int OZ_NST = 6;                   // data ring stages
+constexpr int OZ_THREADS = (OZ_EW + 3) * 32;  // + TMA producer warp + two MMA warps
+constexpr int OZ_KCH = 64;                  // k per chunk (bytes of a SWIZZLE_64B row)
+constexpr int OZ_KCMAX = 4;                 // chunks per launch: contraction <= 256 per launch
+constexpr int OZ_XPL = OZ_BM * OZ_KCH;      // one data digit plane chunk per CTA: 128 rows x 64 B = 8 KB
+constexpr int OZ_FPL = OZ_BNH * OZ_KCH;     // one factor digit plane chunk per CTA: 64 rows x 64 B = 4 KB
+constexpr int OZ_NXS = 14;                  // data plane slots in the ring (two pass-1 chunks)
 static_assert(OZ_EC * (OZ_EW / 4) == OZ_BN, "epilogue column groups cover the tile");
 
 struct OzKernelArgs {
   int64_t M, Nf;     // data rows, factor rows
   int64_t x_rows_p, f_rows_p;
-  int KC;            // 128-wide k chunks
-  int ks_last;       // K-steps of 32 in the last chunk that reach below the contraction length (1..4)
+  int KC;            // 64-wide k chunks of this launch
+  int kbase;         // first k of this launch (contractions > 256 take two launches)
+  int ks_last;       // K-steps of 32 in the last chunk that reach below the contraction length (1..2)
   int mt, nt;        // pair tiles along M (256 rows) and Nf (128 rows)
-  int K;             // contraction length
+  int K;             // contraction length (all launches)
+  bool accum;        // y += (the second launch of a split contraction); else y =
+  bool fixup;        // the launch that recomputes the outputs of wide rows (the last one)
   const int32_t* ex;
   const int32_t* ef;
   double* y;
@@ -440,52 +445,37 @@ __device__ void oz_cta_fixup(const OzKernelArgs& a, int mt_first, int per_nt, ui
 }
 
 // Two passes per tile over the contraction: pass 0 accumulates the weights t = 0..3 (10 digit pairs, data and
-// factor digits 0..3), pass 1 the weights 4..7 (24 pairs, digits 0..6), four int32 accumulators of 128 columns
-// each (all 512 TMEM columns).  Phase q = 2 tile + pass.  Within a phase the first k chunk takes the data
-// digits in descending order and later chunks ascending, so the weights are first written in the order
-// 3, 2, 1, 0 (pass 0) / {6, 7}, 5, 4 (pass 1) and complete in the order 0, 1, 2, 3 / 4, 5, {6, 7}.  The
-// epilogue drains every phase in ascending weight order.  The slot of a weight is chosen so that the next
-// phase first writes its slots in exactly the order the epilogue drains them (the assignment repeats every
-// two tiles):
-//   q % 4 = 0: w0..w3 -> slots 3 2 1 0     q % 4 = 1: w4..w7 -> 0 1 3 2
-//   q % 4 = 2: w0..w3 -> slots 2 3 1 0     q % 4 = 3: w4..w7 -> 0 1 2 3
-__host__ __device__ constexpr int oz_slot(int q4, int t) {
-  // the table above, 2 bits per entry, entry (q4, t) at bit 2 (4 q4 + t)
-  constexpr uint32_t T = (3u << 0) | (2u << 2) | (1u << 4) | (0u << 6) | (0u << 8) | (1u << 10) | (3u << 12) |
-                         (2u << 14) | (2u << 16) | (3u << 18) | (1u << 20) | (0u << 22) | (0u << 24) | (1u << 26) |
-                         (2u << 28) | (3u << 30);
-  return (int)((T >> (2 * (4 * q4 + (t & 3)))) & 3u);
-}
-// digit pairs (I, j) of pass P: i + j in [4P, 4P + 3], i, j <= 6
-__host__ __device__ constexpr int oz_jlo(int P, int I) { return P == 0 ? 0 : (4 - I > 0 ? 4 - I : 0); }
-__host__ __device__ constexpr int oz_jhi(int P, int I) { return P == 0 ? 3 - I : (7 - I < 6 ? 7 - I : 6); }
-// does stage I of the first chunk write weight I + j first (descending digit order)?
-__host__ __device__ constexpr bool oz_first_touch(int P, int I, int j) {
-  return P == 0 ? j == 0 : ((I == 6 && j <= 1) || ((I == 5 || I == 4) && j == 0));
+// factor digits 0..3), pass 1 the weights 4..7 (24 pairs, digits 0..6): four int32 accumulators of 128 columns
+// (all 512 TMEM columns).  Phase q = 2 tile + pass.  Within every 64-wide k chunk the MMAs go weight by weight
+// in the phase's order (pass 0: 0, 1, 2, 3; pass 1: 6, 5, 7, 4); the k-th weight of every phase lives in slot k.
+// So in the first chunk the slots are first written one after another, and in the last chunk they complete
+// one after another, the first ones well before the phase ends: the epilogue drains slot k of phase q while
+// the MMAs of q's remaining weights and of q + 1's first weights run (slack of 12 or more MMAs per slot).
+__host__ __device__ constexpr int oz_weight(int P, int k) {
+  return P == 0 ? k : (k == 0 ? 6 : k == 1 ? 5 : k == 2 ? 7 : 4);
 }
 
-// the MMAs of data digit I in pass P: pairs (I, j) into weight I + j, NKS K-steps of 32 (k step outer, pair
-// inner: consecutive MMAs share the A operand).  so[w & 3]: the TMEM column of weight w's slot in this phase.
-// db_kc: descriptor of factor digit 0 of this k chunk (digit j is j chunks further).  Digit 0 is signed, the
-// others unsigned: the instruction descriptor is chosen per pair.  One elected lane issues the whole stage.
-template <int P, int I>
-__device__ __forceinline__ void oz_stage_mmas(const uint32_t (&so)[4], uint64_t da, uint64_t db_kc, bool first_kc,
-                                              int nks) {
+// the MMAs of weight T (slot sk) in one chunk: pairs (i, T - i), NKS K-steps of 32 each.  xd[i]: descriptor of
+// data digit i's plane chunk, fd: descriptor of factor digit 0's plane chunk (digit j is j planes further).
+// first: the weight's first MMA overwrites its slot.  One elected lane issues (operands computed by the
+// converged warp).
+template <int T>
+__device__ __forceinline__ void oz_weight_mmas(uint32_t td, const uint64_t (&xd)[OZ_S], uint64_t fd, bool first,
+                                               int nks) {
+  constexpr int ilo = T > OZ_S - 1 ? T - (OZ_S - 1) : 0, ihi = T < OZ_S - 1 ? T : OZ_S - 1;
   if (elect_one()) {
-    if (nks == OZ_BK / 32) {
+    if (nks == 2) {
 #pragma unroll
-      for (int kk = 0; kk < OZ_BK / 32; ++kk)
+      for (int i = ilo; i <= ihi; ++i)
 #pragma unroll
-        for (int j = oz_jlo(P, I); j <= oz_jhi(P, I); ++j)
-          mma_i8_pair(so[(I + j) & 3], da + 2 * kk, db_kc + (uint64_t)(j * (OZ_FBYTES >> 4) + 2 * kk),
-                      oz_idesc(I == 0, j == 0), (kk != 0 || !(first_kc && oz_first_touch(P, I, j))) ? 1u : 0u);
-    } else {  // short last chunk: only the K-steps that reach below the contraction length
-#pragma unroll 1
-      for (int kk = 0; kk < nks; ++kk)
+        for (int kk = 0; kk < 2; ++kk)
+          mma_i8_pair(td, xd[i] + 2 * kk, fd + (uint64_t)((T - i) * (OZ_FPL >> 4) + 2 * kk),
+                      oz_idesc(i == 0, T - i == 0), (first && i == ilo && kk == 0) ? 0u : 1u);
+    } else {
 #pragma unroll
-        for (int j = oz_jlo(P, I); j <= oz_jhi(P, I); ++j)
-          mma_i8_pair(so[(I + j) & 3], da + 2 * kk, db_kc + (uint64_t)(j * (OZ_FBYTES >> 4) + 2 * kk),
-                      oz_idesc(I == 0, j == 0), (kk != 0 || !(first_kc && oz_first_touch(P, I, j))) ? 1u : 0u);
+      for (int i = ilo; i <= ihi; ++i)
+        mma_i8_pair(td, xd[i], fd + (uint64_t)((T - i) * (OZ_FPL >> 4)), oz_idesc(i == 0, T - i == 0),
+                    (first && i == ilo) ? 0u : 1u);
     }
   }
   __syncwarp();
@@ -493,9 +483,9 @@ __device__ __forceinline__ void oz_stage_mmas(const uint32_t (&so)[4], uint64_t 
 
 // One CTA pair (cluster of 2, the SMs of a TPC) per pair tile: 256 data rows (128 per CTA = the TMEM lanes of
 // each CTA) x 128 factor rows (64 per CTA), four accumulator slots of 128 columns in each CTA's TMEM.  The
-// leader (rank 0) issues every MMA (M = 256, N = 128, K = 32); both CTAs stream their own data rows and their
-// half of the factor rows (one k chunk of factor digits at a time, double-buffered) by TMA, completion
-// counted on the leader's barriers, and drain their own accumulators.
+// leader (rank 0) issues every MMA (M = 256, N = 128, K = 32); both CTAs keep their half of the factor digits
+// resident (<= 256 k) and stream their own data rows through a ring of 14 plane slots (64 k each) by TMA,
+// completion counted on the leader's barriers, and drain their own accumulators.
 __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap fmap,
                    const __grid_constant__ OzKernelArgs a) {
@@ -504,30 +494,26 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
   extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
   const int KC = a.KC;
-  uint8_t* sF = smem;                                  // [2][S] factor chunks of this CTA's 64 rows
-  uint8_t* sX = smem + 2 * OZ_S * OZ_FBYTES;           // data ring [NST]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_NST * OZ_XBYTES);  // [NST] (leader: both CTAs' bytes)
-  uint64_t* empty = full + OZ_NST;                                        // [NST] (each CTA, multicast commit)
-  uint64_t* ffull = empty + OZ_NST;   // [2] factor chunk landed (leader)
-  uint64_t* fempty = ffull + 2;       // [2] factor chunk consumed (each CTA)
-  uint64_t* sfull = fempty + 2;       // [4] accumulator slot complete (MMA -> epilogues of both CTAs)
+  uint8_t* sF = smem;                                    // [KC][S] resident factor planes, this CTA's 64 rows
+  uint8_t* sX = smem + OZ_KCMAX * OZ_S * OZ_FPL;         // data ring [NXS] plane slots
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_NXS * OZ_XPL);  // [NXS] (leader: both CTAs' bytes)
+  uint64_t* empty = full + OZ_NXS;                                     // [NXS] (each CTA, multicast commit)
+  uint64_t* fbar = empty + OZ_NXS;    // [1] factor landed (leader)
+  uint64_t* sfull = fbar + 1;         // [4] accumulator slot complete (MMA -> epilogues of both CTAs)
   uint64_t* sempty = sfull + OZ_NSLOT;  // [4] accumulator slot drained by both CTAs (leader)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_NSLOT);
   double* sSF = reinterpret_cast<double*>(sempty + OZ_NSLOT + 2);  // 2^(e_f - WSHIFT) of the pair's factor rows
-  double* sFix = sSF + OZ_BN;  // fixup: [OZ_MAXKP] row + [OZ_EW][32] partial sums
+  double* sFix = reinterpret_cast<double*>(sX);  // fixup scratch after the last tile: [OZ_MAXKP] + [OZ_EW][32]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < OZ_NST; ++s) {
+    for (int s = 0; s < OZ_NXS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 2);  // both MMA warps commit
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&ffull[s], 1);
-      mbar_init(&fempty[s], 1);
-    }
+    mbar_init(fbar, 1);
     for (int t = 0; t < OZ_NSLOT; ++t) {
       mbar_init(&sfull[t], 1);
       mbar_init(&sempty[t], 2 * OZ_EW);
@@ -552,99 +538,92 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
 
   if (warp == OZ_EW) {
     if (lane == 0) {
-      uint32_t st = 0, ph = 0, fc = 0;
+      // resident factor digit planes: this CTA's 64 of the pair's 128 rows, [kc][digit] chunks
+      if (leader) mbar_arrive_expect_tx(fbar, (uint32_t)(2 * OZ_S * KC * OZ_FPL));
+      const uint32_t fbar_l = mapa(fbar, 0);
+      for (int kc = 0; kc < KC; ++kc)
+        for (int s = 0; s < OZ_S; ++s)
+          tma_load_2sm(sF + (kc * OZ_S + s) * OZ_FPL, &fmap, a.kbase + kc * OZ_KCH,
+                       (int)(s * a.f_rows_p + n0 + rank * OZ_BNH), fbar_l);
+      uint32_t st = 0, ph = 0;
       bool wrapped = false;
       for (int mt = mt_first; mt < a.mt; mt += per_nt) {
         const int m0 = mt * OZ_PM + (int)rank * OZ_BM;
         for (int pass = 0; pass < 2; ++pass) {
-          const int nd = pass == 0 ? 4 : OZ_S;  // digits of this pass (factor and data)
-          for (int kc = 0; kc < KC; ++kc) {
-            {  // this chunk's factor digits (this CTA's 64 rows) into factor slot fc % 2
-              const uint32_t fs = fc & 1;
-              if (fc >= 2) mbar_wait(&fempty[fs], ((fc >> 1) - 1) & 1);
-              if (leader) mbar_arrive_expect_tx(&ffull[fs], (uint32_t)(2 * nd * OZ_FBYTES));
-              const uint32_t bar = mapa(&ffull[fs], 0);
-              for (int s = 0; s < nd; ++s)
-                tma_load_2sm(sF + (fs * OZ_S + s) * OZ_FBYTES, &fmap, kc * OZ_BK,
-                             (int)(s * a.f_rows_p + n0 + rank * OZ_BNH), bar);
-              ++fc;
-            }
-            for (int pos = 0; pos < nd; ++pos) {
-              const int i = kc == 0 ? nd - 1 - pos : pos;  // the MMA warp's digit order
+          const int nd = pass == 0 ? 4 : OZ_S;  // data digits of this pass
+          for (int kc = 0; kc < KC; ++kc)
+            for (int i = 0; i < nd; ++i) {
               if (wrapped) mbar_wait(&empty[st], ph ^ 1);
-              if (leader) mbar_arrive_expect_tx(&full[st], 2 * OZ_XBYTES);
-              tma_load_2sm(sX + st * OZ_XBYTES, &xmap, kc * OZ_BK, (int)(i * a.x_rows_p + m0), mapa(&full[st], 0));
-              if (++st == OZ_NST) {
+              if (leader) mbar_arrive_expect_tx(&full[st], 2 * OZ_XPL);
+              tma_load_2sm(sX + st * OZ_XPL, &xmap, a.kbase + kc * OZ_KCH, (int)(i * a.x_rows_p + m0),
+                           mapa(&full[st], 0));
+              if (++st == OZ_NXS) {
                 st = 0;
                 ph ^= 1;
                 wrapped = true;
               }
             }
-          }
         }
       }
     }
-  } else if (warp == OZ_EW + 1) {
-    if (leader) {  // the whole warp runs the issue loop (uniform operands); one elected lane issues
-      const uint64_t da0 = sdesc_sw128(smem_u32(sX)), db0 = sdesc_sw128(smem_u32(sF));
-      uint32_t st = 0, ph = 0, fc = 0, q = 0;
+  } else if (warp >= OZ_EW + 1) {
+    // two MMA warps (leader CTA): warp OZ_EW + 1 issues slots 0 and 3, warp OZ_EW + 2 slots 1 and 2, so one
+    // warp's barrier waits and commits overlap the other's MMAs (a single issuing thread left the tensor pipe
+    // idle between short weight groups)
+    const int mw = warp - (OZ_EW + 1);
+    if (leader) {  // each warp runs its issue loop converged (uniform operands); one elected lane issues
+      mbar_wait(fbar, 0);
+      tc_fence_after();
+      const uint32_t sx0 = smem_u32(sX);
+      const uint64_t fd0 = sdesc_sw64(smem_u32(sF));
+      uint32_t st = 0, ph = 0, q = 0;
       for (int mt = mt_first; mt < a.mt; mt += per_nt) {
         for (int pass = 0; pass < 2; ++pass, ++q) {
-          uint32_t so[4];
-#pragma unroll
-          for (int w = 0; w < 4; ++w) so[w] = tbase + (uint32_t)(oz_slot((int)(q & 3), w) * OZ_BN);
+          const int nd = pass == 0 ? 4 : OZ_S;
           for (int kc = 0; kc < KC; ++kc) {
-            const uint32_t fs = fc & 1;
-            mbar_wait(&ffull[fs], (fc >> 1) & 1);
-            tc_fence_after();
-            const uint64_t dbk = db0 + (uint64_t)(fs * OZ_S * (OZ_FBYTES >> 4));
             const bool first = kc == 0, last = kc == KC - 1;
-            const int nks = last ? a.ks_last : OZ_BK / 32;  // K-steps of 32 carrying real contraction indices
-#define OZ_WAIT_SLOT(w) mbar_wait(&sempty[oz_slot((int)(q & 3), (w))], (q - 1) & 1)
-#define OZ_STAGE(P, I)                                                                                 \
-  {                                                                                                    \
-    mbar_wait(&full[st], ph);                                                                          \
-    tc_fence_after();                                                                                  \
-    if (first && q > 0) { /* weights first written by this stage: their slots must be drained */      \
-      if (P == 0) OZ_WAIT_SLOT(I);                                                                     \
-      if (P == 1 && I >= 4) OZ_WAIT_SLOT(I);                                                           \
-      if (P == 1 && I == 6) OZ_WAIT_SLOT(7);                                                           \
-      tc_fence_after();                                                                                \
-    }                                                                                                  \
-    oz_stage_mmas<P, I>(so, da0 + (uint64_t)(st * (OZ_XBYTES >> 4)), dbk, first, nks);                 \
-    tc_commit_pair(&empty[st]); /* frees the ring slot in both CTAs when these MMAs have read it */     \
-    if (last && !first) { /* ascending: weights complete after their last digit */                     \
-      if (P == 0) tc_commit_pair(&sfull[oz_slot((int)(q & 3), I)]);                                    \
-      if (P == 1 && I >= 4) tc_commit_pair(&sfull[oz_slot((int)(q & 3), I)]);                          \
-      if (P == 1 && I == 6) tc_commit_pair(&sfull[oz_slot((int)(q & 3), 7)]);                          \
-    }                                                                                                  \
-    if (++st == OZ_NST) {                                                                              \
-      st = 0;                                                                                          \
-      ph ^= 1;                                                                                         \
-    }                                                                                                  \
-  }
-            static_assert(OZ_S == 7 && OZ_NW == 8, "stage sequences written for 7 digits, 8 weights");
-            if (pass == 0) {
-              if (first) {
-                OZ_STAGE(0, 3) OZ_STAGE(0, 2) OZ_STAGE(0, 1) OZ_STAGE(0, 0)
+            const int nks = last ? a.ks_last : OZ_KCH / 32;  // K-steps of 32 carrying real contraction indices
+            // this chunk's data planes: slots st, st + 1, .. (mod NXS)
+            uint64_t xd[OZ_S];
+            uint32_t s2 = st, p2 = ph;
+#pragma unroll
+            for (int i = 0; i < OZ_S; ++i) {
+              if (i < nd) {
+                mbar_wait(&full[s2], p2);
+                xd[i] = sdesc_sw64(sx0 + s2 * OZ_XPL);
+                if (++s2 == OZ_NXS) {
+                  s2 = 0;
+                  p2 ^= 1;
+                }
               } else {
-                OZ_STAGE(0, 0) OZ_STAGE(0, 1) OZ_STAGE(0, 2) OZ_STAGE(0, 3)
-              }
-            } else {
-              if (first) {
-                OZ_STAGE(1, 6) OZ_STAGE(1, 5) OZ_STAGE(1, 4) OZ_STAGE(1, 3) OZ_STAGE(1, 2) OZ_STAGE(1, 1)
-                OZ_STAGE(1, 0)
-              } else {
-                OZ_STAGE(1, 0) OZ_STAGE(1, 1) OZ_STAGE(1, 2) OZ_STAGE(1, 3) OZ_STAGE(1, 4) OZ_STAGE(1, 5)
-                OZ_STAGE(1, 6)
+                xd[i] = 0;
               }
             }
-#undef OZ_STAGE
-#undef OZ_WAIT_SLOT
-            tc_commit_pair(&fempty[fs]);  // the factor slot is free when this chunk's MMAs have read it
-            ++fc;
-            if (first && last)  // single k chunk (descending): every weight of the pass completes at its end
-              for (int w = 0; w < 4; ++w) tc_commit_pair(&sfull[oz_slot((int)(q & 3), w)]);
+            tc_fence_after();
+            const uint64_t fd = fd0 + (uint64_t)(kc * OZ_S * (OZ_FPL >> 4));
+#define OZ_WEIGHT(P, K)                                                                                \
+  if (mw == ((K == 0 || K == 3) ? 0 : 1)) {                                                            \
+    if (first && q > 0) { /* the slot's previous accumulator must be drained */                      \
+      mbar_wait(&sempty[K], (q - 1) & 1);                                                              \
+      tc_fence_after();                                                                                \
+    }                                                                                                  \
+    oz_weight_mmas<oz_weight(P, K)>(tbase + (uint32_t)(K * OZ_BN), xd, fd, first, nks);                \
+    if (last) tc_commit_pair(&sfull[K]); /* weight complete */                                         \
+  }
+            static_assert(OZ_S == 7 && OZ_NW == 8, "weight sequences written for 7 digits, 8 weights");
+            if (pass == 0) {
+              OZ_WEIGHT(0, 0) OZ_WEIGHT(0, 1) OZ_WEIGHT(0, 3) OZ_WEIGHT(0, 2)
+            } else {
+              OZ_WEIGHT(1, 0) OZ_WEIGHT(1, 1) OZ_WEIGHT(1, 3) OZ_WEIGHT(1, 2)
+            }
+#undef OZ_WEIGHT
+            for (int i = 0; i < nd; ++i) {  // free the chunk's plane slots in both CTAs when its MMAs are done
+              tc_commit_pair(&empty[st]);
+              if (++st == OZ_NXS) {
+                st = 0;
+                ph ^= 1;
+              }
+            }
           }
         }
       }
@@ -666,20 +645,18 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
       const int64_t mm = mv ? m : 0;
       const int64_t row_off = oz_out_off(a, mm);
       const double sx = pow2(code_exp(mv ? a.ex[mm] : 0));  // (outputs of wide rows: replaced by oz_cta_fixup)
-      // sum_t 2^{8 (NW - 1 - t)} C_t over the weights as they complete (largest weight first)
+      // sum_t 2^{8 (NW - 1 - t)} C_t over the weights as they complete
       double acc[OZ_EC];
 #pragma unroll
       for (int c = 0; c < OZ_EC; ++c) acc[c] = 0.0;
 #pragma unroll 1
       for (int pass = 0; pass < 2; ++pass, ++q) {
 #pragma unroll 1
-        for (int w = 0; w < 4; ++w) {
-          const int t = 4 * pass + w;
-          const int p = oz_slot((int)(q & 3), w);
-          mbar_wait(&sfull[p], q & 1);
+        for (int k = 0; k < OZ_NSLOT; ++k) {
+          const int t = pass == 0 ? k : (k == 0 ? 6 : k == 1 ? 5 : k == 2 ? 7 : 4);  // oz_weight(pass, k)
+          mbar_wait(&sfull[k], q & 1);
           tc_fence_after();
           const double wt = (double)(1ll << (8 * (OZ_NW - 1 - t)));
-#pragma unroll
 #pragma unroll
           for (int c = 0; c < OZ_EC; c += 16) {
             uint32_t v[16];
@@ -689,7 +666,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
                   "=r"(v[15])
-                : "r"(tbase + lane_off + (uint32_t)(p * OZ_BN + c0 + c)));
+                : "r"(tbase + lane_off + (uint32_t)(k * OZ_BN + c0 + c)));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
             // int32 -> double without I2F: the bits 0x43300000:(v ^ 2^31) are 2^52 + 2^31 + v exactly, and
             // subtracting 2^52 + 2^31 is exact
@@ -700,7 +677,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(mapa(&sempty[p], 0));
+          if (lane == 0) mbar_arrive_cluster(mapa(&sempty[k], 0));
         }
       }
       if (mv) {
@@ -709,18 +686,33 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
         for (int c = 0; c < OZ_EC; c += 2) {
           const int64_t f = n0 + c0 + c;
           // two exact power-of-two scalings: the factor row's (with the digit weight) and the data row's
-          const double y0 = (acc[c] * sSF[c0 + c]) * sx;
-          const double y1 = (acc[c + 1] * sSF[c0 + c + 1]) * sx;
+          double y0 = (acc[c] * sSF[c0 + c]) * sx;
+          double y1 = (acc[c + 1] * sSF[c0 + c + 1]) * sx;
           if (vec && f + 1 < a.Nf) {  // contiguous factor index (mode 1): one 16-byte store per pair
-            *reinterpret_cast<double2*>(a.y + row_off + f) = make_double2(y0, y1);
+            double2* p = reinterpret_cast<double2*>(a.y + row_off + f);
+            if (a.accum) {
+              const double2 o = *p;
+              y0 += o.x;
+              y1 += o.y;
+            }
+            *p = make_double2(y0, y1);
           } else {
-            if (f < a.Nf) a.y[row_off + f * a.fstride] = y0;
-            if (f + 1 < a.Nf) a.y[row_off + (f + 1) * a.fstride] = y1;
+            if (f < a.Nf) {
+              double* p = a.y + row_off + f * a.fstride;
+              *p = a.accum ? *p + y0 : y0;
+            }
+            if (f + 1 < a.Nf) {
+              double* p = a.y + row_off + (f + 1) * a.fstride;
+              *p = a.accum ? *p + y1 : y1;
+            }
           }
         }
       }
     }
-    oz_cta_fixup(a, mt_first, per_nt, rank, n0, sFix, sFix + OZ_MAXKP);
+    if (a.fixup) {
+      oz_bar_epi();  // (every epilogue warp past its last drain: the data ring is free for the fixup)
+      oz_cta_fixup(a, mt_first, per_nt, rank, n0, sFix, sFix + OZ_MAXKP);
+    }
   }
   tc_fence_before();
   cluster_sync();  // every MMA done and every remote arrive delivered before the pair's TMEM is released
@@ -751,10 +743,11 @@ int get_encode(EncodeTiledFn* fn) {
 }
 
 constexpr size_t oz_smem_bytes() {
-  return 1024 + (size_t)2 * OZ_S * OZ_FBYTES + (size_t)OZ_NST * OZ_XBYTES + (2 * OZ_NST + 4 + 2 * OZ_NSLOT + 2) * 8 +
-         (OZ_BN + OZ_MAXKP + OZ_EW * 32) * sizeof(double);
+  return 1024 + (size_t)OZ_KCMAX * OZ_S * OZ_FPL + (size_t)OZ_NXS * OZ_XPL + (2 * OZ_NXS + 1 + 2 * OZ_NSLOT + 2) * 8 +
+         OZ_BN * sizeof(double);
 }
 static_assert(oz_smem_bytes() <= 227 * 1024, "shared memory per CTA");
+static_assert((OZ_MAXKP + OZ_EW * 32) * sizeof(double) <= (size_t)OZ_NXS * OZ_XPL, "fixup scratch in the data ring");
 
 // cudaFuncSetAttribute is per device: one flag bit per device ordinal
 bool attr_once(std::atomic<uint64_t>& done, int device) {
@@ -797,11 +790,11 @@ int oz_operand_alloc(OzOperand& op, int64_t rows, int64_t k, int box_rows) {
   FDIGA_TRY(get_encode(&enc));
   cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)(OZ_S * rows_p)};
   cuuint64_t strides[1] = {(cuuint64_t)kp};
-  cuuint32_t box[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)OZ_KCH, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   static_assert(sizeof(CUtensorMap) <= sizeof(op.tmap), "tensor map size");
   const CUresult r = enc(reinterpret_cast<CUtensorMap*>(op.tmap), CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, op.digits, dims,
-                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   FDIGA_CHECK(r == CUDA_SUCCESS, FDIGA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return FDIGA_OK;
@@ -860,8 +853,6 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   a.Nf = F.rows;
   a.x_rows_p = X.rows_p;
   a.f_rows_p = F.rows_p;
-  a.KC = (int)(X.kp / OZ_BK);
-  a.ks_last = (int)((g.K - (a.KC - 1) * OZ_BK + 31) / 32);  // g.K: the true contraction length
   a.mt = (int)(X.rows_p / OZ_PM);
   a.nt = (int)(F.rows_p / OZ_BN);
   a.K = (int)g.K;
@@ -902,7 +893,14 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   cfg.attrs = nullptr;
   cfg.numAttrs = 0;
   auto kern = oz_gemm_kernel;
-  {
+  // contractions longer than 256 (the resident factor chunks): two launches, the second accumulating into y
+  for (int kbase = 0; kbase < g.K; kbase += OZ_KCMAX * OZ_KCH) {
+    const int klen = (int)std::min<int64_t>(g.K - kbase, OZ_KCMAX * OZ_KCH);
+    a.kbase = kbase;
+    a.KC = (klen + OZ_KCH - 1) / OZ_KCH;
+    a.ks_last = (klen - (a.KC - 1) * OZ_KCH + 31) / 32;  // K-steps of the last chunk below the contraction length
+    a.accum = kbase > 0;
+    a.fixup = kbase + klen >= g.K;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(X.tmap),
                                              *reinterpret_cast<const CUtensorMap*>(F.tmap), a);
     if (e != cudaSuccess) {
@@ -913,6 +911,7 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
                   cfg.dynamicSmemBytes, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
                   fa.maxDynamicSharedSizeBytes);
     }
+    if (kbase > 0) count_launch(ctx);
   }
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());

@@ -18,7 +18,7 @@ template <int MODE>
 __global__ void __launch_bounds__(128, 1) k(int iters, int* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* s = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t bar, bar2;
+  __shared__ uint64_t bar, bar2, bar3;
   __shared__ uint32_t slot;
   // A: 16 KB at 0; B: 7 planes of 8 KB at 16 KB
   for (int i = threadIdx.x; i < (16 + 56) * 1024 / 4; i += blockDim.x) ((int*)s)[i] = (int)(i * 2654435761u + 12345u + blockIdx.x);
@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int* out) {
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar2)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar3)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (threadIdx.x < 32) {
@@ -38,6 +39,9 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int* out) {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t t = slot;
+  unsigned long long g0, c0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  c0 = clock64();
   if (threadIdx.x == 0 && rank == 0) {
     const uint64_t da = sdesc(su32(s)), db = sdesc(su32(s + 16384));
     for (int it = 0; it < iters; ++it) {
@@ -52,12 +56,21 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int* out) {
             "l"(da + 2 * kk), "l"(db + (uint64_t)(j * 512 + 2 * kk)), "r"(id), "r"(acc));
         if ((MODE & 8) && (q & 3) == 3)
           asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(su32(&bar2)), "h"((uint16_t)3));
+        if ((MODE & 16) && (q & 3) == 3) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if ((MODE & 32) && (q & 3) == 3)  // wait on an already-completed barrier (phase 1 of bar3 never completes: parity 1 returns at once)
+          asm volatile("{\n .reg .pred p;\nW2: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 1;\n @!p bra W2;\n}" ::"r"(su32(&bar3)) : "memory");
       }
     }
     asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(su32(&bar)), "h"((uint16_t)3));
   }
   if (threadIdx.x == 0)
     asm volatile("{\n .reg .pred p;\nW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra W;\n}" ::"r"(su32(&bar)));
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long g1, c1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    c1 = clock64();
+    out[1] = (int)((c1 - c0) / ((g1 - g0) / 1000.0 + 1e-9));  // MHz
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(t));
@@ -66,10 +79,10 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int* out) {
 template <int MODE>
 void run() {
   int* out;
-  cudaMalloc(&out, 4);
+  cudaMalloc(&out, 8);
   const int smem = 1024 + (16 + 56) * 1024;
   cudaFuncSetAttribute(k<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const int iters = 1000;
+  const int iters = 20000;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(148);
   cfg.blockDim = dim3(128);
@@ -92,15 +105,16 @@ void run() {
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
-  printf("mode %2d (B7=%d D4=%d mixed=%d commit=%d): %.1f ns per MMA (err %s)\n", MODE, MODE & 1, (MODE >> 1) & 1,
-         (MODE >> 2) & 1, (MODE >> 3) & 1, ms * 1e6 / (iters * 28.0), cudaGetErrorString(cudaGetLastError()));
+  int hout[2];
+  cudaMemcpy(hout, out, 8, cudaMemcpyDeviceToHost);
+  printf("SM clock during the run: %d MHz; ", hout[1]);
+  printf("mode %2d (B7=%d D4=%d mixed=%d commit=%d fence=%d wait=%d): %.1f ns per MMA (err %s)\n", MODE, MODE & 1, (MODE >> 1) & 1,
+         (MODE >> 2) & 1, (MODE >> 3) & 1, (MODE >> 4) & 1, (MODE >> 5) & 1, ms * 1e6 / (iters * 28.0), cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
-  run<0>();
-  run<1>();
-  run<2>();
-  run<4>();
-  run<8>();
   run<15>();
+  run<16>();
+  run<32>();
+  run<63>();
   return 0;
 }
