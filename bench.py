@@ -3,8 +3,10 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--n 256] [--impl {fdiga,reference}] [--no-gmres]
 
 Headline (BASELINE.json metric, configs[3] at n=256 = the north-star target size):
-  value = N / t_apply  [GDOF/s],  N = n^3,  t_apply = device time of one fd_apply (6 DMMA mode products,
-  eigenvalue divide fused), inputs resident in HBM, CUDA events on the library's stream, max over ranks.
+  value = N / t_apply  [GDOF/s],  N = n^3,  t_apply = device time of one fd_apply (at n = 256: 6 int8-split
+  tensor-core mode products, each a digit split + a tcgen05 GEMM, the eigenvalue divide in the split feeding
+  the backward mode-3 product), inputs resident in HBM, CUDA events on the library's stream,
+  max over ranks.  fp64_native: the same apply on the IEEE-FP64 DMMA path.
   The 134 MB input plus three 134 MB work buffers exceed the 126 MB L2, so no flush is needed.
 Secondary (same JSON line):
   e2e       the same metric through fd_apply_host (pinned host buffers; H2D + apply + D2H timed per step)
@@ -72,7 +74,7 @@ def int8_peak():
 
 def roofline(path, kern, flops, int8_ops, achieved_fp64, fp64_pk, traffic, ws):
     """The dominant kernel's roofline.  DMMA path: dmma_gemm_kernel, FP64 tensor, 4 N n_l flop per launch.
-    int8 path: oz_gemm_kernel, int8 tensor, 2 M N K ops per digit-pair MMA (36 pairs per mode product)."""
+    int8 path: oz_gemm_kernel, int8 tensor, 2 M N K ops per digit-pair MMA (34 pairs per mode product)."""
     fp64_eq = {"achieved": achieved_fp64, "peak": fp64_pk, "unit": "TFLOP/s", "frac": achieved_fp64 / fp64_pk,
                "what": "whole FD apply: 4 N sum(n_l) FP64 flop / apply time, against the FP64 (DMMA) peak"}
     if path == "int8_split" and kern and "int8_gemm" in kern:
@@ -199,6 +201,49 @@ def cpu_fd_sample(n, budget_s=12.0, max_reps=20):
                        f"host has {os.cpu_count()} logical cores", seconds_per_apply=t)
 
 
+def cpu_fd_sample_1thread(n=128, budget_s=8.0):
+    """The oracle FD apply on ONE host thread (threadpoolctl), the closest analogue of the paper's single
+    core, at a size whose apply takes about a second."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:
+        return None
+    with threadpool_limits(limits=1):
+        r = cpu_fd_sample(n, budget_s=budget_s, max_reps=10)
+    r["cores"] = 1
+    r["sample"] = r["sample"].replace("host has", "1 BLAS thread (threadpoolctl); host has")
+    return r
+
+
+def cpu_gmres_sample(budget_s=45.0):
+    """The oracle's FD-preconditioned GMRES(30) (oracle/krylov.py, oracle/fastdiag.py, oracle's sum-factorised
+    matvec) on the host cores: full solves for configs[0..2]; configs[4] timed over its first few Arnoldi steps
+    (ms per iteration, extrapolated to the GPU's iteration count in `est_total_s`)."""
+    from oracle import assembly, fastdiag, krylov
+    from synth import get_config, rhs
+    out = {}
+    t_all = time.perf_counter()
+    for cfg in (1, 2, 3, 5):
+        c = get_config(cfg)
+        t0 = time.perf_counter()
+        disc = assembly.Discretisation(c.d, c.p, c.ne, c.geometry, c.geo_params)
+        f = fastdiag.setup([disc.M] * c.d, [disc.K] * c.d)
+        t_setup = time.perf_counter() - t0
+        b = rhs(cfg, disc.N)
+        cap = 3 if cfg == 5 else 1000
+        t0 = time.perf_counter()
+        _, rep = krylov.gmres(disc.matvec, b, precond=lambda v: fastdiag.apply(f, v), max_iters=cap)
+        dt = time.perf_counter() - t0
+        e = {"N": disc.N, "iters": rep["iters"], "setup_s": t_setup, "solve_s": dt,
+             "ms_per_iter": dt / max(1, rep["iters"]) * 1e3}
+        if cfg == 5:
+            e["note"] = f"first {rep['iters']} Arnoldi steps only (bounded sample)"
+        out[f"cfg{cfg}"] = e
+        if time.perf_counter() - t_all > budget_s:
+            break
+    return out
+
+
 def run_reference(args):
     """The reference arm: the CPU oracle (numpy mode products) on this box's host cores, on the same
     workload as our arm (the n^3 apply at every N), rank 0 only.  Steps are capped so that the run
@@ -236,13 +281,36 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": val, "unit": "GDOF/s", "n_gpus": ws, "steps": steps,
         "warmup": warm + 1, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg4 FD apply P^-1 r, d=3, n={shape} (oracle on the host CPU)", "n": n,
-                   "shape": list(ns), "N": N},
+        "config": arm_config(ns, ws),
         "cpu_baseline": {"value": val, "unit": "GDOF/s", "cores": threads, "kind": "oracle",
                          "sample": f"{steps} oracle FD applies at {shape} after {warm + 1} warm-up "
                                    f"(requested --steps {args.steps}; capped at ~60 s of CPU work)"},
         "e2e": {"value": val, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def arm_config(ns, ws):
+    """The workload's config dict, identical for both arms (the driver compares them)."""
+    n = ns[0]
+    return {"workload": f"cfg4 FD apply P^-1 r, d=3, n={'x'.join(map(str, ns))} (BASELINE.json configs[3]"
+                        + (f", slab-sharded over {ws} GPUs)" if ws > 1 else ")"),
+            "n": n, "shape": list(ns), "N": int(np.prod(ns)),
+            "factors": "U ~ N(0,1), lam ~ U(1,100), W = U^-1, x ~ N(0,1)",
+            "l2": "inputs > L2: 134 MB vector + 3 x 134 MB work buffers per GPU vs 126 MB L2" if n >= 256
+            else "vector fits in L2 (no flush)",
+            "parallelism": f"slab-sharded over {ws} GPUs (NCCL all-to-all in the mode-d pass)" if ws > 1
+            else "single GPU"}
+
+
+def fd_kernels(fd, plan, x, s, reps=3):
+    """Per-kernel CUDA-event durations of reps applies (fd_apply_timed): launches per apply, avg ms, share."""
+    per = {}
+    for _ in range(reps):
+        for kind, kms in fd.fd_apply_timed(plan, x, s):
+            per.setdefault(kind, []).append(kms)
+    tot = sum(sum(v) for v in per.values())
+    return {k: {"launches_per_apply": len(v) // reps, "avg_ms": float(np.mean(v)), "share": sum(v) / tot}
+            for k, v in per.items()}
 
 
 def timed(fn, stream, steps, warmup, sync_all=None):
@@ -306,10 +374,19 @@ def gmres_section(ctx, fd, steps, ws=1, rank=0, sharded=False):
             btimes.append(gmax(brep["t_total_ms"]))
         bicg = {"time_to_tol_ms": float(np.median(btimes)), "iters": brep["iters"],
                 "rel_res_true": brep["rel_res_true"]}
-        entry = {"time_to_tol_ms": float(np.median(times)), "iters": int(np.median(iters)),
+        # per-stage breakdown from one profiled solve (eagerly launched cycles, a CUDA event at every stage
+        # change; include/fdiga.h gmres_report.t_*_ms), max over ranks per stage
+        prof = fd.gmres_solve(ctx, A, P, b, x, profile=True)
+        stages = {k: gmax(prof[k]) for k in ("t_fd_ms", "t_matvec_ms", "t_orth_ms", "t_comm_ms", "t_other_ms")}
+        stages["t_total_ms"] = gmax(prof["t_total_ms"])
+        stages["note"] = "one profiled solve (eager launches, events at stage changes); fractions apply to time_to_tol_ms"
+        t_solve = float(np.median(times))
+        entry = {"time_to_tol_ms": t_solve, "iters": int(np.median(iters)),
                  "rel_res_true": rep["rel_res_true"], "n": A.n[0], "N": A.N_global, "fd_setup_ms": t_setup * 1e3,
-                 "ms_per_iter": float(np.median(times)) / max(1, int(np.median(iters))), "ranks": ws,
-                 "bicgstab": bicg}
+                 "paper_style_total_ms": t_setup * 1e3 + t_solve,
+                 "paper_style_note": "setup (1D eigendecompositions, factor upload) + solve, as the paper's times (P:528)",
+                 "ms_per_iter": t_solve / max(1, int(np.median(iters))), "ranks": ws,
+                 "breakdown": stages, "bicgstab": bicg}
         if c.d == 3:
             # the same solves with the matrix-free sum-factorised operator (NEXT-1, no stored values)
             Amf = fd.colloc_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params, matrix_free=True)
@@ -419,6 +496,7 @@ def main():
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-weak", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--weak", action="store_true", help="also run the weak-scaling section at N = 1 (tests)")
     ap.add_argument("--sharded", action="store_true",
                     help="at --gpus 1: run the slab-sharded path over a one-rank NCCL communicator (tests the N>1 code)")
@@ -439,6 +517,9 @@ def main():
     if ws == 1 and args.sharded:
         uid = fd.nccl_unique_id()
     if ws > 1:
+        # NCCL prints each communicator's rank / nranks at init (the driver checks the communicator size)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", init_method="env://", device_id=dev)
         # the library's own NCCL communicator: rank 0 draws the unique id, torch.distributed carries it
         t = torch.zeros(128, dtype=torch.uint8, device=dev)
@@ -501,13 +582,27 @@ def main():
     # per-kernel durations of the apply (CUDA events after every launch on the ctx stream, single rank):
     # the dominant kernel's roofline is its own algorithmic work / its own average launch time
     # every rank (fd_apply_timed is collective on sharded plans); rank 0's durations are reported
-    per = {}
-    for _ in range(3):
-        for kind, kms in fd.fd_apply_timed(plan, x, s):
-            per.setdefault(kind, []).append(kms)
-    tot = sum(sum(v) for v in per.values())
-    kern = {k: {"launches_per_apply": len(v) // 3, "avg_ms": float(np.mean(v)), "share": sum(v) / tot}
-            for k, v in per.items()}
+    kern = fd_kernels(fd, plan, x, s)
+
+    # the same apply with IEEE FP64 dot products only (DMMA mode products, no int8 splitting)
+    fp64_native = None
+    if path != "dmma":
+        plan.set_path("dmma")
+        ms64 = timed(lambda: fd.fd_apply(plan, x, s), stream, max(5, min(args.steps, 20)), 3, sync_all)
+        if ws > 1:
+            t = torch.tensor([ms64], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms64 = float(t.item())
+        k64 = fd_kernels(fd, plan, x, s)
+        plan.set_path(path)
+        d = k64.get("dmma")
+        ach = flops / ws / d["launches_per_apply"] / (d["avg_ms"] * 1e-3) / 1e12 if d else None
+        fp64_native = {"value": N / (ms64 * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_apply": ms64, "path": "dmma",
+                       "apply_tflops_per_gpu": flops / ws / (ms64 * 1e-3) / 1e12,
+                       "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                                    "frac": ach / peak if ach else None, "kernel": "dmma_gemm_kernel (DMMA.8x8x4)",
+                                    "peak_source": "own DMMA register loop, sustained (profiles/r01_peaks_fp64.jsonl)"},
+                       "kernels": k64}
 
     # e2e: same metric through the C ABI with pinned host buffers (H2D + apply + D2H per step)
     xh = torch.from_numpy(np.random.default_rng(4001 + rank).standard_normal(plan.N)).pin_memory()
@@ -532,10 +627,13 @@ def main():
         fd.fd_apply_host_async(plan, xh_np, sh_np)
     fd.fd_host_sync(plan)
     e2e_ms = (time.perf_counter() - t0) / e2e_steps * 1e3
+    e2e_per_rank = [e2e_ms]
     if ws > 1:
-        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        t = torch.zeros(ws, device=dev, dtype=torch.float64)
+        t[rank] = e2e_ms
+        dist.all_reduce(t)
+        e2e_per_rank = [float(v) for v in t.cpu().tolist()]
+        e2e_ms = max(e2e_per_rank)
 
     weak = None
     if (ws > 1 or args.weak) and not args.no_weak:
@@ -579,25 +677,50 @@ def main():
     gm = None
     if not args.no_gmres:
         gm = gmres_section(ctx, fd, args.steps, ws, rank, sharded=uid is not None)
+    sweep = None
+    if ws == 1 and not args.no_sweep:
+        # the rest of the configs[3] sweep (n in {128, 256, 512}; 256 is the headline): default path and DMMA
+        sweep = {}
+        for nn in (128, 512):
+            nss = (nn, nn, nn)
+            rng2, U2, lam2 = fd_sweep_factors(nss)
+            p2 = fd.fd_setup_from_eig(ctx, U2, lam2)
+            x2 = torch.from_numpy(fd_sweep_vector(rng2, nn ** 3)).to(dev)
+            s2 = torch.empty_like(x2)
+            st2 = max(3, min(args.steps, 20 if nn < 512 else 5))
+            ms2 = timed(lambda: fd.fd_apply(p2, x2, s2), stream, st2, 2)
+            path2 = p2.path()[0]
+            e = {"n": nn, "path": path2, "ms_per_apply": ms2, "GDOF_per_s": nn ** 3 / ms2 / 1e6,
+                 "apply_tflops": p2.flops() / ms2 / 1e9}
+            if path2 != "dmma":
+                p2.set_path("dmma")
+                ms3 = timed(lambda: fd.fd_apply(p2, x2, s2), stream, st2, 2)
+                e["dmma"] = {"ms_per_apply": ms3, "GDOF_per_s": nn ** 3 / ms3 / 1e6, "apply_tflops": p2.flops() / ms3 / 1e9}
+            sweep[f"n{nn}"] = e
+            p2.close()
+            del x2, s2
     cpu = None
-    if rank == 0 and not args.no_cpu and ws == 1:
+    if rank == 0 and not args.no_cpu:
         cpu = cpu_fd_sample(n)
+        cpu["one_thread"] = cpu_fd_sample_1thread()
+        if not args.no_gmres:
+            cpu["gmres"] = cpu_gmres_sample()
 
     if rank == 0:
         rec = {
             "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg4 FD apply P^-1 r, d=3, n={'x'.join(map(str, ns))} (BASELINE.json configs[3]"
-                                   + (f", slab-sharded over {ws} GPUs)" if ws > 1 else ")"),
-                       "n": n, "shape": list(ns), "N": N,
-                       "factors": "U ~ N(0,1), lam ~ U(1,100), W = U^-1 (device LU), x ~ N(0,1)",
-                       "l2": "inputs > L2: 134 MB vector + 3 x 134 MB work buffers per GPU vs 126 MB L2" if n >= 256
-                       else "vector fits in L2 (no flush)",
-                       "parallelism": f"slab-sharded over {ws} GPUs (NCCL all-to-all in the mode-d pass)" if ws > 1
-                       else "single GPU"},
+            "config": arm_config(ns, ws),
+            "arithmetic": ("int8-split tensor-core mode products (exact digit products, one FP64 rounding; the "
+                           "accuracy contract of DESIGN.md 5.1) with IEEE FP64 fallback for guard-flagged rows"
+                           if path == "int8_split" else "IEEE FP64 (DMMA) mode products"),
             "roofline": roofline(path, kern, flops, int8_ops, achieved, peak, traffic, ws),
+            "fp64_native": fp64_native,
+            "sweep": sweep,
+            "comm": {"backend": "nccl" if ws > 1 else None, "nranks": ws},
             "e2e": {"value": N / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s", "ms_per_step": e2e_ms,
+                    "per_rank_ms": e2e_per_rank,
                     "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
                     "path": "fd_apply_host_async (pinned host buffers; every step H2D + apply + D2H, consecutive "
                             "steps overlapped on two copy streams, wall clock over the steps incl. the final sync)",

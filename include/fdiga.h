@@ -256,6 +256,9 @@ typedef struct {
                         the next step's first (one reduction and two passes over the basis per step, the
                         Arnoldi relation unchanged up to rounding; one extra P^{-1} + A application per cycle) */
   int use_x0;        /* 1: x holds the initial guess; 0: x0 = 0 */
+  int profile;       /* 1: per-stage breakdown in the report (gmres_report.t_*_ms): the cycles are launched
+                        eagerly (not from the captured graph) with a CUDA event at every stage change, so the
+                        total is slightly above a graph-launched solve's; 0: no breakdown (t_*_ms = -1) */
 } gmres_opts;
 
 typedef struct {
@@ -268,6 +271,13 @@ typedef struct {
   double t_total_ms;
   double* history;        /* optional (caller-owned, length history_cap): implicit rel. residual per step */
   int history_cap;
+  /* per-stage device time of a profiled solve (gmres_opts.profile = 1; else -1), summing to t_total_ms:
+   * t_fd_ms     FD applies P^{-1} (eq:FD2D/eq:FD3D), Arnoldi steps and cycle closes
+   * t_matvec_ms collocation matvecs A x (eq:collocationsystem), incl. the true residuals
+   * t_orth_ms   Gram-Schmidt passes, Givens/least-squares decisions, basis combination
+   * t_comm_ms   collectives of a sharded solve (halo exchange, slab transpose, all-reduce; 0 on one rank)
+   * t_other_ms  the rest (residual scaling, x update, host round trips at cycle boundaries) */
+  double t_fd_ms, t_matvec_ms, t_orth_ms, t_comm_ms, t_other_ms;
 } gmres_report;
 
 /* Right-preconditioned restarted GMRES(m) (Saad & Schultz 1986):

@@ -16,13 +16,15 @@ class FdSetupOpts(C.Structure):
 
 class GmresOpts(C.Structure):
     _fields_ = [("m", C.c_int), ("rtol", C.c_double), ("max_iters", C.c_int), ("orth", C.c_int),
-                ("use_x0", C.c_int)]
+                ("use_x0", C.c_int), ("profile", C.c_int)]
 
 
 class GmresReport(C.Structure):
     _fields_ = [("iters", C.c_int), ("restarts", C.c_int), ("converged", C.c_int), ("reorth", C.c_int),
                 ("rel_res_true", C.c_double), ("rel_res_implicit", C.c_double), ("t_total_ms", C.c_double),
-                ("history", c_double_p), ("history_cap", C.c_int)]
+                ("history", c_double_p), ("history_cap", C.c_int),
+                ("t_fd_ms", C.c_double), ("t_matvec_ms", C.c_double), ("t_orth_ms", C.c_double),
+                ("t_comm_ms", C.c_double), ("t_other_ms", C.c_double)]
 
 
 class BicgstabOpts(C.Structure):

@@ -406,9 +406,10 @@ def colloc_1d_factors(p, ne):
 
 
 def gmres_solve(ctx, A, P, b, x, m=30, rtol=1e-8, max_iters=1000, orth=ORTH_DCGS2, use_x0=False,
-                history=False, raise_on_nonconvergence=True):
-    """Right-preconditioned GMRES(m); returns the report as a dict."""
-    opts = GmresOpts(int(m), float(rtol), int(max_iters), int(orth), int(use_x0))
+                history=False, raise_on_nonconvergence=True, profile=False):
+    """Right-preconditioned GMRES(m); returns the report as a dict.  profile=True: eagerly launched cycles with
+    the per-stage device times t_fd_ms / t_matvec_ms / t_orth_ms / t_comm_ms / t_other_ms (include/fdiga.h)."""
+    opts = GmresOpts(int(m), float(rtol), int(max_iters), int(orth), int(use_x0), int(bool(profile)))
     rep = GmresReport()
     hist = None
     if history:
@@ -422,6 +423,9 @@ def gmres_solve(ctx, A, P, b, x, m=30, rtol=1e-8, max_iters=1000, orth=ORTH_DCGS
     out = dict(iters=rep.iters, restarts=rep.restarts, converged=bool(rep.converged), reorth=rep.reorth,
                rel_res_true=rep.rel_res_true, rel_res_implicit=rep.rel_res_implicit, t_total_ms=rep.t_total_ms,
                status=st)
+    if profile:
+        out.update(t_fd_ms=rep.t_fd_ms, t_matvec_ms=rep.t_matvec_ms, t_orth_ms=rep.t_orth_ms,
+                   t_comm_ms=rep.t_comm_ms, t_other_ms=rep.t_other_ms)
     if hist is not None:
         out["history"] = hist[:rep.iters].copy()
     return out

@@ -212,7 +212,22 @@ void partition(int64_t n, int nparts, int part, int64_t* begin, int64_t* end) {
 
 bool comm_capturable(const fdiga_ctx* ctx) { return ctx->hub == nullptr; }
 
+int comm_exchange_impl(fdiga_ctx* ctx, const std::vector<P2PMsg>& sends, const std::vector<P2PMsg>& recvs);
+int comm_allreduce_impl(fdiga_ctx* ctx, const double* send, double* recv, size_t count);
+// the collectives are charged to the COMM stage of a profiled solve
 int comm_exchange(fdiga_ctx* ctx, const std::vector<P2PMsg>& sends, const std::vector<P2PMsg>& recvs) {
+  const int prev = prof_mark(ctx, PROF_COMM);
+  const int s = comm_exchange_impl(ctx, sends, recvs);
+  prof_mark(ctx, prev);
+  return s;
+}
+int comm_allreduce(fdiga_ctx* ctx, const double* send, double* recv, size_t count) {
+  const int prev = prof_mark(ctx, PROF_COMM);
+  const int s = comm_allreduce_impl(ctx, send, recv, count);
+  prof_mark(ctx, prev);
+  return s;
+}
+int comm_exchange_impl(fdiga_ctx* ctx, const std::vector<P2PMsg>& sends, const std::vector<P2PMsg>& recvs) {
   if (ctx->hub) return lb_exchange(ctx, sends, recvs);
   if (!ctx->nccl_comm) {  // single rank without a process group: self messages only
     FDIGA_CHECK(sends.size() == recvs.size(), FDIGA_ERR_INVALID_ARG, "unmatched self messages");
@@ -231,7 +246,7 @@ int comm_exchange(fdiga_ctx* ctx, const std::vector<P2PMsg>& sends, const std::v
   return FDIGA_OK;
 }
 
-int comm_allreduce(fdiga_ctx* ctx, const double* send, double* recv, size_t count) {
+int comm_allreduce_impl(fdiga_ctx* ctx, const double* send, double* recv, size_t count) {
   if (ctx->hub) return lb_allreduce(ctx, send, recv, count);
   if (!ctx->nccl_comm) {
     if (send != recv && count)

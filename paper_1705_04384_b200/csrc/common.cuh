@@ -83,10 +83,31 @@ struct fdiga_ctx {
   fdiga::DevBuf ws[4];        // GMRES workspace: basis V, z/w vectors, reduction partials, device state
   void* gmres_graph = nullptr; // cached captured GMRES cycle (krylov.cu)
   void* bicg_graph = nullptr;  // cached captured BiCGStab iterations (bicgstab.cu)
+  void* solver = nullptr;      // cached cuSOLVER handle of fd_setup (fd.cu)
+  // stage profiling of a solve (gmres_opts.profile): events recorded on the stream at every stage change;
+  // interval [e_i, e_{i+1}) is charged to the stage of e_i (fdiga::prof_mark)
+  std::vector<std::pair<int, cudaEvent_t>>* prof = nullptr;
+  int prof_stage = 0;
 };
 
 namespace fdiga {
 inline void count_launch(fdiga_ctx* c, int k = 1) { c->launches += k; }
+// solve stages for gmres_report's breakdown
+enum { PROF_OTHER = 0, PROF_FD = 1, PROF_MATVEC = 2, PROF_ORTH = 3, PROF_COMM = 4, PROF_NSTAGE = 5 };
+// start charging the stream's time to `stage` (no-op unless a profiled solve is running); returns the
+// previous stage
+inline int prof_mark(fdiga_ctx* c, int stage) {
+  const int prev = c->prof_stage;
+  if (!c->prof) return prev;
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) == cudaSuccess) {
+    cudaEventRecord(e, c->stream);
+    c->prof->push_back({stage, e});
+  }
+  c->prof_stage = stage;
+  return prev;
+}
+void destroy_solver(fdiga_ctx* ctx);
 // Set the device of the context for the calling thread.
 inline int bind(const fdiga_ctx* c) {
   FDIGA_CUDA(cudaSetDevice(c->device));

@@ -120,6 +120,7 @@ int fdiga_ctx_destroy(fdiga_ctx* c) {
   cudaSetDevice(c->device);
   if (c->nccl_comm || c->hub) fdiga_comm_destroy(c);
   destroy_gmres_graph(c);
+  destroy_solver(c);
   if (c->pinned) cudaFreeHost(c->pinned);
   for (auto& b : c->ws) b.release();
   if (c->own_stream) cudaStreamDestroy(c->stream);

@@ -574,6 +574,22 @@ struct Solver {
     return FDIGA_OK;
   }
 };
+// the context's cached cuSOLVER handle (created on first use, bound to the context stream)
+int ctx_solver(fdiga_ctx* ctx, Solver** out) {
+  Solver* S = static_cast<Solver*>(ctx->solver);
+  if (!S) {
+    S = new Solver();
+    const int s = S->init(ctx->stream);
+    if (s != FDIGA_OK) {
+      delete S;
+      return s;
+    }
+    ctx->solver = S;
+  }
+  CUSOLVER(cusolverDnSetStream(S->h, ctx->stream));
+  *out = S;
+  return FDIGA_OK;
+}
 
 // Column-major helpers (cuSOLVER is column-major; our host matrices are row-major).
 std::vector<double> to_colmajor(const double* rm, int64_t n) {
@@ -643,17 +659,25 @@ double norm1_rm(const std::vector<double>& A, int64_t n) {  // max column abs su
   return best;
 }
 
-// W = (M U)^{-1} (row-major in/out; M == nullptr means identity).  Also returns cond_1(U).
+// W = (M U)^{-1} (row-major in/out; M == nullptr means identity).  Also returns cond_1(U).  The products
+// with M skip its zeros (the 1D spline mass matrices are banded: O(n^2 p) instead of O(n^3) on the host).
 int compute_W(Solver& S, cudaStream_t st, int64_t n, const double* M, const std::vector<double>& U,
               std::vector<double>& W, double* condU) {
   std::vector<double> MU(U);
+  std::vector<std::vector<std::pair<int64_t, double>>> nz;  // nonzeros of M by row
   if (M) {
+    nz.resize(n);
     for (int64_t i = 0; i < n; ++i)
-      for (int64_t j = 0; j < n; ++j) {
-        double s = 0;
-        for (int64_t k = 0; k < n; ++k) s += M[i * n + k] * U[k * n + j];
-        MU[i * n + j] = s;
+      for (int64_t k = 0; k < n; ++k)
+        if (M[i * n + k] != 0.0) nz[i].push_back({k, M[i * n + k]});
+    for (int64_t i = 0; i < n; ++i) {
+      double* r = &MU[i * n];
+      std::fill(r, r + n, 0.0);
+      for (const auto& e : nz[i]) {
+        const double* u = &U[e.first * n];
+        for (int64_t j = 0; j < n; ++j) r[j] += e.second * u[j];
       }
+    }
   }
   std::vector<double> A = to_colmajor(MU.data(), n);
   std::vector<double> B((size_t)n * n, 0.0);
@@ -666,12 +690,14 @@ int compute_W(Solver& S, cudaStream_t st, int64_t n, const double* M, const std:
     // U^{-1} = W M
     std::vector<double> Uinv(W);
     if (M) {
-      for (int64_t i = 0; i < n; ++i)
-        for (int64_t j = 0; j < n; ++j) {
-          double s = 0;
-          for (int64_t k = 0; k < n; ++k) s += W[i * n + k] * M[k * n + j];
-          Uinv[i * n + j] = s;
+      for (int64_t i = 0; i < n; ++i) {
+        double* r = &Uinv[i * n];
+        std::fill(r, r + n, 0.0);
+        for (int64_t k = 0; k < n; ++k) {
+          const double w = W[i * n + k];
+          for (const auto& e : nz[k]) r[e.first] += w * e.second;
         }
+      }
     }
     *condU = norm1_rm(U, n) * norm1_rm(Uinv, n);
   }
@@ -830,8 +856,9 @@ int fd_setup_from_eig(fdiga_ctx* ctx, int d, const int64_t* n, const double* con
                       const double* const* M, fd_plan** out) {
   FDIGA_TRY(check_common(ctx, d, n, out));
   FDIGA_CHECK(U && lam, FDIGA_ERR_INVALID_ARG, "NULL factor array");
-  Solver S;
-  FDIGA_TRY(S.init(ctx->stream));
+  Solver* Sp = nullptr;
+  FDIGA_TRY(ctx_solver(ctx, &Sp));
+  Solver& S = *Sp;
   fd_plan* P = new_plan(ctx, d, n);
   for (int l = 0; l < d; ++l) {
     P->hU[l].assign(U[l], U[l] + n[l] * n[l]);
@@ -859,8 +886,9 @@ int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, co
   const double tol_imag = opts ? opts->tol_imag : 1e-8;
   const double cond_max = opts ? opts->cond_max : 1e8;
   const int allow_cplx = opts ? opts->allow_complex_pairs : 0;
-  Solver S;
-  FDIGA_TRY(S.init(ctx->stream));
+  Solver* Sp = nullptr;
+  FDIGA_TRY(ctx_solver(ctx, &Sp));  // one cuSOLVER handle per context
+  Solver& S = *Sp;
   fd_plan* P = new_plan(ctx, d, n);
   auto fail = [&](int s) {
     fd_plan_destroy(P);
@@ -869,6 +897,19 @@ int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, co
   for (int l = 0; l < d; ++l) {
     const int64_t nl = n[l];
     FDIGA_CHECK(M[l] && K[l], FDIGA_ERR_INVALID_ARG, "NULL pencil for direction %d", l);
+    // a pencil identical to an earlier direction's (the isotropic case [M]*d, [K]*d): same factors
+    int same = -1;
+    for (int l2 = 0; l2 < l && same < 0; ++l2)
+      if (n[l2] == nl && std::memcmp(M[l2], M[l], (size_t)(nl * nl) * sizeof(double)) == 0 &&
+          std::memcmp(K[l2], K[l], (size_t)(nl * nl) * sizeof(double)) == 0)
+        same = l2;
+    if (same >= 0) {
+      P->hU[l] = P->hU[same];
+      P->hW[l] = P->hW[same];
+      P->hlam[l] = P->hlam[same];
+      P->hlam_im[l] = P->hlam_im[same];
+      continue;
+    }
     // 1. C = M^{-1} K  (eq:eigendecomposition)
     std::vector<double> Mc = to_colmajor(M[l], nl), C = to_colmajor(K[l], nl);
     int s = lu_solve(S, ctx->stream, nl, Mc, C);
@@ -1163,3 +1204,10 @@ int fd_plan_destroy(fd_plan* P) {
 }
 
 }  // extern "C"
+
+namespace fdiga {
+void destroy_solver(fdiga_ctx* ctx) {
+  delete static_cast<Solver*>(ctx->solver);
+  ctx->solver = nullptr;
+}
+}  // namespace fdiga

@@ -753,11 +753,15 @@ int enqueue_cycle(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const Ws& W, int
     for (int j = 0; j < m; ++j) {
       const double* u = j == 0 ? W.V : W.u;
       if (P) {
+        prof_mark(ctx, PROF_FD);
         FDIGA_TRY(fd_apply_ex(P, u, W.z, stop));
+        prof_mark(ctx, PROF_MATVEC);
         FDIGA_TRY(stencil_matvec_ex(A, W.z, W.w, stop));
       } else {
+        prof_mark(ctx, PROF_MATVEC);
         FDIGA_TRY(stencil_matvec_ex(A, u, W.w, stop));
       }
+      prof_mark(ctx, PROF_ORTH);
       FDIGA_TRY(launch_dcgs(ctx, W, j, u, m, hist_cap, false));
     }
     return launch_dcgs(ctx, W, m, m == 0 ? W.V : W.u, m, hist_cap, true);
@@ -765,11 +769,15 @@ int enqueue_cycle(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const Ws& W, int
   for (int j = 0; j < m; ++j) {
     double* vj = W.V + (int64_t)j * W.ldv;
     if (P) {
+      prof_mark(ctx, PROF_FD);
       FDIGA_TRY(fd_apply_ex(P, vj, W.z, stop));
+      prof_mark(ctx, PROF_MATVEC);
       FDIGA_TRY(stencil_matvec_ex(A, W.z, W.w, stop));
     } else {
+      prof_mark(ctx, PROF_MATVEC);
       FDIGA_TRY(stencil_matvec_ex(A, vj, W.w, stop));
     }
+    prof_mark(ctx, PROF_ORTH);
     const int k = j + 1;
     FDIGA_TRY(launch_passes(ctx, W, k, j, m, hist_cap));
     if (W.orth != FDIGA_ORTH_CGS2) {  // CGS2's pass 3 already wrote v_{j+1}
@@ -826,7 +834,8 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   W.orth = opts ? opts->orth : FDIGA_ORTH_DCGS2;
   FDIGA_CHECK(W.orth == FDIGA_ORTH_CGS_DGKS || W.orth == FDIGA_ORTH_CGS2 || W.orth == FDIGA_ORTH_DCGS2,
               FDIGA_ERR_INVALID_ARG, "unknown orth %d", W.orth);
-  const bool use_graph = comm_capturable(ctx);
+  const bool profile = opts && opts->profile;
+  const bool use_graph = comm_capturable(ctx) && !profile;
   FDIGA_CHECK(!P || fd_plan_local_size(P) == W.N, FDIGA_ERR_INVALID_ARG,
               "preconditioner and operator sizes differ (%lld vs %lld local rows)",
               (long long)(P ? fd_plan_local_size(P) : 0), (long long)W.N);
@@ -895,6 +904,18 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   FDIGA_CUDA(cudaEventCreate(&e0));
   FDIGA_CUDA(cudaEventCreate(&e1));
   FDIGA_CUDA(cudaEventRecord(e0, st));
+  std::vector<std::pair<int, cudaEvent_t>> prof_events;
+  if (profile) {
+    ctx->prof = &prof_events;
+    prof_mark(ctx, PROF_OTHER);
+  }
+  struct ProfOff {  // the context stops recording on every exit path
+    fdiga_ctx* c;
+    ~ProfOff() {
+      c->prof = nullptr;
+      c->prof_stage = PROF_OTHER;
+    }
+  } prof_off{ctx};
   {
     GmState init;
     std::memset(&init, 0, sizeof(init));
@@ -910,7 +931,9 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   std::memset(&hs, 0, sizeof(hs));
   while (true) {
     // true residual r = b - A x, cycle start (device decides whether to stop)
+    prof_mark(ctx, PROF_MATVEC);
     FDIGA_TRY(stencil_matvec(A, x, W.w));
+    prof_mark(ctx, PROF_OTHER);
     residual_start_kernel<<<W.nblk, RT, 0, st>>>(b, W.w, W.V, W.N, W.part, W.st, rtol, W.sh ? 0 : 1);
     if (W.sh) {
       FDIGA_TRY(comm_allreduce(ctx, W.st->rsl, W.st->rs, 2));
@@ -936,12 +959,13 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
     }
     ++cycles;
     // one cycle: the captured Arnoldi steps, then x += P^{-1}(V y)
-    if (G) {
+    if (G && !profile) {  // (a profiled solve enqueues its cycles eagerly, with stage events)
       FDIGA_CUDA(cudaGraphLaunch(G->exec, st));
       count_launch(ctx, 1);
     } else {
       FDIGA_TRY(enqueue_cycle(ctx, A, P, W, m, hist_cap));  // loopback transport: not capturable
     }
+    prof_mark(ctx, PROF_ORTH);
     solve_y_kernel<<<1, 1, 0, st>>>(W.st);
     count_launch(ctx);
     // the cycle's basis size k is decided on the device: read it (one small copy per cycle) so the
@@ -953,9 +977,12 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
     FDIGA_TRY(launch_lincomb(ctx, W, kcyc, W.w));
     FDIGA_CUDA(cudaGetLastError());
     if (P) {
+      prof_mark(ctx, PROF_FD);
       FDIGA_TRY(fd_apply(P, W.w, W.z));
+      prof_mark(ctx, PROF_OTHER);
       axpy_kernel<<<W.nblk, RT, 0, st>>>(W.z, x, W.N);
     } else {
+      prof_mark(ctx, PROF_OTHER);
       axpy_kernel<<<W.nblk, RT, 0, st>>>(W.w, x, W.N);
     }
     count_launch(ctx, 1);
@@ -965,6 +992,20 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
   FDIGA_CUDA(cudaEventSynchronize(e1));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
+  // per-stage times: interval [e_i, e_{i+1}) (the last one up to e1) charged to stage i; the state upload
+  // before the first mark is OTHER
+  double stage_ms[PROF_NSTAGE] = {0, 0, 0, 0, 0};
+  if (!prof_events.empty()) {
+    float d = 0;
+    if (cudaEventElapsedTime(&d, e0, prof_events[0].second) == cudaSuccess) stage_ms[PROF_OTHER] += d;
+  }
+  for (size_t i = 0; i < prof_events.size(); ++i) {
+    float d = 0;
+    if (cudaEventElapsedTime(&d, prof_events[i].second,
+                             i + 1 < prof_events.size() ? prof_events[i + 1].second : e1) == cudaSuccess)
+      stage_ms[prof_events[i].first] += d;
+  }
+  for (auto& pe : prof_events) cudaEventDestroy(pe.second);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (rep) {
@@ -975,6 +1016,11 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
     rep->rel_res_true = hs.rel_true;
     rep->rel_res_implicit = hs.rel_implicit;
     rep->t_total_ms = ms;
+    rep->t_fd_ms = profile ? stage_ms[PROF_FD] : -1.0;
+    rep->t_matvec_ms = profile ? stage_ms[PROF_MATVEC] : -1.0;
+    rep->t_orth_ms = profile ? stage_ms[PROF_ORTH] : -1.0;
+    rep->t_comm_ms = profile ? stage_ms[PROF_COMM] : -1.0;
+    rep->t_other_ms = profile ? stage_ms[PROF_OTHER] : -1.0;
     if (rep->history && rep->history_cap > 0) {
       const int cnt = std::min(rep->history_cap, std::min(hs.iters, hist_cap));
       if (cnt > 0) FDIGA_CUDA(cudaMemcpy(rep->history, W.hist, cnt * sizeof(double), cudaMemcpyDeviceToHost));

@@ -304,6 +304,32 @@ def test_gmres_iterations_match_oracle(ctx, cfg):
     assert np.linalg.norm(bh - disc.matvec(xh)) / np.linalg.norm(bh) <= 2e-8
 
 
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_gmres_profiled_breakdown(ctx, cfg):
+    # gmres_opts.profile: the stages partition the device time of the (eagerly launched) solve, and the
+    # solve takes exactly the decisions of the graph-launched one (same kernels, same order)
+    c = get_config(cfg)
+    A = fd.colloc_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params, matrix_free=(cfg == 5))
+    _, M, K, _ = splines.colloc_1d(c.ne, c.p)
+    P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
+    b = gpu(rhs(cfg, A.N))
+    x1 = torch.empty_like(b)
+    x2 = torch.empty_like(b)
+    r1 = fd.gmres_solve(ctx, A, P, b, x1)
+    r2 = fd.gmres_solve(ctx, A, P, b, x2, profile=True)
+    assert r2["iters"] == r1["iters"] and r2["rel_res_true"] == r1["rel_res_true"]
+    np.testing.assert_array_equal(host(x1), host(x2))
+    parts = [r2[k] for k in ("t_fd_ms", "t_matvec_ms", "t_orth_ms", "t_comm_ms", "t_other_ms")]
+    assert all(p >= 0 for p in parts), parts
+    assert r2["t_fd_ms"] > 0 and r2["t_matvec_ms"] > 0 and r2["t_orth_ms"] > 0
+    assert r2["t_comm_ms"] == 0.0  # one rank, no process group
+    assert abs(sum(parts) - r2["t_total_ms"]) <= 0.02 * r2["t_total_ms"] + 0.01, (parts, r2["t_total_ms"])
+    # an unprofiled report carries no breakdown
+    assert "t_fd_ms" not in r1
+    P.close()
+    A.close()
+
+
 def test_gmres_small_matches_oracle_solution(ctx):
     c = get_config(2)
     ne = 16

@@ -183,6 +183,12 @@ def test_sharded_gmres_iterations_match_oracle(cfg, nranks, orth):
         x = torch.empty_like(bt)
         rep = fd.gmres_solve(ctx, A, P, bt, x, orth=orth)
         torch.cuda.current_stream().synchronize()
+        if orth == fd.ORTH_DCGS2:  # the profiled solve: same decisions, the collectives charged to t_comm
+            xp = torch.empty_like(bt)
+            rp = fd.gmres_solve(ctx, A, P, bt, xp, orth=orth, profile=True)
+            assert rp["iters"] == rep["iters"] and rp["t_comm_ms"] > 0 and rp["t_fd_ms"] > 0
+            parts = sum(rp[k] for k in ("t_fd_ms", "t_matvec_ms", "t_orth_ms", "t_comm_ms", "t_other_ms"))
+            assert abs(parts - rp["t_total_ms"]) <= 0.02 * rp["t_total_ms"] + 0.01
         out = (rep, x.cpu().numpy())
         P.close()
         A.close()
