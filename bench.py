@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FD-apply GDOF/s (FP64, 3D) & preconditioned GMRES time-to-1e-8 at 1/2/4/8 B200"
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_peaks_fp64.jsonl")
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_summary.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02_ncu_summary.json")
 
 
 def fp64_peak():
@@ -354,9 +354,15 @@ def gmres_section(ctx, fd, steps, ws=1, rank=0, sharded=False):
         c = get_config(cfg)
         A = fd.colloc_assemble(ctx, c.d, c.p, c.ne, c.geometry, c.geo_params)
         M, K = fd.colloc_1d_factors(c.p, c.ne)
-        t0 = time.perf_counter()
-        P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
-        t_setup = time.perf_counter() - t0
+        # setup timed three times (the first one in a process also pays cuSOLVER's one-time initialisation)
+        setups = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            P = fd.fd_setup(ctx, [M] * c.d, [K] * c.d)
+            setups.append(time.perf_counter() - t0)
+            if len(setups) < 3:
+                P.close()
+        t_setup = float(np.median(setups))
         lo = A.slab[0] * A.n[0] * A.n[1]
         b = torch.from_numpy(rhs(cfg, A.N_global)[lo:lo + A.N].copy()).to(dev)
         x = torch.empty_like(b)
@@ -383,6 +389,7 @@ def gmres_section(ctx, fd, steps, ws=1, rank=0, sharded=False):
         t_solve = float(np.median(times))
         entry = {"time_to_tol_ms": t_solve, "iters": int(np.median(iters)),
                  "rel_res_true": rep["rel_res_true"], "n": A.n[0], "N": A.N_global, "fd_setup_ms": t_setup * 1e3,
+                 "fd_setup_first_ms": setups[0] * 1e3,
                  "paper_style_total_ms": t_setup * 1e3 + t_solve,
                  "paper_style_note": "setup (1D eigendecompositions, factor upload) + solve, as the paper's times (P:528)",
                  "ms_per_iter": t_solve / max(1, int(np.median(iters))), "ranks": ws,

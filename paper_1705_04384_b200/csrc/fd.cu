@@ -11,6 +11,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -886,6 +887,10 @@ int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, co
   const double tol_imag = opts ? opts->tol_imag : 1e-8;
   const double cond_max = opts ? opts->cond_max : 1e8;
   const int allow_cplx = opts ? opts->allow_complex_pairs : 0;
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  double t_lu = 0, t_geev = 0, t_w = 0;  // FDIGA_VERBOSE: setup phase times (ms)
+  auto since = [](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
   Solver* Sp = nullptr;
   FDIGA_TRY(ctx_solver(ctx, &Sp));  // one cuSOLVER handle per context
   Solver& S = *Sp;
@@ -911,9 +916,12 @@ int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, co
       continue;
     }
     // 1. C = M^{-1} K  (eq:eigendecomposition)
+    auto t0 = clk::now();
     std::vector<double> Mc = to_colmajor(M[l], nl), C = to_colmajor(K[l], nl);
     int s = lu_solve(S, ctx->stream, nl, Mc, C);
     if (s) return fail(s);
+    t_lu += since(t0);
+    t0 = clk::now();
     // 2. eigenpairs of C (cuSOLVER Xgeev; real input -> complex eigenvalues, real packed VR)
     double *dC = nullptr, *dVR = nullptr, *dVL = nullptr;
     cuDoubleComplex* dWv = nullptr;
@@ -953,6 +961,8 @@ int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, co
       set_error("cusolverDnXgeev failed (status %d, info %d)", (int)cs, hinfo);
       return fail(FDIGA_ERR_CUSOLVER);
     }
+    t_geev += since(t0);
+    t0 = clk::now();
     // 3. reality guard (Remark 1), sort ascending, unit 2-norm columns
     double rho = 0, maxim = 0;
     for (auto& z : ev) {
@@ -1020,6 +1030,7 @@ int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, co
     double condU = 0;
     s = compute_W(S, ctx->stream, nl, M[l], Ul, P->hW[l], &condU);
     if (s) return fail(s);
+    t_w += since(t0);
     if (!(condU <= cond_max)) {
       set_error("ill-conditioned eigenvector matrix in direction %d: cond_1(U) = %g", l, condU);
       return fail(FDIGA_ERR_ILL_CONDITIONED);
@@ -1028,8 +1039,12 @@ int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, co
     P->hlam[l] = std::move(laml);
     P->hlam_im[l] = std::move(laml_im);
   }
+  const auto t_fin = clk::now();
   int s = finish_plan(P);
   if (s != FDIGA_OK) return fail(s);
+  if (getenv("FDIGA_VERBOSE"))
+    fprintf(stderr, "[fdiga] fd_setup: %.1f ms (LU %.1f, geev %.1f, W %.1f, factors/autotune %.1f)\n",
+            since(t_start), t_lu, t_geev, t_w, since(t_fin));
   *out = P;
   return FDIGA_OK;
 }
