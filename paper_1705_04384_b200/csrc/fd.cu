@@ -423,16 +423,50 @@ int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* Fs, const doub
   return mark(P, 2);
 }
 
+// Single-rank mode products with plane-transposed intermediates (every split a row split but two, every
+// GEMM store coalesced; the mode products commute, so the backward pass may run 3, 1, 2):
+//   t = 0: X[i3][j][k] (k contiguous, K = n_k), data rows (i3, j), output Y[i3][f][j] (the plane transposed)
+//   t = 1: the same contraction, output Y[i3][f][j] ... written as Y[i3][f][j] with j the row's inner index
+// Both are "contract the contiguous axis of each i3 plane and store the plane transposed": with
+// X = x[i3][i2][i1] (k = i1) the result is y[i3][f1][i2]; applied again (k = i2) it gives z[i3][f2][f1], the
+// natural layout.  (Row-contiguous stores of a pair tile's outputs -- the natural mode-1 layout -- touch 32
+// rows per warp store and cost ~35 us more per product at n = 256.)
+int oz_mode_t(fd_plan* P, int l, const OzOperand& Fz, const double* Fs, const double* X, double* Y, const int* skip) {
+  const int64_t nk = P->n[l], nj = P->n[1 - l];  // contracted axis and the other in-plane axis
+  const int64_t c = P->e - P->o;
+  OzOperand& Xz = P->ozX[l];
+  cudaStream_t st = P->ctx->stream;
+  OzGemmArgs g{};
+  g.X = &Xz;
+  g.F = &Fz;
+  g.K = nk;
+  g.y = Y;
+  g.skip = skip;
+  g.xs = X;
+  g.fs = Fs;
+  g.ldf = P->ld[l];
+  if (Xz.rows == 0) return FDIGA_OK;
+  FDIGA_TRY(oz_split(P->ctx, st, X, nj * c, nk, 1, nk, Xz, skip));
+  g.inner = nj;          // row m = (i3, j): b = m / nj, j = m % nj
+  g.bstride = nk * nj;   // one plane
+  g.mstride = 1;         // j contiguous in the output plane
+  g.fstride = nj;        // output row f of the plane
+  g.xs_b = nk * nj, g.xs_i = nk, g.xs_k = 1;
+  FDIGA_TRY(mark(P, 1));
+  FDIGA_TRY(oz_gemm(P->ctx, st, g));
+  return mark(P, 2);
+}
+
 int fd_apply_oz(fd_plan* P, const double* r, double* s, const int* skip) {
   double* a = P->t0.p;
   double* b = P->t1.p;
-  FDIGA_TRY(oz_mode(P, 0, P->ozW[0], P->W[0], r, a, skip));
-  FDIGA_TRY(oz_mode(P, 1, P->ozW[1], P->W[1], a, b, skip));
+  FDIGA_TRY(oz_mode_t(P, 0, P->ozW[0], P->W[0], r, a, skip));  // a = [i3][f1][i2]
+  FDIGA_TRY(oz_mode_t(P, 1, P->ozW[1], P->W[1], a, b, skip));  // b = [i3][f2][f1]
   // the Lambda divide rides in the split that feeds the backward mode-3 product
   FDIGA_TRY(oz_mode(P, 2, P->ozW[2], P->W[2], b, a, skip));
   FDIGA_TRY(oz_mode(P, 2, P->ozU[2], P->U[2], a, b, skip, true));
-  FDIGA_TRY(oz_mode(P, 1, P->ozU[1], P->U[1], b, a, skip));
-  return oz_mode(P, 0, P->ozU[0], P->U[0], a, s, skip);
+  FDIGA_TRY(oz_mode_t(P, 0, P->ozU[0], P->U[0], b, a, skip));  // a = [i3][f1][i2]
+  return oz_mode_t(P, 1, P->ozU[1], P->U[1], a, s, skip);      // s = [i3][i2][i1]
 }
 
 int finish_plan(fd_plan* P) {

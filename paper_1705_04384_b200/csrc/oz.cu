@@ -174,11 +174,14 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
   }
 }
 
-// inner > 1: the contracted index k is strided; rows m = b inner + i.  A block stages a K x 32 tile
-// (coalesced over i), takes the column maxima, and writes the digit rows k-contiguous (transposed).
-// CW = 16 columns i per block (a K x 16 tile: 32 KB at K = 256, six blocks per SM; the launch site records
-// the measured alternatives).  Lane l of a warp covers column l % CW of rows k = l / CW (mod 32 / CW).
-template <int CW>
+// inner > 1: the contracted index k is strided; rows m = b inner + i.  A block stages a K x 16 tile
+// (16 columns i, coalesced 128-byte rows), takes the column statistics, and writes the digit rows
+// k-contiguous (transposed).  Column i of row k is stored at i ^ ((k / 8) mod 16): conflict-free both for the
+// row-wise staging (lanes = i) and for the digit pass (lanes = 8-row chunks c of one column).  The loops
+// step pointers and swizzle terms incrementally and the digit pass maps thread t to column t / 16 and the
+// chunks c = t mod 16 (+ 16, ..): no integer division or 64-bit multiply per element (an earlier version
+// was issue-bound on address arithmetic: 3.5 warp instructions per element).
+constexpr int OZ_CW = 16;
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __restrict__ x, int64_t batch, int K,
                                                             int64_t inner, int8_t* __restrict__ digits,
                                                             int32_t* __restrict__ exps, int32_t* __restrict__ wide,
@@ -186,52 +189,53 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
                                                             const double* __restrict__ lam_row,
                                                             const double* __restrict__ lam_k, const int* skip) {
   if (skip && *skip) return;
-  constexpr int RPW = 32 / CW;  // rows per warp instruction
-  // [K][CW] tile, column i of row k stored at i ^ ((k / 8) mod CW): conflict-free both for the row-wise
-  // staging (lanes = i) and for the digit pass (lanes = 8-row chunks c of one column i)
+  constexpr int CW = OZ_CW, RG = 256 / CW;  // 16 columns, 16 row groups
   extern __shared__ double tile[];
-  __shared__ double pmax[8 * RPW][CW], pmin[8 * RPW][CW];
-  __shared__ int pnf[CW];
+  __shared__ double pmax[RG][CW], pmin[RG][CW];
+  __shared__ int pnf[RG][CW];
   __shared__ int es[CW];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int col = lane % CW, rsub = lane / CW;
+  const int col = threadIdx.x % CW, rg = threadIdx.x / CW;
   const int64_t tiles_i = (inner + CW - 1) / CW;
   const int64_t b = blockIdx.x / tiles_i;
-  const int64_t i0 = (blockIdx.x % tiles_i) * CW;
-  const double* xb = x + b * K * inner;
-  RowStat st;
+  const int64_t i0 = (blockIdx.x - b * tiles_i) * CW;
   const bool iv = i0 + col < inner;
-  if (threadIdx.x < CW) pnf[threadIdx.x] = 0;
-  // the whole K x CW tile in flight at once: 8-byte cp.async (zero-filled outside [0, inner)), no registers
-  for (int k = warp * RPW + rsub; k < K; k += 8 * RPW)
-    cp_async8(smem_u32(&tile[k * CW + (col ^ ((k >> 3) & (CW - 1)))]),
-              iv ? xb + (int64_t)k * inner + i0 + col : xb, iv ? 8 : 0);
-  cp_async_commit();
-  cp_async_wait<0>();
-  // each thread revisits only the elements it copied itself: no barrier needed before this pass
-  // the eigenvalue-sum divide of the FD (eq:FD3D) when the split feeds the backward mode-d product
-  const double lr = (lam_row && iv) ? lam_row[b * inner + i0 + col] : 0.0;
-  for (int k = warp * RPW + rsub; k < K; k += 8 * RPW) {
-    double* tp = &tile[k * CW + (col ^ ((k >> 3) & (CW - 1)))];
-    double val = *tp;
-    if (lam_row) {  // val / (lr + lam_k[k]) (< 1 ulp off), all on the FP64 pipe
-      val *= rcp_fp64(lr + lam_k[k]);
-      *tp = val;
-    }
-    st.add(val);
+  // ---- stage the K x 16 tile: thread (col, rg) copies rows k = rg, rg + 16, .. of its column
+  {
+    const double* src = x + b * K * inner + (int64_t)rg * inner + i0 + col;
+    const int64_t step = RG * inner;
+    uint32_t dst = smem_u32(tile) + 8u * (uint32_t)(rg * CW);
+    for (int k = rg; k < K; k += RG, src += step, dst += 8u * RG * CW)
+      cp_async8(dst + 8u * (uint32_t)(col ^ ((k >> 3) & (CW - 1))), iv ? src : x, iv ? 8 : 0);
+    cp_async_commit();
+    cp_async_wait<0>();
   }
-  pmax[warp * RPW + rsub][col] = st.mx;
-  pmin[warp * RPW + rsub][col] = st.mn;
-  __syncthreads();  // (also orders the pnf reset above before the flags below)
-  if (st.nf) atomicOr(&pnf[col], 1);
+  // ---- column statistics over the elements this thread copied (no barrier needed); the eigenvalue-sum
+  // divide of the FD (eq:FD3D) when the split feeds the backward mode-d product
+  RowStat st;
+  {
+    const double lr = (lam_row && iv) ? lam_row[b * inner + i0 + col] : 0.0;
+    double* tp = tile + rg * CW;
+    for (int k = rg; k < K; k += RG, tp += RG * CW) {
+      double* e = tp + (col ^ ((k >> 3) & (CW - 1)));
+      double val = *e;
+      if (lam_row) {  // val / (lr + lam_k[k]) (< 1 ulp off), all on the FP64 pipe
+        val *= rcp_fp64(lr + lam_k[k]);
+        *e = val;
+      }
+      st.add(val);
+    }
+  }
+  pmax[rg][col] = st.mx;
+  pmin[rg][col] = st.mn;
+  pnf[rg][col] = st.nf ? 1 : 0;
   __syncthreads();
   if (threadIdx.x < CW) {
     RowStat r;
-    r.nf = pnf[threadIdx.x] != 0;
 #pragma unroll
-    for (int w = 0; w < 8 * RPW; ++w) {
+    for (int w = 0; w < RG; ++w) {
       r.mx = fmax(r.mx, pmax[w][threadIdx.x]);
       r.mn = fmin(r.mn, pmin[w][threadIdx.x]);
+      r.nf |= pnf[w][threadIdx.x] != 0;
     }
     const int e = row_exponent(r.mx);
     es[threadIdx.x] = e;
@@ -242,22 +246,23 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
     }
   }
   __syncthreads();
-  const int cpr = kp / 8;  // 8-byte chunks per digit row
-  for (int item = threadIdx.x; item < CW * cpr; item += 256) {
-    const int i = item / cpr, c = item % cpr;
-    if (i0 + i >= inner) continue;
+  // ---- digits: thread (i = t / 16, chunks c = t mod 16, + 16, ..) of 8 k values each
+  const int i = threadIdx.x / 16, cq = threadIdx.x % 16;
+  if (i0 + i >= inner) return;
+  const int e = es[i];
+  const int64_t plane = rows_p * (int64_t)kp;
+  int8_t* drow = digits + (b * inner + i0 + i) * (int64_t)kp;
+  const int cpr = kp / 8;
+  for (int c = cq; c < cpr; c += 16) {
+    const double* tc = tile + (8 * c) * CW + (i ^ (c & (CW - 1)));
     double v[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int k = c * 8 + j;
-      v[j] = k < K ? tile[k * CW + (i ^ ((k >> 3) & (CW - 1)))] : 0.0;
-    }
+    for (int j = 0; j < 8; ++j) v[j] = (8 * c + j < K) ? tc[j * CW] : 0.0;
     uint64_t w[OZ_S];
-    split8(v, es[i], w);
-    const int64_t m = b * inner + i0 + i;
+    split8(v, e, w);
+    int8_t* dp = drow + 8 * c;
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s)
-      *reinterpret_cast<uint64_t*>(digits + ((int64_t)s * rows_p + m) * kp + c * 8) = w[s];
+    for (int s2 = 0; s2 < OZ_S; ++s2, dp += plane) *reinterpret_cast<uint64_t*>(dp) = w[s2];
   }
 }
 
@@ -423,7 +428,34 @@ __device__ void oz_cta_fixup(const OzKernelArgs& a, int mt_first, int per_nt, ui
     const double lr = a.lam_row ? a.lam_row[m] : 0.0;
     for (int k = threadIdx.x; k < a.K; k += OZ_EW * 32) sv[k] = oz_x(a, xr, lr, k);
     oz_bar_epi();
-    for (int h = 0; h < OZ_BN; h += 32) oz_fix_item(a, m, n0 + h + c, true, sv, part, c, sl);
+    // all OZ_BN outputs of the row at once: thread (c, sl) sums k = sl, sl + OZ_EW, .. for the columns
+    // c, c + 32, .. (independent loads in flight), then the OZ_EW partial sums per output in a fixed order
+    constexpr int NQ = OZ_BN / 32;
+    double acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+    const double* ftc = a.ft + n0 + c;
+#pragma unroll 4
+    for (int k = sl; k < a.K; k += OZ_EW) {
+      const double xv = sv[k];
+      const double* fk = ftc + (int64_t)k * a.Nf;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (n0 + c + 32 * q < a.Nf) acc[q] = fma(fk[32 * q], xv, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) part[sl * OZ_BN + 32 * q + c] = acc[q];
+    oz_bar_epi();
+    if (threadIdx.x < OZ_BN) {
+      const int64_t f = n0 + threadIdx.x;
+      if (f < a.Nf) {
+        double t = part[threadIdx.x];
+#pragma unroll
+        for (int q = 1; q < OZ_EW; ++q) t += part[q * OZ_BN + threadIdx.x];
+        a.y[oz_out_off(a, m) + f * a.fstride] = t;
+      }
+    }
+    oz_bar_epi();
   }
   for (int i = 0; i < nf; ++i) {
     const int64_t f = a.fw[2 + i];
@@ -503,7 +535,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
   uint64_t* sempty = sfull + OZ_NSLOT;  // [4] accumulator slot drained by both CTAs (leader)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_NSLOT);
   double* sSF = reinterpret_cast<double*>(sempty + OZ_NSLOT + 2);  // 2^(e_f - WSHIFT) of the pair's factor rows
-  double* sFix = reinterpret_cast<double*>(sX);  // fixup scratch after the last tile: [OZ_MAXKP] + [OZ_EW][32]
+  double* sFix = reinterpret_cast<double*>(sX);  // fixup scratch after the last tile: [OZ_MAXKP] + [OZ_EW][OZ_BN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -747,7 +779,7 @@ constexpr size_t oz_smem_bytes() {
          OZ_BN * sizeof(double);
 }
 static_assert(oz_smem_bytes() <= 227 * 1024, "shared memory per CTA");
-static_assert((OZ_MAXKP + OZ_EW * 32) * sizeof(double) <= (size_t)OZ_NXS * OZ_XPL, "fixup scratch in the data ring");
+static_assert((OZ_MAXKP + OZ_EW * OZ_BN) * sizeof(double) <= (size_t)OZ_NXS * OZ_XPL, "fixup scratch in the data ring");
 
 // cudaFuncSetAttribute is per device: one flag bit per device ordinal
 bool attr_once(std::atomic<uint64_t>& done, int device) {
@@ -828,11 +860,11 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
   } else {
     static std::atomic<uint64_t> attr{0};
     if (attr_once(attr, ctx->device))
-      FDIGA_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      FDIGA_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     // 16 columns per block for every K (<= 512): 32 KB tiles at K = 256, six blocks per SM; at n = 256 this
     // beats 32 columns (three blocks per SM: 1.351 vs 1.336 ms per apply) and 8 (64-byte row segments: 1.368)
-    const int64_t tiles = batch * ((inner + 15) / 16);
-    oz_split_cols_kernel<16><<<(unsigned)tiles, 256, (size_t)K * 16 * sizeof(double), stream>>>(
+    const int64_t tiles = batch * ((inner + OZ_CW - 1) / OZ_CW);
+    oz_split_cols_kernel<<<(unsigned)tiles, 256, (size_t)K * OZ_CW * sizeof(double), stream>>>(
         x, batch, (int)K, inner, op.digits, op.exps, op.wide, op.rows_p, (int)op.kp, lam_row, lam_k, skip);
   }
   count_launch(ctx);
