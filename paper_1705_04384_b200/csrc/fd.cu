@@ -371,53 +371,34 @@ int oz_setup(fd_plan* P, bool force = false) {
   return FDIGA_OK;
 }
 
-// One mode product on the int8 path: split the data along axis l, contract with the factor digits.
-//   l = 0: slab X[i3][i2][i1] (c planes), data rows (i3, i2), k = i1
-//   l = 1: slab, data rows (i3, i1), k = i2 (the split transposes)
-//   l = 2: chunk T[i3][q] (q over len inner indices), data rows q, k = i3; divide_input: X / (lam_inner[q0 + q] +
-//          lam_3[i3]) first (the Lambda divide of eq:FD3D, applied as the data enters the backward product)
-int oz_mode(fd_plan* P, int l, const OzOperand& Fz, const double* Fs, const double* X, double* Y, const int* skip,
-            bool divide_input = false) {
-  const int64_t n1 = P->n[0], n2 = P->n[1], n3 = P->n[2];
-  const int64_t c = P->e - P->o, len = P->len;
-  OzOperand& Xz = P->ozX[l];
+// The mode-3 product on the int8 path (the modes 1 and 2 run plane-transposed, oz_mode_t below): the chunk
+// T[i3][q] (q over len inner indices), data rows q, k = i3, split transposing; divide_input: X / (lam_inner[q0 + q]
+// + lam_3[i3]) first (the Lambda divide of eq:FD3D, applied as the data enters the backward product).
+int oz_mode3(fd_plan* P, const OzOperand& Fz, const double* Fs, const double* X, double* Y, const int* skip,
+             bool divide_input = false) {
+  const int64_t n3 = P->n[2], len = P->len;
+  OzOperand& Xz = P->ozX[2];
   cudaStream_t st = P->ctx->stream;
   OzGemmArgs g{};
   g.X = &Xz;
   g.F = &Fz;
-  g.K = P->n[l];
+  g.K = n3;
   g.y = Y;
   g.skip = skip;
   g.xs = X;  // the FP64 operands, for the outputs of wide rows (oz.cuh: guard)
   g.fs = Fs;
-  g.ldf = P->ld[l];
+  g.ldf = P->ld[2];
   if (Xz.rows == 0) return FDIGA_OK;
-  if (l == 0) {
-    FDIGA_TRY(oz_split(P->ctx, st, X, n2 * c, n1, 1, n1, Xz, skip));
-    g.inner = n2 * c;
-    g.bstride = 0;
-    g.mstride = n1;
-    g.fstride = 1;
-    g.xs_b = 0, g.xs_i = n1, g.xs_k = 1;
-  } else if (l == 1) {
-    FDIGA_TRY(oz_split(P->ctx, st, X, c, n2, n1, 0, Xz, skip));
-    g.inner = n1;
-    g.bstride = n1 * n2;
-    g.mstride = 1;
-    g.fstride = n1;
-    g.xs_b = n1 * n2, g.xs_i = 1, g.xs_k = n1;
-  } else {
-    const double* lr = divide_input ? P->lam_inner + P->q0 : nullptr;
-    const double* lk = divide_input ? P->lam[2] : nullptr;
-    FDIGA_TRY(oz_split(P->ctx, st, X, 1, n3, len, 0, Xz, skip, lr, lk));
-    g.inner = len;
-    g.bstride = 0;
-    g.mstride = 1;
-    g.fstride = len;
-    g.xs_b = 0, g.xs_i = 1, g.xs_k = len;
-    g.lam_row = lr;
-    g.lam_k = lk;
-  }
+  const double* lr = divide_input ? P->lam_inner + P->q0 : nullptr;
+  const double* lk = divide_input ? P->lam[2] : nullptr;
+  FDIGA_TRY(oz_split(P->ctx, st, X, 1, n3, len, 0, Xz, skip, lr, lk));
+  g.inner = len;
+  g.bstride = 0;
+  g.mstride = 1;
+  g.fstride = len;
+  g.xs_b = 0, g.xs_i = 1, g.xs_k = len;
+  g.lam_row = lr;
+  g.lam_k = lk;
   FDIGA_TRY(mark(P, 1));
   FDIGA_TRY(oz_gemm(P->ctx, st, g));
   return mark(P, 2);
@@ -463,8 +444,8 @@ int fd_apply_oz(fd_plan* P, const double* r, double* s, const int* skip) {
   FDIGA_TRY(oz_mode_t(P, 0, P->ozW[0], P->W[0], r, a, skip));  // a = [i3][f1][i2]
   FDIGA_TRY(oz_mode_t(P, 1, P->ozW[1], P->W[1], a, b, skip));  // b = [i3][f2][f1]
   // the Lambda divide rides in the split that feeds the backward mode-3 product
-  FDIGA_TRY(oz_mode(P, 2, P->ozW[2], P->W[2], b, a, skip));
-  FDIGA_TRY(oz_mode(P, 2, P->ozU[2], P->U[2], a, b, skip, true));
+  FDIGA_TRY(oz_mode3(P, P->ozW[2], P->W[2], b, a, skip));
+  FDIGA_TRY(oz_mode3(P, P->ozU[2], P->U[2], a, b, skip, true));
   FDIGA_TRY(oz_mode_t(P, 0, P->ozU[0], P->U[0], b, a, skip));  // a = [i3][f1][i2]
   return oz_mode_t(P, 1, P->ozU[1], P->U[1], a, s, skip);      // s = [i3][i2][i1]
 }
@@ -758,8 +739,8 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
   const int64_t c = P->e - P->o, Nin = P->Nin, len = P->len;
   // forward modes 1..d-1 -> b (slab layout)
   if (d == 3 && P->oz) {
-    FDIGA_TRY(oz_mode(P, 0, P->ozW[0], P->W[0], r, a, skip));
-    FDIGA_TRY(oz_mode(P, 1, P->ozW[1], P->W[1], a, b, skip));
+    FDIGA_TRY(oz_mode_t(P, 0, P->ozW[0], P->W[0], r, a, skip));  // plane-transposed intermediate
+    FDIGA_TRY(oz_mode_t(P, 1, P->ozW[1], P->W[1], a, b, skip));  // natural slab layout again
   } else if (d == 3) {
     FDIGA_TRY(mode1(P, P->W[0], P->ld[0], r, a, n2 * c, skip));
     FDIGA_TRY(model(P, 1, P->W[1], P->ld[1], a, b, n1, c, nullptr, nullptr, skip));
@@ -791,8 +772,8 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
   FDIGA_TRY(comm_exchange(ctx, snd, rcv));  // b = T(n_d x len)
   FDIGA_TRY(mark(P, 4));
   if (P->oz) {  // the Lambda divide rides in the split feeding the backward product (chunk offset q0)
-    FDIGA_TRY(oz_mode(P, 2, P->ozW[2], P->W[2], b, a, skip));
-    FDIGA_TRY(oz_mode(P, 2, P->ozU[2], P->U[2], a, b, skip, true));
+    FDIGA_TRY(oz_mode3(P, P->ozW[2], P->W[2], b, a, skip));
+    FDIGA_TRY(oz_mode3(P, P->ozU[2], P->U[2], a, b, skip, true));
   } else {
     FDIGA_TRY(model(P, d - 1, P->W[d - 1], P->ld[d - 1], b, a, len, 1, P->lam[d - 1], P->lam_inner + P->q0, skip));
     FDIGA_TRY(model(P, d - 1, P->U[d - 1], P->ld[d - 1], a, b, len, 1, nullptr, nullptr, skip));
@@ -807,8 +788,8 @@ int fd_apply_sharded(fd_plan* P, const double* r, double* s, const int* skip) {
     FDIGA_TRY(mark(P, 3));
   }
   if (d == 3 && P->oz) {
-    FDIGA_TRY(oz_mode(P, 1, P->ozU[1], P->U[1], b, a, skip));
-    FDIGA_TRY(oz_mode(P, 0, P->ozU[0], P->U[0], a, s, skip));
+    FDIGA_TRY(oz_mode_t(P, 0, P->ozU[0], P->U[0], b, a, skip));  // the products commute: 1 then 2
+    FDIGA_TRY(oz_mode_t(P, 1, P->ozU[1], P->U[1], a, s, skip));
   } else if (d == 3) {
     FDIGA_TRY(model(P, 1, P->U[1], P->ld[1], b, a, n1, c, nullptr, nullptr, skip));
     FDIGA_TRY(mode1(P, P->U[0], P->ld[0], a, s, n2 * c, skip));
