@@ -2,13 +2,14 @@
 //
 //   oz_split_*_kernel : FP64 operand -> S = 7 int8 digit planes + per-row exponents (HBM-bound pass; the
 //                       strided modes are transposed so every GEMM operand is K-major)
-//   oz_gemm_kernel    : persistent, warp-specialised tcgen05 GEMM.  Warp 8 streams the data digit planes
-//                       through a TMA (SWIZZLE_128B) ring; warp 9 (converged, one elected lane per stage)
-//                       issues tcgen05.mma.kind::i8 into NW = 8 int32 accumulators in TMEM (one per
-//                       digit-pair weight t = i + j); warps 0-7 read them back with tcgen05.ld, combine in
-//                       FP64, scale by the row exponents and store.  The factor's digit planes for the CTA's
-//                       column tile stay resident in shared memory (K <= 256) or stream one k chunk at a time
-//                       (K <= 512).
+//   oz_gemm_kernel    : persistent, warp-specialised tcgen05 GEMM on CTA pairs (cta_group::2, M = 256, N = 128).
+//                       Warp 16 streams the data digit planes through a TMA (SWIZZLE_64B) ring, one full /
+//                       empty barrier pair per 64-wide k chunk; warps 17 and 18 of the leader CTA (converged,
+//                       one elected lane) issue tcgen05.mma.kind::i8 into int32 accumulators in TMEM (one per
+//                       digit-pair weight t = i + j, four passes of two weights over the contraction, the two
+//                       slot groups alternating); warps 0-15 read them back with tcgen05.ld, combine in FP64,
+//                       scale by the row exponents and store.  The factor's digit planes for the CTA's half of
+//                       the column tile stay resident in shared memory (contractions <= 256 per launch).
 //                       Outputs of "wide" rows (oz.cuh: guard) are then recomputed by the CTA that owns them
 //                       as IEEE FP64 dot products of the FP64 operands (oz_cta_fixup).
 #include <cuda.h>
@@ -41,6 +42,13 @@ namespace {
 // ---------------------------------------------------------------------------------------------
 // digit split
 // ---------------------------------------------------------------------------------------------
+// Programmatic dependent launch: every kernel of the int8 path is launched with the programmatic-stream-
+// serialization attribute, lets its successor be scheduled at once (pdl_trigger) and waits for its predecessor's
+// completion and memory (pdl_wait) before it touches anything that kernel wrote or still reads.  The
+// successor's launch latency and prologue (barrier set-up, TMEM allocation) then overlap this kernel's tail.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // 2^k for |k| <= 2044 as a product of two normal powers (each built from its bits)
 __device__ __forceinline__ double pow2(int k) {
   k = max(-2044, min(2044, k));
@@ -135,6 +143,8 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
                                                             int8_t* __restrict__ digits, int32_t* __restrict__ exps,
                                                             int32_t* __restrict__ wide, int64_t rows_p, int kp,
                                                             const int* skip) {
+  pdl_trigger();
+  pdl_wait();
   if (skip && *skip) return;
   const int lane = threadIdx.x & 31;
   const int64_t m = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -188,6 +198,8 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
                                                             int64_t rows_p, int kp,
                                                             const double* __restrict__ lam_row,
                                                             const double* __restrict__ lam_k, const int* skip) {
+  pdl_trigger();
+  pdl_wait();
   if (skip && *skip) return;
   constexpr int CW = OZ_CW, RG = 256 / CW;  // 16 columns, 16 row groups
   extern __shared__ double tile[];
@@ -340,7 +352,8 @@ constexpr int OZ_KCH = 64;                  // k per chunk (bytes of a SWIZZLE_6
 constexpr int OZ_KCMAX = 4;                 // chunks per launch: contraction <= 256 per launch
 constexpr int OZ_XPL = OZ_BM * OZ_KCH;      // one data digit plane chunk per CTA: 128 rows x 64 B = 8 KB
 constexpr int OZ_FPL = OZ_BNH * OZ_KCH;     // one factor digit plane chunk per CTA: 64 rows x 64 B = 4 KB
-constexpr int OZ_NXS = 14;                  // data plane slots in the ring (two pass-1 chunks)
+constexpr int OZ_NXS = 14;                  // data plane slots in the ring (two 7-plane chunks)
+constexpr int OZ_NCB = 8;                   // chunk barriers (full / empty pairs): more than the chunks in flight
 static_assert(OZ_EC * (OZ_EW / 4) == OZ_BN, "epilogue column groups cover the tile");
 
 struct OzKernelArgs {
@@ -420,8 +433,17 @@ __device__ void oz_cta_fixup(const OzKernelArgs& a, int mt_first, int per_nt, ui
                              double* part) {
   const int c = threadIdx.x & 31, sl = threadIdx.x >> 5;
   const int nx = *(volatile int32_t*)a.xw, nf = *(volatile const int32_t*)a.fw;
+  // the wide-row list is scanned from shared memory, a batch of OZ_EW * 32 entries per coalesced load (scanned
+  // from global memory it cost every CTA one dependent L2 round trip per entry: ~12 k cycles of tail per GEMM
+  // for two dozen wide rows)
+  int32_t* lst = reinterpret_cast<int32_t*>(part + OZ_EW * OZ_BN);
   for (int i = 0; i < nx; ++i) {
-    const int64_t m = a.xw[2 + i];
+    if (i % (OZ_EW * 32) == 0) {
+      oz_bar_epi();
+      if (i + (int)threadIdx.x < nx) lst[threadIdx.x] = a.xw[2 + i + threadIdx.x];
+      oz_bar_epi();
+    }
+    const int64_t m = lst[i % (OZ_EW * 32)];
     const int mt = (int)(m / OZ_PM);
     if (mt < mt_first || (mt - mt_first) % per_nt || (uint32_t)((m % OZ_PM) / OZ_BM) != rank) continue;
     const double* xr = a.xs + (m / a.inner) * a.xs_b + (m % a.inner) * a.xs_i;
@@ -458,7 +480,12 @@ __device__ void oz_cta_fixup(const OzKernelArgs& a, int mt_first, int per_nt, ui
     oz_bar_epi();
   }
   for (int i = 0; i < nf; ++i) {
-    const int64_t f = a.fw[2 + i];
+    if (i % (OZ_EW * 32) == 0) {
+      oz_bar_epi();
+      if (i + (int)threadIdx.x < nf) lst[threadIdx.x] = a.fw[2 + i + threadIdx.x];
+      oz_bar_epi();
+    }
+    const int64_t f = lst[i % (OZ_EW * 32)];
     if (f < n0 || f >= n0 + OZ_BN) continue;
     for (int k = threadIdx.x; k < a.K; k += OZ_EW * 32) sv[k] = a.fs[f * a.ldf + k];
     oz_bar_epi();
@@ -476,16 +503,59 @@ __device__ void oz_cta_fixup(const OzKernelArgs& a, int mt_first, int per_nt, ui
   }
 }
 
-// Two passes per tile over the contraction: pass 0 accumulates the weights t = 0..3 (10 digit pairs, data and
-// factor digits 0..3), pass 1 the weights 4..7 (24 pairs, digits 0..6): four int32 accumulators of 128 columns
-// (all 512 TMEM columns).  Phase q = 2 tile + pass.  Within every 64-wide k chunk the MMAs go weight by weight
-// in the phase's order (pass 0: 0, 1, 2, 3; pass 1: 6, 5, 7, 4); the k-th weight of every phase lives in slot k.
-// So in the first chunk the slots are first written one after another, and in the last chunk they complete
-// one after another, the first ones well before the phase ends: the epilogue drains slot k of phase q while
-// the MMAs of q's remaining weights and of q + 1's first weights run (slack of 12 or more MMAs per slot).
+// Passes per tile over the contraction (FDIGA_OZ_NPASS):
+//   4 (default): four passes of two weights each.  The four 128-column TMEM slots form two groups {0, 1} and
+//      {2, 3} used by alternating passes, so the epilogue drains a pass's two accumulators (TMEM read-out and
+//      FP64 combination) while the MMAs of the next pass fill the other group.  Price: a pass streams the data
+//      digit planes its weights need again, 19 plane chunks per 64 k instead of 11.  Pass order
+//      (0,1) (2,3) (4,5) (6,7) (FDIGA_OZ_ORDER 1: 2, 4, 6, 7 planes); order 0 = (4,5) (6,7) (0,3) (1,2) and
+//      order 2 = (0,7) (1,6) (2,5) (3,4) (balanced MMA counts, 25 planes) measured 1 % and 8 % slower.
+//   2: two passes of four weights (all four slots per pass; the earlier kernel).
+// Measured at n = 256 (in-kernel clock64 timeline, tools/oz_trace.py): both schedules run at ~32 k cycles per tile
+// against 17.4 k cycles of MMAs (272 at the probe rate), 4 passes 1 % faster at n = 256 and 3 % at n = 384.  What
+// bounds a tile is the interference between the tensor pipe and the epilogue inside the SM, not the schedule:
+// under a saturated MMA stream a slot drain takes 4-7 k cycles instead of ~1 k alone (tcgen05.ld gets what the
+// MMAs' accumulator traffic leaves), and the tile's 128 KB of y stores take 6 k instead of 3 k cycles while they
+// in turn slow the MMAs (138 instead of ~80 cycles each: the stores and the MMAs' operand reads share the
+// L1 / shared-memory path).
+// Phase q = NPASS tile + pass; its k-th weight lives in slot (pass WPP + k) mod 4, used for the (q / NGRP)-th
+// time.  Within every 64-wide k chunk the MMAs go weight by weight, so a pass's slots complete one after
+// another in the last chunk.
+#ifndef FDIGA_OZ_NPASS
+#define FDIGA_OZ_NPASS 4
+#endif
+#ifndef FDIGA_OZ_ORDER
+#define FDIGA_OZ_ORDER 1
+#endif
+#ifdef FDIGA_OZ_TRACE  // in-kernel clock64 timeline of CTA pair 0 (variant builds; tools/oz_trace.py)
+__device__ long long oz_trace_buf[4096];
+#define OZ_TR(cond, idx, val)                                 \
+  do {                                                        \
+    if ((cond) && blockIdx.x == 0 && (threadIdx.x & 31) == 0) oz_trace_buf[(idx)] = (val); \
+  } while (0)
+#else
+#define OZ_TR(cond, idx, val) do { } while (0)
+#endif
+constexpr int OZ_NPASS = FDIGA_OZ_NPASS;
+constexpr int OZ_WPP = OZ_NW / OZ_NPASS;      // weights per pass
+constexpr int OZ_NGRP = OZ_NSLOT / OZ_WPP;    // slot groups (passes in flight: one filling, the others draining)
+static_assert(OZ_NPASS == 2 || OZ_NPASS == 4, "two passes of four weights or four passes of two");
 __host__ __device__ constexpr int oz_weight(int P, int k) {
-  return P == 0 ? k : (k == 0 ? 6 : k == 1 ? 5 : k == 2 ? 7 : 4);
+  if (OZ_NPASS == 2) return P == 0 ? k : (k == 0 ? 6 : k == 1 ? 5 : k == 2 ? 7 : 4);
+  if (FDIGA_OZ_ORDER == 1) return 2 * P + k;                                  // (0,1) (2,3) (4,5) (6,7)
+  if (FDIGA_OZ_ORDER == 2) return k == 0 ? P : 7 - P;                         // (0,7) (1,6) (2,5) (3,4)
+  return P == 0 ? 4 + k : P == 1 ? 6 + k : P == 2 ? (k == 0 ? 0 : 3) : 1 + k;  // (4,5) (6,7) (0,3) (1,2)
 }
+// data digit planes 0 .. nd - 1 a pass needs: weight t pairs data digit i <= min(t, S - 1) with factor digit t - i
+__host__ __device__ constexpr int oz_nd(int P) {
+  int nd = 0;
+  for (int k = 0; k < OZ_WPP; ++k) {
+    const int t = oz_weight(P, k), hi = t < OZ_S - 1 ? t : OZ_S - 1;
+    nd = hi + 1 > nd ? hi + 1 : nd;
+  }
+  return nd;
+}
+__host__ __device__ constexpr int oz_slot(int P, int k) { return (P * OZ_WPP + k) % OZ_NSLOT; }
 
 // the MMAs of weight T (slot sk) in one chunk: pairs (i, T - i), NKS K-steps of 32 each.  xd[i]: descriptor of
 // data digit i's plane chunk, fd: descriptor of factor digit 0's plane chunk (digit j is j planes further).
@@ -521,17 +591,22 @@ __device__ __forceinline__ void oz_weight_mmas(uint32_t td, const uint64_t (&xd)
 __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap fmap,
                    const __grid_constant__ OzKernelArgs a) {
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  if (a.skip && *a.skip) return;  // (both CTAs of a pair read the same flag)
+  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
+  // (offset arithmetic on the shared array, not an integer round trip: derived pointers stay in the shared
+  // address space for the compiler -- LDS / STS instead of generic accesses)
+  uint8_t* smem = oz_smem_raw + ((1024u - (smem_u32(oz_smem_raw) & 1023u)) & 1023u);
   const int KC = a.KC;
   uint8_t* sF = smem;                                    // [KC][S] resident factor planes, this CTA's 64 rows
   uint8_t* sX = smem + OZ_KCMAX * OZ_S * OZ_FPL;         // data ring [NXS] plane slots
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_NXS * OZ_XPL);  // [NXS] (leader: both CTAs' bytes)
-  uint64_t* empty = full + OZ_NXS;                                     // [NXS] (each CTA, multicast commit)
-  uint64_t* fbar = empty + OZ_NXS;    // [1] factor landed (leader)
-  uint64_t* sfull = fbar + 1;         // [4] accumulator slot complete (MMA -> epilogues of both CTAs)
+  // One full / empty barrier pair per k chunk in flight (chunk number mod NCB): a chunk's nd planes occupy
+  // consecutive ring slots, land on one transaction barrier and are released by one commit per MMA warp (a
+  // barrier pair per plane cost each MMA warp nd commits per chunk, ~90 cycles each, as long as the MMAs of a
+  // short chunk)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_NXS * OZ_XPL);  // [NCB] (leader: both CTAs' bytes)
+  uint64_t* empty = full + OZ_NCB;                                     // [NCB] (each CTA, multicast commit)
+  uint64_t* fbar = empty + OZ_NCB;    // [KCMAX] factor chunk landed (leader)
+  uint64_t* sfull = fbar + OZ_KCMAX;  // [4] accumulator slot complete (MMA -> epilogues of both CTAs)
   uint64_t* sempty = sfull + OZ_NSLOT;  // [4] accumulator slot drained by both CTAs (leader)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + OZ_NSLOT);
   double* sSF = reinterpret_cast<double*>(sempty + OZ_NSLOT + 2);  // 2^(e_f - WSHIFT) of the pair's factor rows
@@ -540,12 +615,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
+  OZ_TR(warp == 0, 0, clock64());
   if (threadIdx.x == 0) {
-    for (int s = 0; s < OZ_NXS; ++s) {
+    for (int s = 0; s < OZ_NCB; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 2);  // both MMA warps commit
     }
-    mbar_init(fbar, 1);
+    for (int s = 0; s < OZ_KCMAX; ++s) mbar_init(&fbar[s], 1);
     for (int t = 0; t < OZ_NSLOT; ++t) {
       mbar_init(&sfull[t], 1);
       mbar_init(&sempty[t], 2 * OZ_EW);
@@ -560,6 +636,11 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
   cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  // set-up done (barriers, TMEM): now wait for the preceding kernel (the split that wrote the data digits;
+  // transitively everything before it) before reading anything it wrote
+  pdl_wait();
+  const bool skip = a.skip && *a.skip;  // (both CTAs of a pair read the same flag)
+  OZ_TR(warp == 0, 1, clock64());
 
   // tile sequence of this pair: column tile nt0 fixed, row tiles strided
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
@@ -568,94 +649,111 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
   const int mt_first = pair / a.nt;
   const int n0 = nt0 * OZ_BN;
 
-  if (warp == OZ_EW) {
+  if (skip) {
+    // (solver graphs: the step is switched off; fall through to the TMEM release)
+  } else if (warp == OZ_EW) {
     if (lane == 0) {
-      // resident factor digit planes: this CTA's 64 of the pair's 128 rows, [kc][digit] chunks
-      if (leader) mbar_arrive_expect_tx(fbar, (uint32_t)(2 * OZ_S * KC * OZ_FPL));
+      // resident factor digit planes: this CTA's 64 of the pair's 128 rows, [kc][digit] chunks, each chunk on
+      // its own barrier and issued just before the first data chunk that needs it (the first MMAs start after
+      // one chunk, not after the whole factor)
       const uint32_t fbar_l = mapa(fbar, 0);
-      for (int kc = 0; kc < KC; ++kc)
-        for (int s = 0; s < OZ_S; ++s)
-          tma_load_2sm(sF + (kc * OZ_S + s) * OZ_FPL, &fmap, a.kbase + kc * OZ_KCH,
-                       (int)(s * a.f_rows_p + n0 + rank * OZ_BNH), fbar_l);
-      uint32_t st = 0, ph = 0;
-      bool wrapped = false;
+      uint32_t n = 0, pos = 0;           // chunk number, ring slot of its first plane
+      uint32_t tn = 0, occ = 0;          // oldest chunk whose slots are still held; slots held by tn .. n - 1
+      int tpass = 0, tkc = 0;
       for (int mt = mt_first; mt < a.mt; mt += per_nt) {
         const int m0 = mt * OZ_PM + (int)rank * OZ_BM;
-        for (int pass = 0; pass < 2; ++pass) {
-          const int nd = pass == 0 ? 4 : OZ_S;  // data digits of this pass
-          for (int kc = 0; kc < KC; ++kc)
-            for (int i = 0; i < nd; ++i) {
-              if (wrapped) mbar_wait(&empty[st], ph ^ 1);
-              if (leader) mbar_arrive_expect_tx(&full[st], 2 * OZ_XPL);
-              tma_load_2sm(sX + st * OZ_XPL, &xmap, a.kbase + kc * OZ_KCH, (int)(i * a.x_rows_p + m0),
-                           mapa(&full[st], 0));
-              if (++st == OZ_NXS) {
-                st = 0;
-                ph ^= 1;
-                wrapped = true;
-              }
+        for (int pass = 0; pass < OZ_NPASS; ++pass) {
+          const uint32_t nd = oz_nd(pass);  // data digit planes of this pass
+          for (int kc = 0; kc < KC; ++kc, ++n) {
+            if (n < (uint32_t)KC) {
+              if (leader) mbar_arrive_expect_tx(&fbar[kc], (uint32_t)(2 * OZ_S * OZ_FPL));
+              for (int s = 0; s < OZ_S; ++s)
+                tma_load_2sm(sF + (kc * OZ_S + s) * OZ_FPL, &fmap, a.kbase + kc * OZ_KCH,
+                             (int)(s * a.f_rows_p + n0 + rank * OZ_BNH), fbar_l + 8u * (uint32_t)kc);
             }
+            while (occ + nd > OZ_NXS) {  // the chunks whose slots this one overwrites must be complete
+              mbar_wait(&empty[tn % OZ_NCB], (tn / OZ_NCB) & 1);
+              occ -= oz_nd(tpass);
+              if (++tkc == KC) {
+                tkc = 0;
+                if (++tpass == OZ_NPASS) tpass = 0;
+              }
+              ++tn;
+            }
+            const uint32_t fb = mapa(&full[n % OZ_NCB], 0);
+            if (leader) mbar_arrive_expect_tx(&full[n % OZ_NCB], 2 * nd * OZ_XPL);
+            for (uint32_t i = 0; i < nd; ++i) {
+              tma_load_2sm(sX + pos * OZ_XPL, &xmap, a.kbase + kc * OZ_KCH, (int)(i * a.x_rows_p + m0), fb);
+              if (++pos == OZ_NXS) pos = 0;
+            }
+            occ += nd;
+          }
         }
       }
     }
   } else if (warp >= OZ_EW + 1) {
-    // two MMA warps (leader CTA): warp OZ_EW + 1 issues slots 0 and 3, warp OZ_EW + 2 slots 1 and 2, so one
-    // warp's barrier waits and commits overlap the other's MMAs (a single issuing thread left the tensor pipe
-    // idle between short weight groups)
+    // two MMA warps (leader CTA), each issuing half of a pass's weights (four passes: warp k the pass's k-th
+    // weight; two passes: slots 0, 3 and 1, 2), so one warp's barrier waits and commits overlap the other's
+    // MMAs (a single issuing thread left the tensor pipe idle between short weight groups)
     const int mw = warp - (OZ_EW + 1);
     if (leader) {  // each warp runs its issue loop converged (uniform operands); one elected lane issues
-      mbar_wait(fbar, 0);
-      tc_fence_after();
       const uint32_t sx0 = smem_u32(sX);
       const uint64_t fd0 = sdesc_sw64(smem_u32(sF));
-      uint32_t st = 0, ph = 0, q = 0;
+      uint32_t n = 0, pos = 0, q = 0;  // chunk number, ring slot of its first plane, phase
       for (int mt = mt_first; mt < a.mt; mt += per_nt) {
-        for (int pass = 0; pass < 2; ++pass, ++q) {
-          const int nd = pass == 0 ? 4 : OZ_S;
-          for (int kc = 0; kc < KC; ++kc) {
+        for (int pass = 0; pass < OZ_NPASS; ++pass, ++q) {
+          const int nd = oz_nd(pass);
+          const uint32_t use = q / OZ_NGRP;  // how often this pass's slots were used before
+          OZ_TR(true, 16 + mw * 512 + q * 8 + 0, clock64());
+          for (int kc = 0; kc < KC; ++kc, ++n) {
+            OZ_TR(kc <= 1, 16 + mw * 512 + q * 8 + 1 + 2 * kc, clock64());
             const bool first = kc == 0, last = kc == KC - 1;
             const int nks = last ? a.ks_last : OZ_KCH / 32;  // K-steps of 32 carrying real contraction indices
-            // this chunk's data planes: slots st, st + 1, .. (mod NXS)
+            if (n < (uint32_t)KC) mbar_wait(&fbar[kc], 0);  // (first pass of the first tile: the factor chunk)
+            mbar_wait(&full[n % OZ_NCB], (n / OZ_NCB) & 1);
+            // this chunk's data planes: slots pos, pos + 1, .. (mod NXS)
             uint64_t xd[OZ_S];
-            uint32_t s2 = st, p2 = ph;
 #pragma unroll
             for (int i = 0; i < OZ_S; ++i) {
               if (i < nd) {
-                mbar_wait(&full[s2], p2);
-                xd[i] = sdesc_sw64(sx0 + s2 * OZ_XPL);
-                if (++s2 == OZ_NXS) {
-                  s2 = 0;
-                  p2 ^= 1;
-                }
+                xd[i] = sdesc_sw64(sx0 + pos * OZ_XPL);
+                if (++pos == OZ_NXS) pos = 0;
               } else {
                 xd[i] = 0;
               }
             }
             tc_fence_after();
+            OZ_TR(kc <= 1, 16 + mw * 512 + q * 8 + 2 + 2 * kc, clock64());
             const uint64_t fd = fd0 + (uint64_t)(kc * OZ_S * (OZ_FPL >> 4));
 #define OZ_WEIGHT(P, K)                                                                                \
-  if (mw == ((K == 0 || K == 3) ? 0 : 1)) {                                                            \
-    if (first && q > 0) { /* the slot's previous accumulator must be drained */                      \
-      mbar_wait(&sempty[K], (q - 1) & 1);                                                              \
+  if (mw == (OZ_NPASS == 4 ? K : ((K == 0 || K == 3) ? 0 : 1))) {                                      \
+    if (first && use > 0) { /* the slot's previous accumulator must be drained */                    \
+      mbar_wait(&sempty[oz_slot(P, K)], (use - 1) & 1);                                                \
       tc_fence_after();                                                                                \
     }                                                                                                  \
-    oz_weight_mmas<oz_weight(P, K)>(tbase + (uint32_t)(K * OZ_BN), xd, fd, first, nks);                \
-    if (last) tc_commit_pair(&sfull[K]); /* weight complete */                                         \
+    oz_weight_mmas<oz_weight(P, K)>(tbase + (uint32_t)(oz_slot(P, K) * OZ_BN), xd, fd, first, nks);    \
+    if (last) tc_commit_pair(&sfull[oz_slot(P, K)]); /* weight complete */                             \
   }
             static_assert(OZ_S == 7 && OZ_NW == 8, "weight sequences written for 7 digits, 8 weights");
+#if FDIGA_OZ_NPASS == 4
+            switch (pass) {
+              case 0: OZ_WEIGHT(0, 0) OZ_WEIGHT(0, 1) break;
+              case 1: OZ_WEIGHT(1, 0) OZ_WEIGHT(1, 1) break;
+              case 2: OZ_WEIGHT(2, 0) OZ_WEIGHT(2, 1) break;
+              default: OZ_WEIGHT(3, 0) OZ_WEIGHT(3, 1) break;
+            }
+#else
             if (pass == 0) {
               OZ_WEIGHT(0, 0) OZ_WEIGHT(0, 1) OZ_WEIGHT(0, 3) OZ_WEIGHT(0, 2)
             } else {
               OZ_WEIGHT(1, 0) OZ_WEIGHT(1, 1) OZ_WEIGHT(1, 3) OZ_WEIGHT(1, 2)
             }
+#endif
 #undef OZ_WEIGHT
-            for (int i = 0; i < nd; ++i) {  // free the chunk's plane slots in both CTAs when its MMAs are done
-              tc_commit_pair(&empty[st]);
-              if (++st == OZ_NXS) {
-                st = 0;
-                ph ^= 1;
-              }
-            }
+            OZ_TR(kc == 0, 16 + mw * 512 + q * 8 + 5, clock64());
+            OZ_TR(last, 16 + mw * 512 + q * 8 + 6, clock64());
+            // free the chunk's plane slots in both CTAs when its MMAs are done
+            tc_commit_pair(&empty[n % OZ_NCB]);
           }
         }
       }
@@ -677,17 +775,20 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
       const int64_t mm = mv ? m : 0;
       const int64_t row_off = oz_out_off(a, mm);
       const double sx = pow2(code_exp(mv ? a.ex[mm] : 0));  // (outputs of wide rows: replaced by oz_cta_fixup)
+      OZ_TR(warp == 0 && sx != 0.0, 3072 + (q / OZ_NPASS) * 4 + 2, clock64());
       // sum_t 2^{8 (NW - 1 - t)} C_t over the weights as they complete
       double acc[OZ_EC];
 #pragma unroll
       for (int c = 0; c < OZ_EC; ++c) acc[c] = 0.0;
 #pragma unroll 1
-      for (int pass = 0; pass < 2; ++pass, ++q) {
+      for (int pass = 0; pass < OZ_NPASS; ++pass, ++q) {
 #pragma unroll 1
-        for (int k = 0; k < OZ_NSLOT; ++k) {
-          const int t = pass == 0 ? k : (k == 0 ? 6 : k == 1 ? 5 : k == 2 ? 7 : 4);  // oz_weight(pass, k)
-          mbar_wait(&sfull[k], q & 1);
+        for (int k = 0; k < OZ_WPP; ++k) {
+          const int t = oz_weight(pass, k), slot = oz_slot(pass, k);
+          OZ_TR(warp == 0, 2048 + (q * OZ_WPP + k) * 4 + 0, clock64());
+          mbar_wait(&sfull[slot], (q / OZ_NGRP) & 1);
           tc_fence_after();
+          OZ_TR(warp == 0, 2048 + (q * OZ_WPP + k) * 4 + 1, clock64());
           const double wt = (double)(1ll << (8 * (OZ_NW - 1 - t)));
 #pragma unroll
           for (int c = 0; c < OZ_EC; c += 16) {
@@ -698,7 +799,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
                   "=r"(v[15])
-                : "r"(tbase + lane_off + (uint32_t)(k * OZ_BN + c0 + c)));
+                : "r"(tbase + lane_off + (uint32_t)(slot * OZ_BN + c0 + c)));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
             // int32 -> double without I2F: the bits 0x43300000:(v ^ 2^31) are 2^52 + 2^31 + v exactly, and
             // subtracting 2^52 + 2^31 is exact
@@ -709,10 +810,25 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(mapa(&sempty[k], 0));
+          if (lane == 0) mbar_arrive_cluster(mapa(&sempty[slot], 0));
+          OZ_TR(warp == 0, 2048 + (q * OZ_WPP + k) * 4 + 2, clock64());
         }
       }
-      if (mv) {
+      OZ_TR(warp == 0, 3072 + (q / OZ_NPASS - 1) * 4, clock64());
+      if (mv && !a.accum && n0 + OZ_BN <= a.Nf) {
+        // full column tile (the common case): straight-line stores, one f stride per column; for every
+        // column a warp stores 32 consecutive rows' values (mstride == 1 in every FD product: 256 contiguous
+        // bytes).  Two exact power-of-two scalings: the factor row's (with the digit weight) and the data row's
+        double* yp = a.y + row_off + (n0 + c0) * a.fstride;
+        const double2* sf = reinterpret_cast<const double2*>(sSF + c0);
+#pragma unroll
+        for (int c = 0; c < OZ_EC; c += 2) {
+          const double2 f2 = sf[c >> 1];
+          yp[0] = (acc[c] * f2.x) * sx;
+          yp[a.fstride] = (acc[c + 1] * f2.y) * sx;
+          yp += 2 * a.fstride;
+        }
+      } else if (mv) {
         const bool vec = a.yvec && a.fstride == 1 && ((row_off + n0 + c0) & 1) == 0;
 #pragma unroll
         for (int c = 0; c < OZ_EC; c += 2) {
@@ -740,16 +856,20 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
           }
         }
       }
+      OZ_TR(warp == 0, 3072 + (q / OZ_NPASS - 1) * 4 + 1, clock64());
     }
+    OZ_TR(warp == 0, 2, clock64());
     if (a.fixup) {
       oz_bar_epi();  // (every epilogue warp past its last drain: the data ring is free for the fixup)
       oz_cta_fixup(a, mt_first, per_nt, rank, n0, sFix, sFix + OZ_MAXKP);
     }
   }
+  OZ_TR(warp == 0, 3, clock64());
   tc_fence_before();
   cluster_sync();  // every MMA done and every remote arrive delivered before the pair's TMEM is released
   tc_fence_after();
   if (warp == OZ_EW + 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+  OZ_TR(warp == 0, 4, clock64());
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -775,11 +895,12 @@ int get_encode(EncodeTiledFn* fn) {
 }
 
 constexpr size_t oz_smem_bytes() {
-  return 1024 + (size_t)OZ_KCMAX * OZ_S * OZ_FPL + (size_t)OZ_NXS * OZ_XPL + (2 * OZ_NXS + 1 + 2 * OZ_NSLOT + 2) * 8 +
+  return 1024 + (size_t)OZ_KCMAX * OZ_S * OZ_FPL + (size_t)OZ_NXS * OZ_XPL + (2 * OZ_NCB + OZ_KCMAX + 2 * OZ_NSLOT + 2) * 8 +
          OZ_BN * sizeof(double);
 }
 static_assert(oz_smem_bytes() <= 227 * 1024, "shared memory per CTA");
-static_assert((OZ_MAXKP + OZ_EW * OZ_BN) * sizeof(double) <= (size_t)OZ_NXS * OZ_XPL, "fixup scratch in the data ring");
+static_assert((OZ_MAXKP + OZ_EW * OZ_BN) * sizeof(double) + OZ_EW * 32 * sizeof(int32_t) <= (size_t)OZ_NXS * OZ_XPL,
+              "fixup scratch in the data ring");
 
 // cudaFuncSetAttribute is per device: one flag bit per device ordinal
 bool attr_once(std::atomic<uint64_t>& done, int device) {
@@ -843,6 +964,32 @@ int oz_operand_set_ft(OzOperand& op, const double* F_host, int64_t n) {
   return FDIGA_OK;
 }
 
+// Off by default (FDIGA_OZ_PDL=1 sets the attribute; without it the kernels' griddepcontrol instructions are
+// no-ops): measured on a B200 it shortens the small shapes (n = 128: 0.199 -> 0.172 ms per apply) but costs the
+// n = 256 apply 9 us (1.122 -> 1.131 ms, reproducibly), and the int8 path is the default only for n >= 192.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FDIGA_OZ_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+// launch with the programmatic-stream-serialization attribute (see pdl_trigger / pdl_wait)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch, int64_t K, int64_t inner,
              int64_t ldx, OzOperand& op, const int* skip, const double* lam_row, const double* lam_k) {
 
@@ -851,12 +998,8 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
   if (rows == 0) return FDIGA_OK;
   if (inner == 1 && !lam_row) {  // (the divide is done by the strided kernel, which handles inner == 1 too)
     const unsigned grid = (unsigned)((rows + 7) / 8);
-    if (op.kp <= 256)
-      oz_split_rows_kernel<1><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.wide, op.rows_p,
-                                                        (int)op.kp, skip);
-    else
-      oz_split_rows_kernel<2><<<grid, 256, 0, stream>>>(x, rows, (int)K, ldx, op.digits, op.exps, op.wide, op.rows_p,
-                                                        (int)op.kp, skip);
+    FDIGA_CUDA(launch_pdl(op.kp <= 256 ? oz_split_rows_kernel<1> : oz_split_rows_kernel<2>, dim3(grid), dim3(256), 0,
+                          stream, x, rows, (int)K, ldx, op.digits, op.exps, op.wide, op.rows_p, (int)op.kp, skip));
   } else {
     static std::atomic<uint64_t> attr{0};
     if (attr_once(attr, ctx->device))
@@ -864,8 +1007,9 @@ int oz_split(fdiga_ctx* ctx, cudaStream_t stream, const double* x, int64_t batch
     // 16 columns per block for every K (<= 512): 32 KB tiles at K = 256, six blocks per SM; at n = 256 this
     // beats 32 columns (three blocks per SM: 1.351 vs 1.336 ms per apply) and 8 (64-byte row segments: 1.368)
     const int64_t tiles = batch * ((inner + OZ_CW - 1) / OZ_CW);
-    oz_split_cols_kernel<<<(unsigned)tiles, 256, (size_t)K * OZ_CW * sizeof(double), stream>>>(
-        x, batch, (int)K, inner, op.digits, op.exps, op.wide, op.rows_p, (int)op.kp, lam_row, lam_k, skip);
+    FDIGA_CUDA(launch_pdl(oz_split_cols_kernel, dim3((unsigned)tiles), dim3(256), (size_t)K * OZ_CW * sizeof(double),
+                          stream, x, batch, (int)K, inner, op.digits, op.exps, op.wide, op.rows_p, (int)op.kp, lam_row,
+                          lam_k, skip));
   }
   count_launch(ctx);
   FDIGA_CUDA(cudaGetLastError());
@@ -922,8 +1066,11 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   cfg.blockDim = dim3(OZ_THREADS);
   cfg.dynamicSmemBytes = oz_smem_bytes();
   cfg.stream = stream;
-  cfg.attrs = nullptr;
-  cfg.numAttrs = 0;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   auto kern = oz_gemm_kernel;
   // contractions longer than 256 (the resident factor chunks): two launches, the second accumulating into y
   for (int kbase = 0; kbase < g.K; kbase += OZ_KCMAX * OZ_KCH) {
@@ -951,3 +1098,9 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
 }
 
 }  // namespace fdiga
+
+#ifdef FDIGA_OZ_TRACE
+extern "C" int fdiga_oz_trace_read(long long* dst, int n) {
+  return (int)cudaMemcpyFromSymbol(dst, fdiga::oz_trace_buf, sizeof(long long) * (size_t)n);
+}
+#endif
