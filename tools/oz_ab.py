@@ -32,6 +32,12 @@ ks = {}
 for _ in range(5):
     for k, t in fd.fd_apply_timed(P, x, y):
         ks.setdefault(k, []).append(t)
+seq = [[] for _ in range(64)]
+for _ in range(5):
+    for i, (k, t) in enumerate(fd.fd_apply_timed(P, x, y)):
+        seq[i].append((k, t))
+if os.environ.get("OZ_AB_SEQ"):
+    print("  per launch (us): " + "  ".join(f"{v[0][0]}:{np.mean([t for _, t in v]) * 1e3:.1f}" for v in seq if v), flush=True)
 lib = os.environ.get("FDIGA_LIB", "in-tree")
 print(f"{lib} n={n} {path}: {ms:.4f} ms/apply  " +
       "  ".join(f"{k}: {np.mean(v) * 1e3:.1f} us x{len(v) // 5}" for k, v in ks.items()), flush=True)
