@@ -324,6 +324,7 @@ extern "C" int bicgstab_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, cons
                               const bicgstab_opts* opts, bicgstab_report* rep) {
   FDIGA_CHECK(ctx && A && ((b && x) || stencil_local_rows(A) == 0), FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_TRY(bind(ctx));
+  NvtxSolveScope nvtx_(ctx, "fdiga:bicgstab_solve");
   const double rtol = opts ? opts->rtol : 1e-8;
   const int max_iters = opts ? opts->max_iters : 1000;
   const int use_x0 = opts ? opts->use_x0 : 0;

@@ -1,8 +1,10 @@
 // Internal helpers shared by the libfdiga translation units (never exported).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -88,9 +90,30 @@ struct fdiga_ctx {
   // interval [e_i, e_{i+1}) is charged to the stage of e_i (fdiga::prof_mark)
   std::vector<std::pair<int, cudaEvent_t>>* prof = nullptr;
   int prof_stage = 0;
+  int nvtx_stage_open = -1;  // FDIGA_NVTX: -1 outside a solve, 0 inside without an open stage range, 1 with one
 };
 
 namespace fdiga {
+// NVTX ranges (FDIGA_NVTX=1; header-only NVTX 3, no link dependency): one per API call (NvtxRange) and one per
+// solve stage (prof_mark), so that profilers can filter by stage (ncu --nvtx --nvtx-include "fdiga:fd/").
+inline bool nvtx_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("FDIGA_NVTX");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+struct NvtxRange {
+  bool on;
+  explicit NvtxRange(const char* name) : on(nvtx_on()) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 inline void count_launch(fdiga_ctx* c, int k = 1) { c->launches += k; }
 // solve stages for gmres_report's breakdown
 enum { PROF_OTHER = 0, PROF_FD = 1, PROF_MATVEC = 2, PROF_ORTH = 3, PROF_COMM = 4, PROF_NSTAGE = 5 };
@@ -98,6 +121,13 @@ enum { PROF_OTHER = 0, PROF_FD = 1, PROF_MATVEC = 2, PROF_ORTH = 3, PROF_COMM = 
 // previous stage
 inline int prof_mark(fdiga_ctx* c, int stage) {
   const int prev = c->prof_stage;
+  if (nvtx_on() && c->nvtx_stage_open >= 0) {  // inside a solve: close the previous stage's range, open the next
+    static const char* const names[PROF_NSTAGE] = {"fdiga:other", "fdiga:fd", "fdiga:matvec", "fdiga:orth", "fdiga:comm"};
+    if (c->nvtx_stage_open) nvtxRangePop();
+    nvtxRangePushA(names[stage]);
+    c->nvtx_stage_open = 1;
+    if (!c->prof) c->prof_stage = stage;
+  }
   if (!c->prof) return prev;
   cudaEvent_t e = nullptr;
   if (cudaEventCreate(&e) == cudaSuccess) {
@@ -107,6 +137,24 @@ inline int prof_mark(fdiga_ctx* c, int stage) {
   c->prof_stage = stage;
   return prev;
 }
+// NVTX scope of a solve: the call's range plus the stage ranges prof_mark opens and closes inside it
+struct NvtxSolveScope {
+  fdiga_ctx* c;
+  bool on;
+  NvtxSolveScope(fdiga_ctx* ctx, const char* name) : c(ctx), on(nvtx_on()) {
+    if (!on) return;
+    nvtxRangePushA(name);
+    c->nvtx_stage_open = 0;
+  }
+  ~NvtxSolveScope() {
+    if (!on) return;
+    if (c->nvtx_stage_open == 1) nvtxRangePop();
+    c->nvtx_stage_open = -1;
+    nvtxRangePop();
+  }
+  NvtxSolveScope(const NvtxSolveScope&) = delete;
+  NvtxSolveScope& operator=(const NvtxSolveScope&) = delete;
+};
 void destroy_solver(fdiga_ctx* ctx);
 // Set the device of the context for the calling thread.
 inline int bind(const fdiga_ctx* c) {

@@ -897,6 +897,7 @@ int fd_setup_from_eig(fdiga_ctx* ctx, int d, const int64_t* n, const double* con
 
 int fd_setup(fdiga_ctx* ctx, int d, const int64_t* n, const double* const* M, const double* const* K,
              const fd_setup_opts* opts, fd_plan** out) {
+  fdiga::NvtxRange nvtx_("fdiga:fd_setup");
   FDIGA_TRY(check_common(ctx, d, n, out));
   FDIGA_CHECK(M && K, FDIGA_ERR_INVALID_ARG, "NULL pencil array");
   const double tol_imag = opts ? opts->tol_imag : 1e-8;
@@ -1074,9 +1075,13 @@ int fd_get_factors(const fd_plan* P, int l, double* U, double* W, double* lam_re
   return FDIGA_OK;
 }
 
-int fd_apply(fd_plan* P, const double* r, double* s) { return fdiga::fd_apply_ex(P, r, s, nullptr); }
+int fd_apply(fd_plan* P, const double* r, double* s) {
+  fdiga::NvtxRange nvtx_("fdiga:fd_apply");
+  return fdiga::fd_apply_ex(P, r, s, nullptr);
+}
 
 int fd_apply_host(fd_plan* P, const double* r_host, double* s_host) {
+  fdiga::NvtxRange nvtx_("fdiga:fd_apply_host");
   FDIGA_CHECK(P && r_host && s_host, FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_TRY(bind(P->ctx));
   FDIGA_TRY(P->host_io.ensure(std::max<int64_t>(1, P->Nloc)));

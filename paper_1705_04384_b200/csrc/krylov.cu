@@ -820,6 +820,7 @@ extern "C" int gmres_solve(fdiga_ctx* ctx, fdiga_stencil* A, fd_plan* P, const d
                            const gmres_opts* opts, gmres_report* rep) {
   FDIGA_CHECK(ctx && A && ((b && x) || stencil_local_rows(A) == 0), FDIGA_ERR_INVALID_ARG, "NULL argument");
   FDIGA_TRY(bind(ctx));
+  NvtxSolveScope nvtx_(ctx, "fdiga:gmres_solve");
   const int m = opts ? opts->m : 30;
   const double rtol = opts ? opts->rtol : 1e-8;
   const int max_iters = opts ? opts->max_iters : 1000;

@@ -702,7 +702,10 @@ int colloc_1d_convection(int p, int64_t ne, const double* wt, double* H) {
   return FDIGA_OK;
 }
 
-int stencil_matvec(fdiga_stencil* S, const double* x, double* y) { return fdiga::stencil_matvec_ex(S, x, y, nullptr); }
+int stencil_matvec(fdiga_stencil* S, const double* x, double* y) {
+  fdiga::NvtxRange nvtx_("fdiga:stencil_matvec");
+  return fdiga::stencil_matvec_ex(S, x, y, nullptr);
+}
 
 }  // extern "C"
 

@@ -698,3 +698,30 @@ def test_fd_apply_large_2d_ragged(ctx):
     s = torch.empty(r.size, dtype=torch.float64, device=DEV)
     fd.fd_apply(plan, gpu(r), s)
     assert rel(host(s), fastdiag.apply(f, r)) <= 1e-12
+
+
+def test_nvtx_stage_ranges_leave_the_solve_unchanged():
+    """FDIGA_NVTX=1 (NVTX ranges per API call and per solve stage, read once per process) must not change
+    results: the exactly preconditioned cfg1 solve still takes 1 iteration, profiled and graph-launched."""
+    import subprocess
+    import sys
+    code = (
+        "import torch, paper_1705_04384_b200 as fd\n"
+        "from synth import get_config, rhs\n"
+        "ctx = fd.Context(0, stream=torch.cuda.current_stream().cuda_stream)\n"
+        "c = get_config(1)\n"
+        "A = fd.colloc_assemble(ctx, 2, c.p, c.ne, c.geometry)\n"
+        "M, K = fd.colloc_1d_factors(c.p, c.ne)\n"
+        "P = fd.fd_setup(ctx, [M, M], [K, K])\n"
+        "b = torch.from_numpy(rhs(1, A.N)).cuda(); x = torch.empty_like(b)\n"
+        "for prof in (False, True):\n"
+        "    rep = fd.gmres_solve(ctx, A, P, b, x, profile=prof)\n"
+        "    assert rep['converged'] and rep['iters'] == 1, rep\n"
+        "rep = fd.bicgstab_solve(ctx, A, P, b, x)\n"
+        "assert rep['converged'], rep\n"
+        "print('nvtx ok')\n"
+    )
+    env = dict(os.environ, FDIGA_NVTX="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "nvtx ok" in out.stdout, out.stderr[-2000:]
