@@ -302,7 +302,7 @@ def arm_config(ns, ws):
             else "single GPU"}
 
 
-def fd_kernels(fd, plan, x, s, reps=3):
+def fd_kernels(fd, plan, x, s, reps=5):
     """Per-kernel CUDA-event durations of reps applies (fd_apply_timed): launches per apply, avg ms, share."""
     per = {}
     for _ in range(reps):

@@ -521,6 +521,9 @@ __device__ void oz_cta_fixup(const OzKernelArgs& a, int mt_first, int per_nt, ui
 // Phase q = NPASS tile + pass; its k-th weight lives in slot (pass WPP + k) mod 4, used for the (q / NGRP)-th
 // time.  Within every 64-wide k chunk the MMAs go weight by weight, so a pass's slots complete one after
 // another in the last chunk.
+#ifndef FDIGA_OZ_PDL_DEFAULT
+#define FDIGA_OZ_PDL_DEFAULT 0
+#endif
 #ifndef FDIGA_OZ_NPASS
 #define FDIGA_OZ_NPASS 4
 #endif
@@ -964,15 +967,15 @@ int oz_operand_set_ft(OzOperand& op, const double* F_host, int64_t n) {
   return FDIGA_OK;
 }
 
-// Off by default (FDIGA_OZ_PDL=1 sets the attribute; without it the kernels' griddepcontrol instructions are
-// no-ops): measured on a B200 it shortens the small shapes (n = 128: 0.199 -> 0.172 ms per apply) but costs the
-// n = 256 apply 9 us (1.122 -> 1.131 ms, reproducibly), and the int8 path is the default only for n >= 192.
-bool pdl_enabled() {
-  static const bool on = [] {
+// FDIGA_OZ_PDL: bit 0 = the splits carry the attribute (a split may start under the preceding GEMM's tail), bit 1
+// = the GEMMs carry it (a GEMM may set up under the preceding split's tail); without it the kernels'
+// griddepcontrol instructions are no-ops.
+int pdl_mode() {
+  static const int mode = [] {
     const char* e = std::getenv("FDIGA_OZ_PDL");
-    return e && e[0] == '1';
+    return e ? std::atoi(e) : FDIGA_OZ_PDL_DEFAULT;
   }();
-  return on;
+  return mode;
 }
 // launch with the programmatic-stream-serialization attribute (see pdl_trigger / pdl_wait)
 template <typename... KArgs, typename... Args>
@@ -986,7 +989,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = (pdl_mode() & 1) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
@@ -1070,7 +1073,7 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = (pdl_mode() & 2) ? 1 : 0;
   auto kern = oz_gemm_kernel;
   // contractions longer than 256 (the resident factor chunks): two launches, the second accumulating into y
   for (int kbase = 0; kbase < g.K; kbase += OZ_KCMAX * OZ_KCH) {
