@@ -522,7 +522,7 @@ __device__ void oz_cta_fixup(const OzKernelArgs& a, int mt_first, int per_nt, ui
 // time.  Within every 64-wide k chunk the MMAs go weight by weight, so a pass's slots complete one after
 // another in the last chunk.
 #ifndef FDIGA_OZ_PDL_DEFAULT
-#define FDIGA_OZ_PDL_DEFAULT 0
+#define FDIGA_OZ_PDL_DEFAULT 2
 #endif
 #ifndef FDIGA_OZ_NPASS
 #define FDIGA_OZ_NPASS 4
@@ -968,8 +968,10 @@ int oz_operand_set_ft(OzOperand& op, const double* F_host, int64_t n) {
 }
 
 // FDIGA_OZ_PDL: bit 0 = the splits carry the attribute (a split may start under the preceding GEMM's tail), bit 1
-// = the GEMMs carry it (a GEMM may set up under the preceding split's tail); without it the kernels'
-// griddepcontrol instructions are no-ops.
+// = the GEMMs carry it (a GEMM sets up -- barriers, TMEM, cluster sync -- under the preceding split's tail);
+// without the attribute a kernel's griddepcontrol instructions are no-ops.  Measured at n = 256 (apply, ms):
+// 0: 1.118, 1: 1.149, 2: 1.098, 3: 1.127 -- early split blocks take SMs from the GEMM's last tiles, the GEMM's
+// early set-up is free.  Default 2.
 int pdl_mode() {
   static const int mode = [] {
     const char* e = std::getenv("FDIGA_OZ_PDL");
