@@ -6,8 +6,8 @@
 //                       Warp 16 streams the data digit planes through a TMA (SWIZZLE_64B) ring, one full /
 //                       empty barrier pair per 64-wide k chunk; warps 17 and 18 of the leader CTA (converged,
 //                       one elected lane) issue tcgen05.mma.kind::i8 into int32 accumulators in TMEM (one per
-//                       digit-pair weight t = i + j, four passes of two weights over the contraction, the two
-//                       slot groups alternating); warps 0-15 read them back with tcgen05.ld, combine in FP64,
+//                       digit-pair weight t = i + j, two passes of four weights over the contraction); warps
+//                       0-15 read them back with tcgen05.ld, combine in FP64,
 //                       scale by the row exponents and store.  The factor's digit planes for the CTA's half of
 //                       the column tile stay resident in shared memory (contractions <= 256 per launch).
 //                       Outputs of "wide" rows (oz.cuh: guard) are then recomputed by the CTA that owns them
@@ -504,28 +504,31 @@ __device__ void oz_cta_fixup(const OzKernelArgs& a, int mt_first, int per_nt, ui
 }
 
 // Passes per tile over the contraction (FDIGA_OZ_NPASS):
-//   4 (default): four passes of two weights each.  The four 128-column TMEM slots form two groups {0, 1} and
-//      {2, 3} used by alternating passes, so the epilogue drains a pass's two accumulators (TMEM read-out and
-//      FP64 combination) while the MMAs of the next pass fill the other group.  Price: a pass streams the data
-//      digit planes its weights need again, 19 plane chunks per 64 k instead of 11.  Pass order
-//      (0,1) (2,3) (4,5) (6,7) (FDIGA_OZ_ORDER 1: 2, 4, 6, 7 planes); order 0 = (4,5) (6,7) (0,3) (1,2) and
-//      order 2 = (0,7) (1,6) (2,5) (3,4) (balanced MMA counts, 25 planes) measured 1 % and 8 % slower.
-//   2: two passes of four weights (all four slots per pass; the earlier kernel).
-// Measured at n = 256 (in-kernel clock64 timeline, tools/oz_trace.py): both schedules run at ~32 k cycles per tile
-// against 17.4 k cycles of MMAs (272 at the probe rate), 4 passes 1 % faster at n = 256 and 3 % at n = 384.  What
-// bounds a tile is the interference between the tensor pipe and the epilogue inside the SM, not the schedule:
-// under a saturated MMA stream a slot drain takes 4-7 k cycles instead of ~1 k alone (tcgen05.ld gets what the
-// MMAs' accumulator traffic leaves), and the tile's 128 KB of y stores take 6 k instead of 3 k cycles while they
-// in turn slow the MMAs (138 instead of ~80 cycles each: the stores and the MMAs' operand reads share the
-// L1 / shared-memory path).
+//   2 (default): two passes of four weights, pass 0 the weights 0..3 (data digits 0..3), pass 1 the weights 6, 5,
+//      7, 4 (digits 0..6): all four 128-column TMEM slots per pass, 11 data plane chunks per 64 k.
+//   4: four passes of two weights each.  The slots form two groups {0, 1} and {2, 3} used by alternating passes,
+//      so the epilogue drains a pass's two accumulators while the MMAs of the next pass fill the other group.
+//      Price: a pass streams the data digit planes its weights need again, 19 plane chunks per 64 k instead of 11.
+//      Pass order (0,1) (2,3) (4,5) (6,7) (FDIGA_OZ_ORDER 1: 2, 4, 6, 7 planes); order 0 = (4,5) (6,7) (0,3) (1,2)
+//      and order 2 = (0,7) (1,6) (2,5) (3,4) (balanced MMA counts, 25 planes) measured 1 % and 8 % slower.
+// Measured (in-kernel clock64 timeline, tools/oz_trace.py; tools/oz_ab.py, tools/oz_sustained.py): both schedules
+// run at ~32 k cycles per tile at n = 256 against 17.4 k cycles of MMAs (272 at the probe rate).  What bounds a
+// tile is the interference between the tensor pipe and the epilogue inside the SM, not the schedule: under a
+// saturated MMA stream a slot drain takes 4-7 k cycles instead of ~1 k alone (tcgen05.ld gets what the MMAs'
+// accumulator traffic leaves), and the tile's 128 KB of y stores take 6 k instead of 3 k cycles while they in
+// turn slow the MMAs (138 instead of ~80 cycles each: the stores and the MMAs' operand reads share the L1 /
+// shared-memory path).  From idle (burst) the two schedules are within 1 % at n = 256 (four passes 2.5 % ahead
+// at n = 384, two passes 2 % ahead at n = 512); under sustained load the path is limited by the board's 1000 W
+// power cap, and the schedule that moves less data wins: two passes 1.230 vs 1.253 ms per n = 256 apply (SM
+// clock 1732 vs 1702 MHz), 20.2 vs 20.6 ms at n = 512, equal at n = 384.  Hence the default.
 // Phase q = NPASS tile + pass; its k-th weight lives in slot (pass WPP + k) mod 4, used for the (q / NGRP)-th
 // time.  Within every 64-wide k chunk the MMAs go weight by weight, so a pass's slots complete one after
-// another in the last chunk.
+// another in the last chunk and the epilogue drains slot k while the remaining weights' MMAs run.
 #ifndef FDIGA_OZ_PDL_DEFAULT
 #define FDIGA_OZ_PDL_DEFAULT 2
 #endif
 #ifndef FDIGA_OZ_NPASS
-#define FDIGA_OZ_NPASS 4
+#define FDIGA_OZ_NPASS 2
 #endif
 #ifndef FDIGA_OZ_ORDER
 #define FDIGA_OZ_ORDER 1
@@ -559,6 +562,19 @@ __host__ __device__ constexpr int oz_nd(int P) {
   return nd;
 }
 __host__ __device__ constexpr int oz_slot(int P, int k) { return (P * OZ_WPP + k) % OZ_NSLOT; }
+// the schedule covers every weight exactly once, and a pass loads every data digit its weights pair with
+constexpr bool oz_schedule_ok() {
+  int seen = 0;
+  for (int P = 0; P < OZ_NPASS; ++P)
+    for (int k = 0; k < OZ_WPP; ++k) {
+      const int t = oz_weight(P, k);
+      if (t < 0 || t >= OZ_NW || (seen >> t & 1)) return false;
+      seen |= 1 << t;
+      if ((t < OZ_S - 1 ? t : OZ_S - 1) + 1 > oz_nd(P) || oz_nd(P) > OZ_S) return false;
+    }
+  return seen == (1 << OZ_NW) - 1;
+}
+static_assert(oz_schedule_ok(), "pass schedule");
 
 // the MMAs of weight T (slot sk) in one chunk: pairs (i, T - i), NKS K-steps of 32 each.  xd[i]: descriptor of
 // data digit i's plane chunk, fd: descriptor of factor digit 0's plane chunk (digit j is j planes further).
