@@ -21,6 +21,15 @@
  *     fd_setup*, colloc_assemble, stencil_create and gmres_solve synchronise before returning.
  *   - Multi-rank: every call is collective; all ranks call it in the same order with the
  *     same global arguments.
+ *   - Environment (read once per process; none changes results beyond rounding):
+ *       FDIGA_FD_OZ=0/1     force the FP64 DMMA / the int8-split tensor-core FD path for every plan that supports
+ *                           it (default rule: int8 for 3D real-spectrum plans with 192 <= n_l <= 512; fd_plan_set_path
+ *                           switches one plan)
+ *       FDIGA_OZ_PDL=k      programmatic dependent launch on the int8 path: bit 0 the digit splits, bit 1 the GEMMs
+ *                           (default 2)
+ *       FDIGA_NVTX=1        NVTX ranges per API call and per solve stage (fdiga:fd, fdiga:matvec, fdiga:orth, ...)
+ *       FDIGA_VERBOSE=1/2   set-up phase timings / autotuner results on stderr
+ *       FDIGA_GEMM_TABLE, FDIGA_GEMM_TABLE_OUT, FDIGA_GEMM_TUNE_ALWAYS   the DMMA tile table (fd_gemm.cu)
  */
 #ifndef FDIGA_H
 #define FDIGA_H
