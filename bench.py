@@ -594,6 +594,12 @@ def main():
     # the power-capped one)
     time.sleep(0.5)
     kern = fd_kernels(fd, plan, x, s)
+    if "split" in kern:  # the digit splits are HBM-bound: 8 N bytes read + 7 N written per launch
+        hb, hsrc = hbm_peak()
+        sb = 15.0 * N / ws
+        kern["split"].update({"bound": "hbm", "algorithmic_bytes_per_launch": sb,
+                              "achieved_gbs": sb / (kern["split"]["avg_ms"] * 1e-3) / 1e9, "peak_gbs": hb,
+                              "frac": sb / (kern["split"]["avg_ms"] * 1e-3) / 1e9 / hb, "peak_source": hsrc})
 
     # the same apply with IEEE FP64 dot products only (DMMA mode products, no int8 splitting)
     fp64_native = None

@@ -9,7 +9,8 @@
 //                       digit-pair weight t = i + j, two passes of four weights over the contraction); warps
 //                       0-15 read them back with tcgen05.ld, combine in FP64,
 //                       scale by the row exponents and store.  The factor's digit planes for the CTA's half of
-//                       the column tile stay resident in shared memory (contractions <= 256 per launch).
+//                       the column tile stay resident in shared memory for contractions <= 256; longer ones
+//                       (<= 512) stream them through the ring beside the data planes (oz_gemm_kernel<true>).
 //                       Outputs of "wide" rows (oz.cuh: guard) are then recomputed by the CTA that owns them
 //                       as IEEE FP64 dot products of the FP64 operands (oz_cta_fixup).
 #include <cuda.h>
@@ -353,6 +354,10 @@ constexpr int OZ_KCMAX = 4;                 // chunks per launch: contraction <=
 constexpr int OZ_XPL = OZ_BM * OZ_KCH;      // one data digit plane chunk per CTA: 128 rows x 64 B = 8 KB
 constexpr int OZ_FPL = OZ_BNH * OZ_KCH;     // one factor digit plane chunk per CTA: 64 rows x 64 B = 4 KB
 constexpr int OZ_NXS = 14;                  // data plane slots in the ring (two 7-plane chunks)
+// Streamed-factor variant (contractions 256 < K <= 512 in one launch): no resident factor; every ring slot holds
+// a data digit plane chunk (8 KB) and, behind it, the same digit's factor plane chunk (4 KB)
+constexpr int OZ_NXS_SF = 18;
+constexpr int OZ_SLOT_SF = OZ_BM * 64 + OZ_BNH * 64;  // = OZ_XPL + OZ_FPL (defined below): 12 KB
 constexpr int OZ_NCB = 8;                   // chunk barriers (full / empty pairs): more than the chunks in flight
 static_assert(OZ_EC * (OZ_EW / 4) == OZ_BN, "epilogue column groups cover the tile");
 
@@ -577,12 +582,12 @@ constexpr bool oz_schedule_ok() {
 static_assert(oz_schedule_ok(), "pass schedule");
 
 // the MMAs of weight T (slot sk) in one chunk: pairs (i, T - i), NKS K-steps of 32 each.  xd[i]: descriptor of
-// data digit i's plane chunk, fd: descriptor of factor digit 0's plane chunk (digit j is j planes further).
+// data digit i's plane chunk, fdv[j]: descriptor of factor digit j's plane chunk.
 // first: the weight's first MMA overwrites its slot.  One elected lane issues (operands computed by the
 // converged warp).
 template <int T>
-__device__ __forceinline__ void oz_weight_mmas(uint32_t td, const uint64_t (&xd)[OZ_S], uint64_t fd, bool first,
-                                               int nks) {
+__device__ __forceinline__ void oz_weight_mmas(uint32_t td, const uint64_t (&xd)[OZ_S], const uint64_t (&fdv)[OZ_S],
+                                               bool first, int nks) {
   constexpr int ilo = T > OZ_S - 1 ? T - (OZ_S - 1) : 0, ihi = T < OZ_S - 1 ? T : OZ_S - 1;
   if (elect_one()) {
     if (nks == 2) {
@@ -590,12 +595,12 @@ __device__ __forceinline__ void oz_weight_mmas(uint32_t td, const uint64_t (&xd)
       for (int i = ilo; i <= ihi; ++i)
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk)
-          mma_i8_pair(td, xd[i] + 2 * kk, fd + (uint64_t)((T - i) * (OZ_FPL >> 4) + 2 * kk),
+          mma_i8_pair(td, xd[i] + 2 * kk, fdv[T - i] + 2 * kk,
                       oz_idesc(i == 0, T - i == 0), (first && i == ilo && kk == 0) ? 0u : 1u);
     } else {
 #pragma unroll
       for (int i = ilo; i <= ihi; ++i)
-        mma_i8_pair(td, xd[i], fd + (uint64_t)((T - i) * (OZ_FPL >> 4)), oz_idesc(i == 0, T - i == 0),
+        mma_i8_pair(td, xd[i], fdv[T - i], oz_idesc(i == 0, T - i == 0),
                     (first && i == ilo) ? 0u : 1u);
     }
   }
@@ -607,9 +612,16 @@ __device__ __forceinline__ void oz_weight_mmas(uint32_t td, const uint64_t (&xd)
 // leader (rank 0) issues every MMA (M = 256, N = 128, K = 32); both CTAs keep their half of the factor digits
 // resident (<= 256 k) and stream their own data rows through a ring of 14 plane slots (64 k each) by TMA,
 // completion counted on the leader's barriers, and drain their own accumulators.
+// SF (streamed factor, contractions 256 < K <= 512 in one launch): no resident factor; ring slot i of a chunk
+// holds data digit i's plane chunk and, behind it, factor digit i's (the passes need the same digits of both).
+// One launch then runs one epilogue per tile over the whole contraction instead of two launches of half the
+// contraction each, the second re-reading and accumulating into y.
+template <bool SF>
 __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap fmap,
                    const __grid_constant__ OzKernelArgs a) {
+  constexpr int NXS = SF ? OZ_NXS_SF : OZ_NXS;              // ring slots
+  constexpr int SLOT = SF ? OZ_XPL + OZ_FPL : OZ_XPL;       // bytes per ring slot
   pdl_trigger();
   extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
   // (offset arithmetic on the shared array, not an integer round trip: derived pointers stay in the shared
@@ -617,12 +629,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
   uint8_t* smem = oz_smem_raw + ((1024u - (smem_u32(oz_smem_raw) & 1023u)) & 1023u);
   const int KC = a.KC;
   uint8_t* sF = smem;                                    // [KC][S] resident factor planes, this CTA's 64 rows
-  uint8_t* sX = smem + OZ_KCMAX * OZ_S * OZ_FPL;         // data ring [NXS] plane slots
+  uint8_t* sX = smem + (SF ? 0 : OZ_KCMAX * OZ_S * OZ_FPL);  // ring [NXS] of plane slots
   // One full / empty barrier pair per k chunk in flight (chunk number mod NCB): a chunk's nd planes occupy
   // consecutive ring slots, land on one transaction barrier and are released by one commit per MMA warp (a
   // barrier pair per plane cost each MMA warp nd commits per chunk, ~90 cycles each, as long as the MMAs of a
   // short chunk)
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + OZ_NXS * OZ_XPL);  // [NCB] (leader: both CTAs' bytes)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + NXS * SLOT);       // [NCB] (leader: both CTAs' bytes)
   uint64_t* empty = full + OZ_NCB;                                     // [NCB] (each CTA, multicast commit)
   uint64_t* fbar = empty + OZ_NCB;    // [KCMAX] factor chunk landed (leader)
   uint64_t* sfull = fbar + OZ_KCMAX;  // [4] accumulator slot complete (MMA -> epilogues of both CTAs)
@@ -684,13 +696,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
         for (int pass = 0; pass < OZ_NPASS; ++pass) {
           const uint32_t nd = oz_nd(pass);  // data digit planes of this pass
           for (int kc = 0; kc < KC; ++kc, ++n) {
-            if (n < (uint32_t)KC) {
+            if (!SF && n < (uint32_t)KC) {
               if (leader) mbar_arrive_expect_tx(&fbar[kc], (uint32_t)(2 * OZ_S * OZ_FPL));
               for (int s = 0; s < OZ_S; ++s)
                 tma_load_2sm(sF + (kc * OZ_S + s) * OZ_FPL, &fmap, a.kbase + kc * OZ_KCH,
                              (int)(s * a.f_rows_p + n0 + rank * OZ_BNH), fbar_l + 8u * (uint32_t)kc);
             }
-            while (occ + nd > OZ_NXS) {  // the chunks whose slots this one overwrites must be complete
+            while (occ + nd > NXS) {  // the chunks whose slots this one overwrites must be complete
               mbar_wait(&empty[tn % OZ_NCB], (tn / OZ_NCB) & 1);
               occ -= oz_nd(tpass);
               if (++tkc == KC) {
@@ -700,10 +712,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
               ++tn;
             }
             const uint32_t fb = mapa(&full[n % OZ_NCB], 0);
-            if (leader) mbar_arrive_expect_tx(&full[n % OZ_NCB], 2 * nd * OZ_XPL);
+            if (leader) mbar_arrive_expect_tx(&full[n % OZ_NCB], 2 * nd * SLOT);
             for (uint32_t i = 0; i < nd; ++i) {
-              tma_load_2sm(sX + pos * OZ_XPL, &xmap, a.kbase + kc * OZ_KCH, (int)(i * a.x_rows_p + m0), fb);
-              if (++pos == OZ_NXS) pos = 0;
+              tma_load_2sm(sX + pos * SLOT, &xmap, a.kbase + kc * OZ_KCH, (int)(i * a.x_rows_p + m0), fb);
+              if (SF)
+                tma_load_2sm(sX + pos * SLOT + OZ_XPL, &fmap, a.kbase + kc * OZ_KCH,
+                             (int)(i * a.f_rows_p + n0 + rank * OZ_BNH), fb);
+              if (++pos == NXS) pos = 0;
             }
             occ += nd;
           }
@@ -728,29 +743,31 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
             OZ_TR(kc <= 1, 16 + mw * 512 + q * 8 + 1 + 2 * kc, clock64());
             const bool first = kc == 0, last = kc == KC - 1;
             const int nks = last ? a.ks_last : OZ_KCH / 32;  // K-steps of 32 carrying real contraction indices
-            if (n < (uint32_t)KC) mbar_wait(&fbar[kc], 0);  // (first pass of the first tile: the factor chunk)
+            if (!SF && n < (uint32_t)KC) mbar_wait(&fbar[kc], 0);  // (first pass of the first tile: the factor chunk)
             mbar_wait(&full[n % OZ_NCB], (n / OZ_NCB) & 1);
             // this chunk's data planes: slots pos, pos + 1, .. (mod NXS)
-            uint64_t xd[OZ_S];
+            uint64_t xd[OZ_S], fdv[OZ_S];
 #pragma unroll
             for (int i = 0; i < OZ_S; ++i) {
               if (i < nd) {
-                xd[i] = sdesc_sw64(sx0 + pos * OZ_XPL);
-                if (++pos == OZ_NXS) pos = 0;
+                xd[i] = sdesc_sw64(sx0 + pos * SLOT);
+                fdv[i] = SF ? sdesc_sw64(sx0 + pos * SLOT + OZ_XPL)
+                            : fd0 + (uint64_t)((kc * OZ_S + i) * (OZ_FPL >> 4));
+                if (++pos == NXS) pos = 0;
               } else {
                 xd[i] = 0;
+                fdv[i] = 0;
               }
             }
             tc_fence_after();
             OZ_TR(kc <= 1, 16 + mw * 512 + q * 8 + 2 + 2 * kc, clock64());
-            const uint64_t fd = fd0 + (uint64_t)(kc * OZ_S * (OZ_FPL >> 4));
 #define OZ_WEIGHT(P, K)                                                                                \
   if (mw == (OZ_NPASS == 4 ? K : ((K == 0 || K == 3) ? 0 : 1))) {                                      \
     if (first && use > 0) { /* the slot's previous accumulator must be drained */                    \
       mbar_wait(&sempty[oz_slot(P, K)], (use - 1) & 1);                                                \
       tc_fence_after();                                                                                \
     }                                                                                                  \
-    oz_weight_mmas<oz_weight(P, K)>(tbase + (uint32_t)(oz_slot(P, K) * OZ_BN), xd, fd, first, nks);    \
+    oz_weight_mmas<oz_weight(P, K)>(tbase + (uint32_t)(oz_slot(P, K) * OZ_BN), xd, fdv, first, nks);   \
     if (last) tc_commit_pair(&sfull[oz_slot(P, K)]); /* weight complete */                             \
   }
             static_assert(OZ_S == 7 && OZ_NW == 8, "weight sequences written for 7 digits, 8 weights");
@@ -913,11 +930,12 @@ int get_encode(EncodeTiledFn* fn) {
   return FDIGA_OK;
 }
 
-constexpr size_t oz_smem_bytes() {
-  return 1024 + (size_t)OZ_KCMAX * OZ_S * OZ_FPL + (size_t)OZ_NXS * OZ_XPL + (2 * OZ_NCB + OZ_KCMAX + 2 * OZ_NSLOT + 2) * 8 +
-         OZ_BN * sizeof(double);
+constexpr size_t oz_smem_bytes(bool sf) {
+  return 1024 + (sf ? (size_t)OZ_NXS_SF * (OZ_XPL + OZ_FPL) : (size_t)OZ_KCMAX * OZ_S * OZ_FPL + (size_t)OZ_NXS * OZ_XPL) +
+         (2 * OZ_NCB + OZ_KCMAX + 2 * OZ_NSLOT + 2) * 8 + OZ_BN * sizeof(double);
 }
-static_assert(oz_smem_bytes() <= 227 * 1024, "shared memory per CTA");
+static_assert(oz_smem_bytes(false) <= 227 * 1024 && oz_smem_bytes(true) <= 227 * 1024, "shared memory per CTA");
+static_assert(OZ_SLOT_SF == OZ_XPL + OZ_FPL, "streamed-factor ring slot");
 static_assert((OZ_MAXKP + OZ_EW * OZ_BN) * sizeof(double) + OZ_EW * 32 * sizeof(int32_t) <= (size_t)OZ_NXS * OZ_XPL,
               "fixup scratch in the data ring");
 
@@ -1076,26 +1094,37 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   FDIGA_CHECK(g.xs && g.fs && F.ft, FDIGA_ERR_INVALID_ARG, "oz_gemm: FP64 operands for the wide-row fallback missing");
   const int npairs_max = ctx->sm_count / 2;
   FDIGA_CHECK(a.nt <= npairs_max, FDIGA_ERR_NOT_SUPPORTED, "oz_gemm: too many column tiles");
+  // contractions up to 256: the factor digits resident in shared memory; longer ones (<= 512): one launch of
+  // the streamed-factor kernel (FDIGA_OZ_SF=0: two resident-factor launches, the second accumulating into y)
+  static const bool sf_on = [] {
+    const char* e = std::getenv("FDIGA_OZ_SF");
+    return !(e && e[0] == '0');
+  }();
+  const bool sf = sf_on && g.K > OZ_KCMAX * OZ_KCH;
   static std::atomic<uint64_t> attr{0};
-  if (attr_once(attr, ctx->device))
-    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz_smem_bytes()));
+  if (attr_once(attr, ctx->device)) {
+    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)oz_smem_bytes(false)));
+    FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)oz_smem_bytes(true)));
+  }
   // persistent grid of CTA pairs (clusters of 2): a multiple of the column-tile count, one CTA per SM
   int64_t npairs = (int64_t)(npairs_max / a.nt) * a.nt;
   npairs = std::min<int64_t>(npairs, (int64_t)a.mt * a.nt);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(2 * npairs));
   cfg.blockDim = dim3(OZ_THREADS);
-  cfg.dynamicSmemBytes = oz_smem_bytes();
+  cfg.dynamicSmemBytes = oz_smem_bytes(sf);
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = (pdl_mode() & 2) ? 1 : 0;
-  auto kern = oz_gemm_kernel;
-  // contractions longer than 256 (the resident factor chunks): two launches, the second accumulating into y
-  for (int kbase = 0; kbase < g.K; kbase += OZ_KCMAX * OZ_KCH) {
-    const int klen = (int)std::min<int64_t>(g.K - kbase, OZ_KCMAX * OZ_KCH);
+  auto kern = sf ? oz_gemm_kernel<true> : oz_gemm_kernel<false>;
+  const int kmax = sf ? (int)g.K : OZ_KCMAX * OZ_KCH;  // contraction per launch
+  for (int kbase = 0; kbase < g.K; kbase += kmax) {
+    const int klen = (int)std::min<int64_t>(g.K - kbase, kmax);
     a.kbase = kbase;
     a.KC = (klen + OZ_KCH - 1) / OZ_KCH;
     a.ks_last = (klen - (a.KC - 1) * OZ_KCH + 31) / 32;  // K-steps of the last chunk below the contraction length
@@ -1105,7 +1134,7 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
                                              *reinterpret_cast<const CUtensorMap*>(F.tmap), a);
     if (e != cudaSuccess) {
       cudaFuncAttributes fa{};
-      cudaFuncGetAttributes(&fa, oz_gemm_kernel);
+      cudaFuncGetAttributes(&fa, kern);
       FDIGA_CHECK(false, FDIGA_ERR_CUDA, "oz_gemm launch: %s (grid %u, block %u, smem %zu; kernel: %d regs, max %d threads, "
                   "static smem %zu, max dyn smem %d)", cudaGetErrorString(e), cfg.gridDim.x, cfg.blockDim.x,
                   cfg.dynamicSmemBytes, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
