@@ -27,6 +27,8 @@
  *                           switches one plan)
  *       FDIGA_OZ_PDL=k      programmatic dependent launch on the int8 path: bit 0 the digit splits, bit 1 the GEMMs
  *                           (default 2)
+ *       FDIGA_OZ_SF=0/1/2   int8 GEMM with streamed factor digits: never (two launches for 256 < n_l <= 512) / for
+ *                           n_l > 256 (default) / always
  *       FDIGA_NVTX=1        NVTX ranges per API call and per solve stage (fdiga:fd, fdiga:matvec, fdiga:orth, ...)
  *       FDIGA_VERBOSE=1/2   set-up phase timings / autotuner results on stderr
  *       FDIGA_GEMM_TABLE, FDIGA_GEMM_TABLE_OUT, FDIGA_GEMM_TUNE_ALWAYS   the DMMA tile table (fd_gemm.cu)

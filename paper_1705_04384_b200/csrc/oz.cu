@@ -1096,11 +1096,11 @@ int oz_gemm(fdiga_ctx* ctx, cudaStream_t stream, const OzGemmArgs& g) {
   FDIGA_CHECK(a.nt <= npairs_max, FDIGA_ERR_NOT_SUPPORTED, "oz_gemm: too many column tiles");
   // contractions up to 256: the factor digits resident in shared memory; longer ones (<= 512): one launch of
   // the streamed-factor kernel (FDIGA_OZ_SF=0: two resident-factor launches, the second accumulating into y)
-  static const bool sf_on = [] {
+  static const int sf_mode = [] {
     const char* e = std::getenv("FDIGA_OZ_SF");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 1;
   }();
-  const bool sf = sf_on && g.K > OZ_KCMAX * OZ_KCH;
+  const bool sf = sf_mode == 2 || (sf_mode == 1 && g.K > OZ_KCMAX * OZ_KCH);  // (2: every contraction, for A/B runs)
   static std::atomic<uint64_t> attr{0};
   if (attr_once(attr, ctx->device)) {
     FDIGA_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
