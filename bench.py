@@ -86,6 +86,8 @@ def roofline(path, kern, flops, int8_ops, achieved_fp64, fp64_pk, traffic, ws):
                 "kernel": f"oz_gemm_kernel (tcgen05.mma.kind::i8, {g['launches_per_apply']} launches per apply, "
                           f"{100 * g['share']:.0f}% of the apply; the other steps under 'kernels')",
                 "int8_ops_per_apply": int8_ops, "avg_launch_ms": g["avg_ms"], "peak_source": src,
+                # context: our own back-to-back tcgen05.mma.kind::i8 issue loop (profiles/r01_tc_int8_mma_rate.txt)
+                "probe_peak": 4550.0, "frac_of_probe": ach / 4550.0,
                 "kernels": kern, "fp64_equivalent": fp64_eq}
     if kern and "dmma" in kern:
         g = kern["dmma"]
