@@ -148,12 +148,13 @@ ADVERSARIAL = {
 
 @pytest.mark.parametrize("kind", sorted(ADVERSARIAL))
 @pytest.mark.parametrize("l", [0, 1, 2])
-def test_guard_wide_fibres_meet_the_fp64_bound(ctx, l, kind):
+@pytest.mark.parametrize("nl", [256, 320])  # 320: the streamed-factor GEMM (contractions > 256 in one launch)
+def test_guard_wide_fibres_meet_the_fp64_bound(ctx, l, kind, nl):
     # intra-fibre dynamic range along each contracted axis: the guard sends those fibres to IEEE FP64 dot
     # products, so the int8 path meets the plain FP64 bound (B_fp64 of the library order) -- without the guard
     # the spike row's error is ~1e-5 relative (test_int8_split_scheme.py)
     rng = np.random.default_rng(10 + l)
-    f, x = _single_axis_problem(l, ADVERSARIAL[kind](rng, 256), seed=l, zero_col=(kind == "spike_vs_zero"))
+    f, x = _single_axis_problem(l, ADVERSARIAL[kind](rng, nl), seed=l, zero_col=(kind == "spike_vs_zero"))
     plan = fd.fd_setup_from_factors(ctx, f.U, f.W, f.lam)
     got = run(plan, x, "int8_split")
     check_bound(f, x, got, "dmma")
