@@ -21,8 +21,10 @@ constexpr int OZ_BM = 128;   // data rows per CTA (TMEM lanes); a CTA pair (cta_
 constexpr int OZ_PM = 256;   // data rows per pair tile (MMA M)
 constexpr int OZ_BN = 128;   // factor rows per pair tile (MMA N = TMEM columns per accumulator)
 constexpr int OZ_BNH = 64;   // factor rows per CTA (each CTA of the pair holds half of B)
-constexpr int OZ_BK = 128;   // bytes (= k) per TMA box row (SWIZZLE_128B)
-constexpr int OZ_MAXKP = 512;  // contraction lengths up to 512 (factor digits resident up to 256, streamed above)
+constexpr int OZ_BK = 128;   // the contraction length of an operand is padded to a multiple of this (zero digits);
+                             // the TMA boxes are 64 k wide (SWIZZLE_64B rows, oz.cu: OZ_KCH)
+constexpr int OZ_MAXKP = 512;  // contraction lengths up to 512 (factor digits resident up to 256, streamed beside the
+                               // data digits above: one launch either way)
 // Guard ("accuracy contract"): a row (data fibre or factor row) is "wide" when it holds a
 // non-finite value, a nonzero |x| < 2^(e - OZ_SPREAD) (its digits would keep fewer than 55 - OZ_SPREAD = 31
 // significant bits of that value), or its exponent is below OZ_EMIN (the digit scaling 2^(55 - e) would leave
