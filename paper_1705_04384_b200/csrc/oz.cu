@@ -148,7 +148,10 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
   pdl_wait();
   if (skip && *skip) return;
   const int lane = threadIdx.x & 31;
-  const int64_t m = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  // blocks run over the rows from the last to the first: the GEMM before this split wrote y in increasing row
+  // order and the GEMM after it reads the digits in increasing row order, so the split reads what was written
+  // last (still in L2) first and leaves the digits the next GEMM needs first for last
+  const int64_t m = (int64_t)(gridDim.x - 1 - blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (m >= rows) return;
   const double* xr = x + m * ldx;
   double v[NCH][8];
@@ -209,8 +212,9 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
   __shared__ int es[CW];
   const int col = threadIdx.x % CW, rg = threadIdx.x / CW;
   const int64_t tiles_i = (inner + CW - 1) / CW;
-  const int64_t b = blockIdx.x / tiles_i;
-  const int64_t i0 = (blockIdx.x - b * tiles_i) * CW;
+  const int64_t blk = (int64_t)gridDim.x - 1 - blockIdx.x;  // last tiles first (see oz_split_rows_kernel)
+  const int64_t b = blk / tiles_i;
+  const int64_t i0 = (blk - b * tiles_i) * CW;
   const bool iv = i0 + col < inner;
   // ---- stage the K x 16 tile: thread (col, rg) copies rows k = rg, rg + 16, .. of its column
   {
