@@ -177,9 +177,13 @@ __device__ __forceinline__ void dc_stream(const double* __restrict__ V, int64_t 
     fence_barrier_init();
   }
   __syncthreads();
+  // pass B walks the chunks from the last to the first: it follows pass A over the same (K + 2) vectors, whose
+  // last chunks are what is still in L2 (up to ~126 MB of the (K + 2) 8 N bytes); it has no reduction, so the
+  // order changes no result bit
+  auto chunk_of = [&](int64_t c) { return PASS == 1 ? nchunk - 1 - c : c; };
   auto issue = [&](int64_t c, int s) {
     const int lane = tid & 31;
-    const int64_t e0 = c * SC;
+    const int64_t e0 = chunk_of(c) * SC;
     const uint32_t bytes = (uint32_t)((ldv - e0 < SC ? ldv - e0 : SC) * 8);
     double* dst = dsm + (size_t)s * (K + 2) * SC;
     if (lane == 0) mbar_arrive_expect_tx(&full[s], ROWS * bytes);
@@ -198,7 +202,7 @@ __device__ __forceinline__ void dc_stream(const double* __restrict__ V, int64_t 
     const int s = it % S;
     mbar_wait(&full[s], (uint32_t)((it / S) & 1));
     const double* buf = dsm + (size_t)s * (K + 2) * SC;
-    const int64_t e = c * SC + tid;
+    const int64_t e = chunk_of(c) * SC + tid;
     if (e < N) {
       const double uv = buf[K * SC + tid];
       const double zv = EXTRA == 2 ? buf[(K + 1) * SC + tid] : 0.0;
